@@ -1,0 +1,146 @@
+/*
+ * starmm_b200.h -- C ABI of the B200-native semiring matrix-multiplication path.
+ *
+ * This is the drop-in boundary under the reference package's Python surface
+ * (starmm, /root/reference/pkg/src/starmm).  No C++ types, no torch types:
+ * plain device pointers, element strides and an opaque cudaStream_t passed
+ * as void*.  Every function returns an int status (0 = ok); no C++ exception
+ * crosses this boundary.  Status codes map 1:1 onto the reference exception
+ * classes (errors.py:4-41).
+ *
+ * Which reference interface each entry point replaces (file:line relative to
+ * /root/reference/pkg/src/starmm/):
+ *
+ *   starmm_plan_create   Executor.__init__(cfg) + Config (runtime.py:60-79,
+ *                        matrix.py:32-61): binds semiring, schedule, base_dim,
+ *                        workers and allocation mode; owns the block pool
+ *                        (pool.py:67-88) as a device scratch arena.
+ *   starmm_execute       registry.run_algorithm (registry.py:23-57) ->
+ *                        classic._classic_root (classic.py:241-265) for
+ *                        co2 / co3 / tar / sar / star: C <- C (+) A (x) B.
+ *   starmm_plan_stats    Pool.snapshot_counts (pool.py:158-167) +
+ *                        MetricsSnapshot (metrics.py:19-36) GPU analogues.
+ *   starmm_plan_reset_stats  Pool.reset (pool.py:148-156).
+ *   starmm_plan_destroy  Executor.close (runtime.py:83-93).
+ *   starmm_matmul        Semiring.matmul (semiring.py:92-94; numba kernels
+ *                        _mm_int / _mm_float / _mm_minplus, semiring.py:22-60):
+ *                        out <- A (x) B from the additive identity.
+ *   starmm_madd          kernels.madd (kernels.py:47-52) / Semiring.fold_add
+ *                        (semiring.py:96-98, 116-117, 126-127): C <- C (+) D.
+ *   starmm_atomic_accumulate  classic.atomic_accumulate (classic.py:268-284) /
+ *                        ops.accumulate_region (ops.py:76-101): concurrent-safe
+ *                        C <- C (+) P (hardware atomics / per-tile slots).
+ *   starmm_strerror      str(exception) for the status taxonomy.
+ *
+ * Matrices are row-major with a leading dimension in ELEMENTS (ld >= cols),
+ * like MatrixRegion.row_stride (matrix.py:144-146).  The caller owns A, B and
+ * C; the library reads A and B and updates C in place.  Calls are stream-
+ * ordered on `stream` and, like the reference entry points, block until the
+ * result is in C (STARMM_F_ASYNC opts out of the final synchronisation).
+ */
+#ifndef STARMM_B200_H_
+#define STARMM_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define STARMM_ABI_VERSION 1
+
+/* ---- status codes (errors.py:4-41) ------------------------------------- */
+enum starmm_status {
+    STARMM_OK = 0,
+    STARMM_DIM_MISMATCH = 1,          /* DimMismatch        errors.py:8  */
+    STARMM_INVALID_SPLIT = 2,         /* InvalidSplit       errors.py:12 */
+    STARMM_NOT_BASE_CASE = 3,         /* NotBaseCase        errors.py:16 */
+    STARMM_ALLOC_FAILURE = 4,         /* AllocFailure       errors.py:20 */
+    STARMM_CONTRACT_VIOLATION = 5,    /* ContractViolation  errors.py:24 */
+    STARMM_ALIGNMENT_ERROR = 6,       /* AlignmentError     errors.py:28 */
+    STARMM_NO_ADDITIVE_INVERSE = 7,   /* NoAdditiveInverse  errors.py:32 */
+    STARMM_TOO_LARGE = 8,             /* TooLarge           errors.py:36 */
+    STARMM_INTERNAL_ERROR = 9,        /* InternalError      errors.py:40 */
+    STARMM_CUDA_ERROR = 100           /* 100 + cudaError_t passthrough   */
+};
+
+/* ---- semiring ids (semiring.py:130-145 + this build's 32-bit ids) ------- */
+enum starmm_semiring {
+    STARMM_SR_INT64 = 0,          /* "int": int64 (+,x), wraps mod 2^64          */
+    STARMM_SR_FP64 = 1,           /* "float": float64 (+,x)                       */
+    STARMM_SR_TROPICAL_F64 = 2,   /* "tropical": float64 (min,+), zero = +inf     */
+    STARMM_SR_TROPICAL_F32 = 3,   /* "tropical_f32": float32 (min,+)              */
+    STARMM_SR_TROPICAL_I32 = 4    /* "tropical_i32": int32 (min,+), INT32_MAX=+inf */
+};
+
+/* ---- schedules (registry.py:11 CLASSICAL) ------------------------------ */
+enum starmm_algo {
+    STARMM_CO2 = 0, STARMM_CO3 = 1, STARMM_TAR = 2, STARMM_SAR = 3, STARMM_STAR = 4
+};
+
+/* ---- allocation modes (registry.py:20,32-33) ---------------------------- */
+enum starmm_alloc { STARMM_POOLED = 0, STARMM_RAW = 1 };
+
+/* ---- flags ------------------------------------------------------------- */
+#define STARMM_F_ASYNC          0x1  /* do not synchronise the stream at return        */
+#define STARMM_F_NO_FASTPATH    0x2  /* disable range-guarded exact narrow paths       */
+#define STARMM_F_INIT_IDENTITY  0x4  /* ignore incoming C: C <- A (x) B (k-split partials) */
+#define STARMM_F_ALLOW_NONPOW2  0x8  /* accept any n >= 1 (divergence from matrix.py:57-61) */
+
+typedef struct starmm_plan starmm_plan;
+
+typedef struct {
+    /* pool (pool.py:158-167) */
+    int64_t pool_total_allocated_bytes;
+    int64_t pool_high_water_bytes;
+    int64_t pool_fresh_count;
+    int64_t pool_reuse_count;
+    /* metrics (metrics.py:19-36) */
+    int64_t tile_serializations;     /* write-backs through a tile slot / atomic-madd */
+    int64_t pair_count;              /* SAR pair states created                       */
+    int64_t pair_transitions;        /* Empty->FirstRunning + FirstRunning->FirstDone */
+    int64_t lazy_temp_acquires;      /* SAR halves that found their sibling running   */
+    int64_t raw_alloc_count;
+    int64_t raw_alloc_bytes;
+    /* plan / launch description */
+    int64_t tasks;                   /* leaf tasks (output tile x k-slice) last run   */
+    int64_t workers;                 /* persistent CTAs (GPU workers)                 */
+    int64_t ksplit;                  /* k-slices per output tile                      */
+    int64_t tar_levels;              /* split levels run with the TAR protocol        */
+    int64_t kernel_launches;         /* launches issued by the last execute           */
+    int64_t path;                    /* kernel path id of the last execute */
+    int64_t executes;
+} starmm_stats;
+
+int  starmm_abi_version(void);
+const char* starmm_strerror(int status);
+
+/* n_rows x n_cols of C = m x n, inner dimension k.  The reference API is square
+ * (m = n = k, power of two >= base_dim, matrix.py:57-61); the plan accepts
+ * rectangles so the multi-GPU layer can run 2D output blocks and k-slices. */
+int  starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mode,
+                        int64_t m, int64_t n, int64_t k, int base_dim, int workers,
+                        int ksplit_log2 /* -1 = auto */, int device, int flags);
+int  starmm_execute(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,
+                    const void* B, int64_t ldb, void* stream);
+int  starmm_plan_stats(starmm_plan* plan, starmm_stats* out);
+int  starmm_plan_reset_stats(starmm_plan* plan);
+void starmm_plan_destroy(starmm_plan* plan);
+
+/* one-shot kernels */
+int  starmm_matmul(int semiring, void* out, int64_t ldo, const void* A, int64_t lda,
+                   const void* B, int64_t ldb, int64_t m, int64_t n, int64_t k,
+                   void* stream, int flags);
+int  starmm_madd(int semiring, void* C, int64_t ldc, const void* D, int64_t ldd,
+                 int64_t rows, int64_t cols, void* stream, int flags);
+int  starmm_atomic_accumulate(int semiring, void* C, int64_t ldc, const void* P, int64_t ldp,
+                              int64_t rows, int64_t cols, void* stream, int flags);
+
+/* device facts used by the Python layer for planning / reporting */
+int  starmm_device_sm_count(int device);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* STARMM_B200_H_ */

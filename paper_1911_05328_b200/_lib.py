@@ -1,0 +1,145 @@
+"""ctypes binding of libstarmm_b200.so (include/starmm_b200.h).
+
+The product path has no CPU fallback: if the shared library is missing or
+cannot be loaded, every entry point raises (StarMMError subclass
+``NativeUnavailable``).  Build it with ``python __graft_entry__.py`` or
+``make -C paper_1911_05328_b200/csrc``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from . import errors
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libstarmm_b200.so")
+
+# enums (include/starmm_b200.h)
+SR_INT64, SR_FP64, SR_TROPICAL_F64, SR_TROPICAL_F32, SR_TROPICAL_I32 = range(5)
+ALGO_IDS = {"co2": 0, "co3": 1, "tar": 2, "sar": 3, "star": 4}
+ALLOC_IDS = {"pooled": 0, "raw": 1}
+F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2 = 0x1, 0x2, 0x4, 0x8
+
+PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f32_fadd2_fmnmx3",
+              5: "simt_i32_via_f32_carrier", 6: "simt_i32_viaddmnmx", 7: "simt_i32_saturating",
+              8: "simt_f64_min"}
+
+
+class StarmmStats(ctypes.Structure):
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "pool_total_allocated_bytes", "pool_high_water_bytes", "pool_fresh_count",
+        "pool_reuse_count", "tile_serializations", "pair_count", "pair_transitions",
+        "lazy_temp_acquires", "raw_alloc_count", "raw_alloc_bytes", "tasks", "workers",
+        "ksplit", "tar_levels", "kernel_launches", "path", "executes")]
+
+    def to_dict(self):
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+_lib = None
+_lock = threading.Lock()
+
+# status -> exception class (errors.py:4-41)
+_STATUS_EXC = {
+    1: errors.DimMismatch, 2: errors.InvalidSplit, 3: errors.NotBaseCase,
+    4: errors.AllocFailure, 5: errors.ContractViolation, 6: errors.AlignmentError,
+    7: errors.NoAdditiveInverse, 8: errors.TooLarge, 9: errors.InternalError,
+}
+
+
+def lib():
+    """Load the native library (once).  Raises NativeUnavailable if absent."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise errors.NativeUnavailable(
+                f"{LIB_PATH} is not built; run `make -C {os.path.join(_HERE, 'csrc')}` "
+                "(there is no CPU fallback)")
+        try:
+            L = ctypes.CDLL(LIB_PATH)
+        except OSError as e:
+            raise errors.NativeUnavailable(f"cannot load {LIB_PATH}: {e}") from e
+        i64, vp, ci = ctypes.c_int64, ctypes.c_void_p, ctypes.c_int
+        L.starmm_abi_version.restype = ci
+        L.starmm_strerror.restype = ctypes.c_char_p
+        L.starmm_strerror.argtypes = [ci]
+        L.starmm_device_sm_count.argtypes = [ci]
+        L.starmm_device_sm_count.restype = ci
+        L.starmm_plan_create.argtypes = [ctypes.POINTER(vp), ci, ci, ci, i64, i64, i64, ci, ci,
+                                         ci, ci, ci]
+        L.starmm_plan_create.restype = ci
+        L.starmm_execute.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp]
+        L.starmm_execute.restype = ci
+        L.starmm_plan_stats.argtypes = [vp, ctypes.POINTER(StarmmStats)]
+        L.starmm_plan_stats.restype = ci
+        L.starmm_plan_reset_stats.argtypes = [vp]
+        L.starmm_plan_reset_stats.restype = ci
+        L.starmm_plan_destroy.argtypes = [vp]
+        L.starmm_plan_destroy.restype = None
+        L.starmm_matmul.argtypes = [ci, vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, ci]
+        L.starmm_matmul.restype = ci
+        L.starmm_madd.argtypes = [ci, vp, i64, vp, i64, i64, i64, vp, ci]
+        L.starmm_madd.restype = ci
+        L.starmm_atomic_accumulate.argtypes = [ci, vp, i64, vp, i64, i64, i64, vp, ci]
+        L.starmm_atomic_accumulate.restype = ci
+        if L.starmm_abi_version() != 1:
+            raise errors.NativeUnavailable("libstarmm_b200.so ABI version mismatch")
+        _lib = L
+    return _lib
+
+
+def check(status: int, what: str = "") -> None:
+    """Raise the reference exception class matching a C-ABI status."""
+    if status == 0:
+        return
+    msg = lib().starmm_strerror(status).decode()
+    if what:
+        msg = f"{what}: {msg}"
+    if status >= 100:
+        raise errors.CudaError(msg)
+    raise _STATUS_EXC.get(status, errors.InternalError)(msg)
+
+
+class Plan:
+    """Owns one starmm_plan (Executor + Config analogue for one problem shape)."""
+
+    def __init__(self, sr: int, algo: str, mode: str, m: int, n: int, k: int, base_dim: int,
+                 workers: int, ksplit_log2: int, device: int, flags: int):
+        self._h = ctypes.c_void_p()
+        check(lib().starmm_plan_create(ctypes.byref(self._h), sr, ALGO_IDS[algo], ALLOC_IDS[mode],
+                                       m, n, k, base_dim, workers, ksplit_log2, device, flags),
+              "starmm_plan_create")
+        self.sr, self.algo, self.mode = sr, algo, mode
+        self.m, self.n, self.k, self.device, self.flags = m, n, k, device, flags
+
+    def execute(self, C_ptr: int, ldc: int, A_ptr: int, lda: int, B_ptr: int, ldb: int,
+                stream: int) -> None:
+        check(lib().starmm_execute(self._h, C_ptr, ldc, A_ptr, lda, B_ptr, ldb, stream),
+              "starmm_execute")
+
+    def stats(self) -> dict:
+        st = StarmmStats()
+        check(lib().starmm_plan_stats(self._h, ctypes.byref(st)), "starmm_plan_stats")
+        d = st.to_dict()
+        d["path_name"] = PATH_NAMES.get(d["path"], "none")
+        return d
+
+    def reset_stats(self) -> None:
+        check(lib().starmm_plan_reset_stats(self._h), "starmm_plan_reset_stats")
+
+    def close(self) -> None:
+        if self._h:
+            lib().starmm_plan_destroy(self._h)
+            self._h = ctypes.c_void_p()
+
+    def __del__(self):  # pragma: no cover - best effort
+        try:
+            self.close()
+        except Exception:
+            pass

@@ -1,0 +1,131 @@
+// aux_kernels.cuh -- HBM-bound helpers around the tile products:
+//   range_*      range guards for the exact narrow fast paths (one pass, O(n^2))
+//   pack_*       panel packing into the k-group-major layout of simt_kernel.cuh
+//   pad_copy     zero-padded copy for the DMMA path when n is not tile aligned
+//   fill         C <- identity (INIT_IDENTITY with split-k protocols)
+//   madd / red   C <- C (+) D elementwise (kernels.madd, kernels.py:47-52; CO3
+//                merge_tasks, ops.py:108-155) and its atomic variant
+//                (accumulate_region, ops.py:76-101)
+#pragma once
+#include "common.cuh"
+
+namespace starmm {
+
+// ---- range guard -----------------------------------------------------------
+// out[0] = max |x| over the operand (finite entries only for tropical_i32),
+// as an unsigned 64-bit magnitude; reduced with atomicMax.
+template <class T>
+__global__ void range_absmax_kernel(const T* X, long long rows, long long cols, long long ld,
+                                    unsigned long long* out, int skip_i32_inf) {
+    unsigned long long m = 0;
+    long long total = rows * cols;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cols, c = idx - r * cols;
+        T v = X[r * ld + c];
+        if (skip_i32_inf && (long long)v == 0x7fffffffLL) continue;
+        long long sv = (long long)v;
+        unsigned long long a = sv < 0 ? (unsigned long long)(-(sv + 1)) + 1ull : (unsigned long long)sv;
+        m = a > m ? a : m;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+    }
+    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+// ---- packing ---------------------------------------------------------------
+// Element conversion into the packed domain, with the pad value (annihilator
+// of the product, so padded k terms contribute the additive identity).
+struct ConvIdentity {   // same type
+    template <class T> static STARMM_DEV T cvt(T x) { return x; }
+};
+struct ConvI32ToF32 {   // int32 tropical -> fp32 carrier, INT32_MAX -> +inf
+    static STARMM_DEV float cvt(int x) {
+        return x == 0x7fffffff ? __int_as_float(0x7f800000) : (float)x;
+    }
+};
+struct ConvI32Vmin {    // int32 tropical -> VIADDMNMX encoding, INT32_MAX -> 2^30 - 1
+    static STARMM_DEV int cvt(int x) { return x == 0x7fffffff ? (1 << 30) - 1 : x; }
+};
+struct ConvI64ToI32 {   // int64 ring, range-guarded narrow path
+    static STARMM_DEV int cvt(long long x) { return (int)x; }
+};
+
+// A (rows x kdim, ld) -> P[kp/G][rowsp][G], transposing through a 32x32 smem tile
+// so that both the global reads and the packed writes are coalesced.
+template <class Tin, class Tp, int G, class Conv>
+__global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long long lda,
+                              Tp* P, long long rowsp, long long kp, Tp pad) {
+    __shared__ Tp tile[32][33];
+    long long r0 = (long long)blockIdx.y * 32, k0 = (long long)blockIdx.x * 32;
+    int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        long long r = r0 + i, k = k0 + tx;
+        tile[i][tx] = (r < rows && k < kdim) ? (Tp)Conv::cvt(A[r * lda + k]) : pad;
+    }
+    __syncthreads();
+    // write: packed index for (k, r): ((k/G) * rowsp + r) * G + k%G
+    for (int i = ty; i < 32; i += 8) {
+        long long k = k0 + i;
+        long long r = r0 + tx;
+        if (k < kp && r < rowsp) P[((k / G) * rowsp + r) * G + (k % G)] = tile[tx][i];
+    }
+}
+
+// B (kdim x cols, ld) -> P[kp/G][colsp][G]
+template <class Tin, class Tp, int G, class Conv>
+__global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long long ldb,
+                              Tp* P, long long colsp, long long kp, Tp pad) {
+    long long total = (kp / G) * colsp;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long kg = idx / colsp, c = idx - kg * colsp;
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+            long long k = kg * G + g;
+            P[idx * G + g] = (k < kdim && c < cols) ? (Tp)Conv::cvt(B[k * ldb + c]) : pad;
+        }
+    }
+}
+
+// Zero-padded copy (DMMA path): dst[rp x cp] from src[rows x cols, ld].
+template <class T>
+__global__ void pad_copy_kernel(const T* src, long long rows, long long cols, long long ld,
+                                T* dst, long long rp, long long cp) {
+    long long total = rp * cp;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cp, c = idx - r * cp;
+        dst[idx] = (r < rows && c < cols) ? src[r * ld + c] : (T)0;
+    }
+}
+
+template <class Sr>
+__global__ void fill_kernel(typename Sr::T* C, long long rows, long long cols, long long ld) {
+    long long total = rows * cols;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cols, c = idx - r * cols;
+        C[r * ld + c] = Sr::identity();
+    }
+}
+
+// C <- C (+) D.  atomic = 1 merges with the semiring's atomic-madd.
+template <class Sr>
+__global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr::T* D, long long ldd,
+                            long long rows, long long cols, int atomic) {
+    long long total = rows * cols;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cols, c = idx - r * cols;
+        typename Sr::T d = D[r * ldd + c];
+        typename Sr::T* p = &C[r * ldc + c];
+        if (atomic) Sr::atomic_fold(p, d);
+        else *p = Sr::fold(*p, d);
+    }
+}
+
+}  // namespace starmm

@@ -1,0 +1,236 @@
+// simt_kernel.cuh -- CUDA-core semiring tile product for the semirings with
+// no tensor-core path: (min,+) over fp32 / int32 / fp64 and exact int64 (+,x).
+//
+// Replaces the reference's numba kernels _mm_minplus / _mm_int
+// (semiring.py:22-32, 48-60).  One kernel template, specialised by an inner
+// "term" policy:
+//
+//   PolF32Pair   fp32 (min,+) on k-PAIRS: FADD2 (packed add of two k terms)
+//                + FMNMX3 (3-input min)  -> 1 issue slot per inner term.
+//                Also the exact carrier for int32 (min,+) when every finite
+//                |x| <= 2^23 (range guard): sums stay exact in fp32.
+//   PolI32Vmin   int32 (min,+): VIADDMNMX (min(a+b, c) in one DPX op); finite
+//                |x| < 2^28 with +inf encoded as 2^30-1 (no overflow possible).
+//   PolI32Sat    int32 (min,+) general: saturating semantics of the oracle.
+//   PolF64Min    fp64 (min,+) (the reference's own "tropical"): DADD + DMNMX.
+//   PolI64       int64 (+,x) mod 2^64: IMAD.WIDE + IMAD + IADD3 (4 SASS/term).
+//   PolI64Narrow int64 (+,x) when K*max|a|*max|b| < 2^31 (range guard): IMAD
+//                on int32 accumulators, sign-extended in the epilogue -- exact.
+//
+// Operands come from PACKED panels (aux_kernels.cuh pack_*): A and B are both
+// laid out k-group-major, P[k/G][x][G] (x = m for A, n for B; G = 2 for the
+// paired policy, else 1), padded to the tile grid with the product's
+// annihilator, so a k-stage is a contiguous slab that 16-byte cp.async copies
+// verbatim and every thread reads its operands with conflict-free LDS.128.
+//
+// CTA tile 128x128, 256 threads, 8x8 outputs per thread, k-stage 16, 3-deep
+// cp.async ring.  Warps are 4 (rows) x 8 (cols) threads so A reads broadcast
+// across 8 lanes and B reads across 4.
+#pragma once
+#include "common.cuh"
+#include "writeback.cuh"
+#include "dmma_kernel.cuh"   // cp.async helpers
+
+namespace starmm {
+
+// ---- inner term policies ---------------------------------------------------
+struct PolF32Pair {        // packed element float, G = 2, accumulator float
+    using Tp = float; using Acc = float;
+    static constexpr int G = 2;
+    static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
+    // a = (A[i][k], A[i][k+1]), b = (B[k][j], B[k+1][j])
+    static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
+        float2 v = __fadd2_rn(a, b);
+        c = fminf(fminf(c, v.x), v.y);
+    }
+};
+struct PolF64Min {
+    using Tp = double; using Acc = double;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return __longlong_as_double(0x7ff0000000000000ULL); }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fmin(c, a + b); }
+};
+struct PolI32Vmin {
+    using Tp = int; using Acc = int;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return 0x7fffffff; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s32(a, b, c); }
+};
+struct PolI32Sat {
+    using Tp = int; using Acc = int;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return 0x7fffffff; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
+        long long s = (long long)a + (long long)b;
+        s = (a == 0x7fffffff || b == 0x7fffffff) ? 0x7fffffffLL : s;
+        s = s > 0x7fffffffLL ? 0x7fffffffLL : (s < -0x80000000LL ? -0x80000000LL : s);
+        c = min(c, (int)s);
+    }
+};
+struct PolI64 {
+    using Tp = long long; using Acc = unsigned long long;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return 0ull; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
+        c += (unsigned long long)a * (unsigned long long)b;
+    }
+};
+struct PolI64Narrow {
+    using Tp = int; using Acc = int;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return 0; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c += a * b; }
+};
+
+// Accumulator -> output element conversion per (policy, output semiring).
+template <class Pol, class Sr> struct Finish;
+template <> struct Finish<PolF32Pair, SrTropF32> {
+    static STARMM_DEV float out(float v) { return v; }
+};
+template <> struct Finish<PolF32Pair, SrTropI32> {   // fp32 carrier -> int32, +inf -> INT32_MAX
+    static STARMM_DEV int out(float v) { return v == __int_as_float(0x7f800000) ? 0x7fffffff : (int)v; }
+};
+template <> struct Finish<PolF64Min, SrTropF64> {
+    static STARMM_DEV double out(double v) { return v; }
+};
+template <> struct Finish<PolI32Vmin, SrTropI32> {  // encoded sums >= 2^29 involve +inf
+    static STARMM_DEV int out(int v) { return v >= (1 << 29) ? 0x7fffffff : v; }
+};
+template <> struct Finish<PolI32Sat, SrTropI32> {
+    static STARMM_DEV int out(int v) { return v; }
+};
+template <> struct Finish<PolI64, SrInt64> {
+    static STARMM_DEV long long out(unsigned long long v) { return (long long)v; }
+};
+template <> struct Finish<PolI64Narrow, SrInt64> {
+    static STARMM_DEV long long out(int v) { return (long long)v; }
+};
+
+namespace simt {
+constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, THREADS = 256;
+template <class Pol>
+constexpr int smem_bytes() { return STAGES * (BM + BN) * BK * (int)sizeof(typename Pol::Tp) + 64; }
+}  // namespace simt
+
+struct SimtParams {
+    const void* Ap;   // packed [Kp/G][Mp][G]
+    const void* Bp;   // packed [Kp/G][Np][G]
+    long long Mp, Np; // padded extents (multiples of 128)
+    TaskGrid g;
+    WbParams w;
+};
+
+template <class Pol, class Sr>
+__global__ void __launch_bounds__(simt::THREADS, 1) simt_mm_kernel(SimtParams p) {
+    using namespace simt;
+    using Tp = typename Pol::Tp;
+    using Acc = typename Pol::Acc;
+    constexpr int G = Pol::G;
+    constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // x-positions per 16-byte load
+    constexpr int NQ = 8 / VEC;                         // 16-byte loads per operand per k-group
+    constexpr int KG = BK / G;                          // k-groups per stage
+    constexpr int A_STAGE = KG * BM * G;                // elements
+    constexpr int B_STAGE = KG * BN * G;
+    constexpr int CHUNK = 16 / (int)sizeof(Tp);         // elements per cp.async
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    Tp* As = reinterpret_cast<Tp*>(smem_raw);
+    Tp* Bs = As + STAGES * A_STAGE;
+    int* smem_word = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int ty = (warp >> 1) * 4 + (lane >> 3);      // 0..15
+    const int tx = (warp & 1) * 8 + (lane & 7);        // 0..15
+    const TaskGrid& g = p.g;
+    const int nk = (int)(g.kslice / BK);
+    const Tp* Ap = reinterpret_cast<const Tp*>(p.Ap);
+    const Tp* Bp = reinterpret_cast<const Tp*>(p.Bp);
+
+    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
+        int tm, tn, s, tile;
+        decode_task(g, t, tm, tn, s, tile);
+        const int mode = task_mode(p.w, g, s);
+        int pair_seen = PAIR_EMPTY;
+        if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
+
+        // k-group row kg of A covers Mp*G contiguous elements
+        const long long kg0 = (long long)s * g.kslice / G;
+        const Tp* Ag = Ap + kg0 * p.Mp * G + (long long)tm * BM * G;
+        const Tp* Bg = Bp + kg0 * p.Np * G + (long long)tn * BN * G;
+
+        auto load_stage = [&](int kt, int stage) {
+            const long long kgs = (long long)kt * KG;
+            Tp* as = As + stage * A_STAGE;
+            Tp* bs = Bs + stage * B_STAGE;
+            constexpr int ROW_CHUNKS = BM * G / CHUNK;
+            constexpr int TOTAL = KG * ROW_CHUNKS;
+#pragma unroll
+            for (int i = 0; i < TOTAL / THREADS; ++i) {
+                int c = tid + i * THREADS;
+                int r = c / ROW_CHUNKS, q = c % ROW_CHUNKS;
+                cp_async16(as + r * BM * G + q * CHUNK, Ag + (kgs + r) * p.Mp * G + q * CHUNK);
+                cp_async16(bs + r * BN * G + q * CHUNK, Bg + (kgs + r) * p.Np * G + q * CHUNK);
+            }
+        };
+
+        Acc acc[8][8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+            for (int j = 0; j < 8; ++j) acc[i][j] = Pol::init();
+
+#pragma unroll
+        for (int st = 0; st < STAGES - 1; ++st) {
+            if (st < nk) load_stage(st, st);
+            cp_async_commit();
+        }
+        for (int kt = 0; kt < nk; ++kt) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            int nxt = kt + STAGES - 1;
+            if (nxt < nk) load_stage(nxt, nxt % STAGES);
+            cp_async_commit();
+            const Tp* as = As + (kt % STAGES) * A_STAGE + ty * VEC * G;
+            const Tp* bs = Bs + (kt % STAGES) * B_STAGE + tx * VEC * G;
+#pragma unroll
+            for (int kg = 0; kg < KG; ++kg) {
+                // 8 row operands / 8 column operands, each G elements wide
+                Tp a[8 * G], b[8 * G];
+#pragma unroll
+                for (int q = 0; q < NQ; ++q) {
+                    *reinterpret_cast<int4*>(&a[q * VEC * G]) =
+                        *reinterpret_cast<const int4*>(as + kg * BM * G + q * 16 * VEC * G);
+                    *reinterpret_cast<int4*>(&b[q * VEC * G]) =
+                        *reinterpret_cast<const int4*>(bs + kg * BN * G + q * 16 * VEC * G);
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i)
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        if constexpr (G == 2) {
+                            Pol::term2(acc[i][j], make_float2(a[2 * i], a[2 * i + 1]),
+                                       make_float2(b[2 * j], b[2 * j + 1]));
+                        } else {
+                            Pol::term(acc[i][j], a[i], b[j]);
+                        }
+                    }
+            }
+        }
+        cp_async_wait<0>();
+        __syncthreads();
+
+        using T = typename Sr::T;
+        writeback<Sr, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
+                              [&](auto f) {
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    int r = (i / VEC) * 16 * VEC + ty * VEC + (i % VEC);
+                    int c = (j / VEC) * 16 * VEC + tx * VEC + (j % VEC);
+                    f(r, c, (T)Finish<Pol, Sr>::out(acc[i][j]));
+                }
+        });
+    }
+}
+
+}  // namespace starmm

@@ -1,0 +1,625 @@
+// starmm_api.cu -- the C ABI of include/starmm_b200.h: plans, the device
+// scratch arena (the LIFO block pool), path selection and launches.
+//
+// Reference mapping (relative to /root/reference/pkg/src/starmm/):
+//   plan create/destroy ....... Executor(cfg) lifecycle (runtime.py:57-98)
+//   execute validation ........ registry.run_algorithm (registry.py:23-57)
+//   schedule dispatch ......... classic._classic_root (classic.py:241-265)
+//   switch depth .............. classic.switch_depth (classic.py:78-83)
+//   arena (pooled/raw temps) .. Executor.acquire_temp/release_temp (runtime.py:198-229)
+//                               and Pool (pool.py:67-167): exact-size LIFO stacks,
+//                               blocks never cleared, fresh/reuse/high-water counters
+//   co3 merge ................. ops.merge_tasks (ops.py:108-155)
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <vector>
+#include <algorithm>
+#include <cmath>
+#include <limits>
+
+#include "../../include/starmm_b200.h"
+#include "common.cuh"
+#include "writeback.cuh"
+#include "dmma_kernel.cuh"
+#include "simt_kernel.cuh"
+#include "aux_kernels.cuh"
+
+using namespace starmm;
+
+namespace {
+
+thread_local int g_last_cuda_error = 0;
+
+int cuda_status(cudaError_t e) {
+    if (e == cudaSuccess) return STARMM_OK;
+    g_last_cuda_error = (int)e;
+    if (e == cudaErrorMemoryAllocation) { cudaGetLastError(); return STARMM_ALLOC_FAILURE; }
+    return STARMM_CUDA_ERROR + (int)e;
+}
+
+#define CK(x) do { cudaError_t _e = (x); if (_e != cudaSuccess) return cuda_status(_e); } while (0)
+#define TRY(x) do { int _s = (x); if (_s != STARMM_OK) return _s; } while (0)
+
+bool is_pow2(long long x) { return x >= 1 && (x & (x - 1)) == 0; }
+long long round_up(long long x, long long m) { return (x + m - 1) / m * m; }
+
+int elem_bytes(int sr) {
+    return (sr == STARMM_SR_TROPICAL_F32 || sr == STARMM_SR_TROPICAL_I32) ? 4 : 8;
+}
+
+// classic.py:78-83: smallest k with 4**k >= p
+int switch_depth(int p) {
+    int k = 0;
+    long long q = 1;
+    while (q < p) { q *= 4; ++k; }
+    return k;
+}
+
+// ---- the arena: exact-size LIFO free stacks (pool.py:89-132) -----------------
+struct Arena {
+    std::map<size_t, std::vector<void*>> free_stacks;
+    std::vector<std::pair<void*, size_t>> owned;
+    long long total_allocated = 0, issued = 0, high_water = 0, fresh = 0, reuse = 0;
+
+    int acquire(size_t bytes, void** out, bool count_as_temp, long long* fresh_ctr,
+                long long* reuse_ctr) {
+        bytes = (size_t)round_up((long long)std::max<size_t>(bytes, 256), 256);
+        auto& st = free_stacks[bytes];
+        if (!st.empty()) {
+            *out = st.back();             // LIFO pop (pool.py:97)
+            st.pop_back();
+            if (count_as_temp) ++*reuse_ctr;
+        } else {
+            void* p = nullptr;
+            cudaError_t e = cudaMalloc(&p, bytes);
+            if (e != cudaSuccess) return cuda_status(e);
+            owned.push_back({p, bytes});
+            total_allocated += (long long)bytes;
+            *out = p;
+            if (count_as_temp) ++*fresh_ctr;
+        }
+        issued += (long long)bytes;
+        high_water = std::max(high_water, issued);
+        return STARMM_OK;
+    }
+    void release(void* p, size_t bytes) {
+        bytes = (size_t)round_up((long long)std::max<size_t>(bytes, 256), 256);
+        free_stacks[bytes].push_back(p);  // blocks are not cleared (pool.py:4-6)
+        issued -= (long long)bytes;
+    }
+    void destroy() {
+        for (auto& o : owned) cudaFree(o.first);
+        owned.clear();
+        free_stacks.clear();
+    }
+};
+
+struct Block { void* p = nullptr; size_t bytes = 0; };
+
+}  // namespace
+
+struct starmm_plan {
+    int sr, algo, alloc, base_dim, workers, ksplit_req, device, flags;
+    long long m, n, k;
+    int sms = 0;
+    Arena arena;
+    // persistent device bookkeeping (from the arena, kept for the plan's life)
+    unsigned long long* d_counters = nullptr;   // CNT__N
+    unsigned long long* d_range = nullptr;      // 2 words
+    unsigned* d_worker_used = nullptr;          // per persistent worker
+    int max_workers = 0;
+    starmm_stats st;
+    long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
+    long long raw_count = 0, raw_bytes = 0;
+};
+
+namespace {
+
+// ---- kernel instantiation table ----------------------------------------------
+enum PathId : int {
+    PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
+    PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8
+};
+
+template <class Pol, class Sr>
+int launch_simt(const SimtParams& p, int grid, cudaStream_t s) {
+    auto kern = simt_mm_kernel<Pol, Sr>;
+    constexpr int smem = simt::smem_bytes<Pol>();
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+        attr_done = true;
+    }
+    kern<<<grid, simt::THREADS, smem, s>>>(p);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(dmma_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                dmma::SMEM_BYTES));
+        attr_done = true;
+    }
+    dmma_fp64_kernel<<<grid, dmma::THREADS, dmma::SMEM_BYTES, s>>>(p);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+int grid_blocks(long long n) { return (int)std::min<long long>((n + 255) / 256, 148LL * 16); }
+
+template <class Sr>
+int launch_madd(void* C, long long ldc, const void* D, long long ldd, long long rows, long long cols,
+                int atomic, cudaStream_t s) {
+    if (rows <= 0 || cols <= 0) return STARMM_OK;
+    using T = typename Sr::T;
+    madd_kernel<Sr><<<grid_blocks(rows * cols), 256, 0, s>>>((T*)C, ldc, (const T*)D, ldd, rows, cols,
+                                                           atomic);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+int madd_dispatch(int sr, void* C, long long ldc, const void* D, long long ldd, long long rows,
+                  long long cols, int atomic, cudaStream_t s) {
+    switch (sr) {
+    case STARMM_SR_INT64: return launch_madd<SrInt64>(C, ldc, D, ldd, rows, cols, atomic, s);
+    case STARMM_SR_FP64: return launch_madd<SrFp64>(C, ldc, D, ldd, rows, cols, atomic, s);
+    case STARMM_SR_TROPICAL_F64: return launch_madd<SrTropF64>(C, ldc, D, ldd, rows, cols, atomic, s);
+    case STARMM_SR_TROPICAL_F32: return launch_madd<SrTropF32>(C, ldc, D, ldd, rows, cols, atomic, s);
+    case STARMM_SR_TROPICAL_I32: return launch_madd<SrTropI32>(C, ldc, D, ldd, rows, cols, atomic, s);
+    }
+    return STARMM_CONTRACT_VIOLATION;
+}
+
+template <class Sr>
+int launch_fill(void* C, long long rows, long long cols, long long ld, cudaStream_t s) {
+    fill_kernel<Sr><<<grid_blocks(rows * cols), 256, 0, s>>>((typename Sr::T*)C, rows, cols, ld);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+int fill_dispatch(int sr, void* C, long long rows, long long cols, long long ld, cudaStream_t s) {
+    switch (sr) {
+    case STARMM_SR_INT64: return launch_fill<SrInt64>(C, rows, cols, ld, s);
+    case STARMM_SR_FP64: return launch_fill<SrFp64>(C, rows, cols, ld, s);
+    case STARMM_SR_TROPICAL_F64: return launch_fill<SrTropF64>(C, rows, cols, ld, s);
+    case STARMM_SR_TROPICAL_F32: return launch_fill<SrTropF32>(C, rows, cols, ld, s);
+    case STARMM_SR_TROPICAL_I32: return launch_fill<SrTropI32>(C, rows, cols, ld, s);
+    }
+    return STARMM_CONTRACT_VIOLATION;
+}
+
+template <class Tin, class Tp, int G, class Conv>
+int launch_pack(const void* A, long long lda, const void* B, long long ldb, long long m,
+                long long n, long long k, void* Ap, void* Bp, long long Mp, long long Np,
+                long long Kp, Tp pad, cudaStream_t s) {
+    dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
+    pack_a_kernel<Tin, Tp, G, Conv><<<ga, dim3(32, 8), 0, s>>>((const Tin*)A, m, k, lda, (Tp*)Ap, Mp,
+                                                              Kp, pad);
+    CK(cudaGetLastError());
+    pack_b_kernel<Tin, Tp, G, Conv><<<grid_blocks((Kp / G) * Np), 256, 0, s>>>(
+        (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+int occupancy_grid(starmm_plan* P, int per_sm, long long tasks) {
+    long long g = (long long)P->sms * per_sm;
+    return (int)std::max<long long>(1, std::min<long long>(g, tasks));
+}
+
+// max |x| of A and B via the range kernels; returns host values.
+template <class T>
+int range_pair(starmm_plan* P, const void* A, long long lda, const void* B, long long ldb,
+               int skip_inf, cudaStream_t s, unsigned long long* ma, unsigned long long* mb) {
+    CK(cudaMemsetAsync(P->d_range, 0, 2 * sizeof(unsigned long long), s));
+    range_absmax_kernel<T><<<grid_blocks(P->m * P->k), 256, 0, s>>>((const T*)A, P->m, P->k, lda,
+                                                                   P->d_range, skip_inf);
+    CK(cudaGetLastError());
+    range_absmax_kernel<T><<<grid_blocks(P->k * P->n), 256, 0, s>>>((const T*)B, P->k, P->n, ldb,
+                                                                   P->d_range + 1, skip_inf);
+    CK(cudaGetLastError());
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *ma = h[0];
+    *mb = h[1];
+    return STARMM_OK;
+}
+
+int ensure_bookkeeping(starmm_plan* P) {
+    if (P->d_counters) return STARMM_OK;
+    P->max_workers = P->sms * 2;
+    long long fr = 0, ru = 0;
+    void* p = nullptr;
+    size_t bytes = CNT__N * 8 + 16 + (size_t)P->max_workers * 4;
+    TRY(P->arena.acquire(bytes, &p, false, &fr, &ru));
+    CK(cudaMemset(p, 0, bytes));
+    P->d_counters = (unsigned long long*)p;
+    P->d_range = P->d_counters + CNT__N;
+    P->d_worker_used = (unsigned*)(P->d_range + 2);
+    return STARMM_OK;
+}
+
+}  // namespace
+
+// ============================================================================
+extern "C" {
+
+int starmm_abi_version(void) { return STARMM_ABI_VERSION; }
+
+const char* starmm_strerror(int status) {
+    switch (status) {
+    case STARMM_OK: return "ok";
+    case STARMM_DIM_MISMATCH: return "DimMismatch: operands do not have compatible dimensions";
+    case STARMM_INVALID_SPLIT: return "InvalidSplit: n must be a power of two >= base dimension";
+    case STARMM_NOT_BASE_CASE: return "NotBaseCase: region is not base-sized";
+    case STARMM_ALLOC_FAILURE: return "AllocFailure: device allocation failed";
+    case STARMM_CONTRACT_VIOLATION: return "ContractViolation: invalid argument";
+    case STARMM_ALIGNMENT_ERROR: return "AlignmentError: region not aligned to the base-tile grid";
+    case STARMM_NO_ADDITIVE_INVERSE: return "NoAdditiveInverse";
+    case STARMM_TOO_LARGE: return "TooLarge: problem exceeds supported size";
+    case STARMM_INTERNAL_ERROR: return "InternalError";
+    }
+    if (status >= STARMM_CUDA_ERROR) return cudaGetErrorString((cudaError_t)(status - STARMM_CUDA_ERROR));
+    return "unknown status";
+}
+
+int starmm_device_sm_count(int device) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    return v;
+}
+
+int starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mode, int64_t m,
+                       int64_t n, int64_t k, int base_dim, int workers, int ksplit_log2, int device,
+                       int flags) {
+    if (!plan) return STARMM_CONTRACT_VIOLATION;
+    *plan = nullptr;
+    if (semiring < 0 || semiring > STARMM_SR_TROPICAL_I32) return STARMM_CONTRACT_VIOLATION;
+    if (algo < STARMM_CO2 || algo > STARMM_STAR) return STARMM_CONTRACT_VIOLATION;
+    if (alloc_mode != STARMM_POOLED && alloc_mode != STARMM_RAW) return STARMM_CONTRACT_VIOLATION;
+    if (alloc_mode == STARMM_RAW && algo != STARMM_CO3) return STARMM_CONTRACT_VIOLATION;  // registry.py:34-35
+    if (m < 1 || n < 1 || k < 1) return STARMM_DIM_MISMATCH;
+    if (!is_pow2(base_dim) || workers < 1) return STARMM_CONTRACT_VIOLATION;          // matrix.py:44-47
+    if (ksplit_log2 > 16) return STARMM_CONTRACT_VIOLATION;
+    // Config.check_problem (matrix.py:57-61) unless the caller opted out.
+    if (!(flags & STARMM_F_ALLOW_NONPOW2)) {
+        if (!(m == n && n == k)) return STARMM_DIM_MISMATCH;
+        if (!is_pow2(n) || n < base_dim) return STARMM_INVALID_SPLIT;
+    }
+    if (m > (1LL << 31) || n > (1LL << 31) || k > (1LL << 31)) return STARMM_TOO_LARGE;
+    int ndev = 0;
+    CK(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) return STARMM_CONTRACT_VIOLATION;
+    starmm_plan* P = new starmm_plan();
+    P->sr = semiring; P->algo = algo; P->alloc = alloc_mode; P->base_dim = base_dim;
+    P->workers = workers; P->ksplit_req = ksplit_log2; P->device = device; P->flags = flags;
+    P->m = m; P->n = n; P->k = k;
+    memset(&P->st, 0, sizeof(P->st));
+    P->sms = starmm_device_sm_count(device);
+    *plan = P;
+    return STARMM_OK;
+}
+
+void starmm_plan_destroy(starmm_plan* P) {
+    if (!P) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(P->device);
+    cudaDeviceSynchronize();
+    P->arena.destroy();
+    cudaSetDevice(prev);
+    delete P;
+}
+
+int starmm_plan_reset_stats(starmm_plan* P) {
+    if (!P) return STARMM_CONTRACT_VIOLATION;
+    if (P->d_counters) {
+        CK(cudaMemset(P->d_counters, 0, CNT__N * 8));
+        CK(cudaMemset(P->d_worker_used, 0, (size_t)P->max_workers * 4));
+    }
+    memset(&P->st, 0, sizeof(P->st));
+    P->ws_fresh = P->ws_reuse = P->ws_high_water = 0;
+    P->raw_count = P->raw_bytes = 0;
+    return STARMM_OK;
+}
+
+int starmm_plan_stats(starmm_plan* P, starmm_stats* out) {
+    if (!P || !out) return STARMM_CONTRACT_VIOLATION;
+    *out = P->st;
+    unsigned long long c[CNT__N];
+    memset(c, 0, sizeof(c));
+    if (P->d_counters) CK(cudaMemcpy(c, P->d_counters, sizeof(c), cudaMemcpyDeviceToHost));
+    out->tile_serializations = (int64_t)c[CNT_SERIALIZATIONS];
+    out->pair_transitions = (int64_t)c[CNT_PAIR_TRANSITIONS];
+    out->lazy_temp_acquires = (int64_t)c[CNT_LAZY_ACQUIRES];
+    out->pool_fresh_count = (int64_t)c[CNT_POOL_FRESH] + P->ws_fresh;
+    out->pool_reuse_count = (int64_t)(c[CNT_POOL_ACQUIRES] - c[CNT_POOL_FRESH]) + P->ws_reuse;
+    out->pool_high_water_bytes = std::max<int64_t>((int64_t)c[CNT_POOL_HIGH_WATER], P->ws_high_water);
+    out->pool_total_allocated_bytes = P->arena.total_allocated;
+    out->raw_alloc_count = P->raw_count;
+    out->raw_alloc_bytes = P->raw_bytes;
+    return STARMM_OK;
+}
+
+int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
+                   int64_t ldb, void* stream) {
+    if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
+    if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
+    const int eb = elem_bytes(P->sr);
+    if (((uintptr_t)C | (uintptr_t)A | (uintptr_t)B) % eb) return STARMM_ALIGNMENT_ERROR;
+    int prev_dev = 0;
+    CK(cudaGetDevice(&prev_dev));
+    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(ensure_bookkeeping(P));
+    const bool init_identity = (P->flags & STARMM_F_INIT_IDENTITY) != 0;
+    const bool fast_ok = !(P->flags & STARMM_F_NO_FASTPATH);
+    int launches = 0;
+
+    // ---- path selection (range guards are exact-by-construction checks) ----
+    int path = 0;
+    if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
+    else if (P->sr == STARMM_SR_TROPICAL_F32) path = PATH_SIMT_F32_PAIR;
+    else if (P->sr == STARMM_SR_TROPICAL_F64) path = PATH_SIMT_F64_MIN;
+    else if (P->sr == STARMM_SR_INT64) {
+        path = PATH_SIMT_I64;
+        if (fast_ok) {
+            unsigned long long ma, mb;
+            TRY(range_pair<long long>(P, A, lda, B, ldb, 0, s, &ma, &mb));
+            launches += 2;
+            // exact iff every partial sum fits int32: K * max|a| * max|b| < 2^31
+            long double bound = (long double)P->k * (long double)ma * (long double)mb;
+            if (ma < (1ull << 31) && mb < (1ull << 31) && bound < 2147483648.0L)
+                path = PATH_SIMT_I64_NARROW;
+        }
+    } else {  // tropical_i32
+        path = PATH_SIMT_I32_SAT;
+        if (fast_ok) {
+            unsigned long long ma, mb;
+            TRY(range_pair<int>(P, A, lda, B, ldb, 1, s, &ma, &mb));
+            launches += 2;
+            unsigned long long mx = std::max(ma, mb);
+            if (mx <= (1ull << 23)) path = PATH_SIMT_I32_CARRIER;      // fp32-exact sums
+            else if (mx < (1ull << 28)) path = PATH_SIMT_I32_VMIN;     // no int32 overflow
+        }
+    }
+    const bool is_dmma = (path == PATH_DMMA_F64);
+    const int BK = is_dmma ? dmma::BK : simt::BK;
+
+    // ---- the split: leaf tasks = output tiles x k-slices ----
+    const long long tiles_m = (P->m + 127) / 128, tiles_n = (P->n + 127) / 128;
+    const long long tiles = tiles_m * tiles_n;
+    const int gpu_workers = P->sms;                      // one persistent CTA per SM
+    int s_log2;
+    if (P->ksplit_req >= 0) {
+        s_log2 = P->ksplit_req;
+    } else if (P->algo == STARMM_CO2) {
+        s_log2 = 0;                                      // k-halves serialised (classic.py:125-128)
+    } else {
+        s_log2 = 1;                                      // sibling k-halves concurrent
+        while ((tiles << s_log2) < gpu_workers) ++s_log2;  // ... and enough leaves to fill the GPU
+    }
+    // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels than
+    // the recursion has (log2(k / b))
+    while (s_log2 > 0 && ((P->k >> s_log2) < std::max(P->base_dim, BK) || (P->k >> s_log2) < 1))
+        --s_log2;
+    const int S = 1 << s_log2;
+    int tar_levels = 0;
+    if (P->algo == STARMM_TAR) tar_levels = s_log2;
+    if (P->algo == STARMM_STAR) tar_levels = std::min(switch_depth(P->workers), s_log2);
+
+    const long long Mp = tiles_m * 128, Np = tiles_n * 128;
+    const long long Kp = round_up(P->k, std::max<long long>(32, (long long)BK * S));
+    const long long kslice = Kp / S;
+
+    TaskGrid g;
+    g.tiles_m = (int)tiles_m; g.tiles_n = (int)tiles_n; g.S = S; g.log2S = s_log2;
+    g.tar_levels = tar_levels; g.group_m = 8; g.kslice = kslice;
+    const long long ntasks = tiles * S;
+    if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
+    g.num_tasks = (int)ntasks;
+
+    // ---- staging buffers from the arena (not counted as algorithm temps) ----
+    std::vector<Block> staged;
+    auto stage_acquire = [&](size_t bytes, void** p) -> int {
+        long long fr = 0, ru = 0;
+        TRY(P->arena.acquire(bytes, p, false, &fr, &ru));
+        staged.push_back({*p, bytes});
+        return STARMM_OK;
+    };
+    int rc = STARMM_OK;
+    const void* opA = A; const void* opB = B;
+    long long olda = lda, oldb = ldb;
+    do {
+        if (is_dmma) {
+            bool direct = (P->m % 128 == 0) && (P->n % 128 == 0) && (P->k == Kp) &&
+                          (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
+            if (!direct) {
+                void *pa, *pb;
+                if ((rc = stage_acquire((size_t)(Mp * Kp * 8), &pa))) break;
+                if ((rc = stage_acquire((size_t)(Kp * Np * 8), &pb))) break;
+                pad_copy_kernel<double><<<grid_blocks(Mp * Kp), 256, 0, s>>>((const double*)A, P->m, P->k,
+                                                                            lda, (double*)pa, Mp, Kp);
+                pad_copy_kernel<double><<<grid_blocks(Kp * Np), 256, 0, s>>>((const double*)B, P->k, P->n,
+                                                                            ldb, (double*)pb, Kp, Np);
+                if ((rc = cuda_status(cudaGetLastError()))) break;
+                launches += 2;
+                opA = pa; opB = pb; olda = Kp; oldb = Np;
+            }
+        } else {
+            int pe = (path == PATH_SIMT_I64 || path == PATH_SIMT_F64_MIN) ? 8 : 4;
+            void *pa, *pb;
+            if ((rc = stage_acquire((size_t)(Mp * Kp * pe), &pa))) break;
+            if ((rc = stage_acquire((size_t)(Kp * Np * pe), &pb))) break;
+            const float finf = std::numeric_limits<float>::infinity();
+            switch (path) {
+            case PATH_SIMT_F32_PAIR:
+                rc = launch_pack<float, float, 2, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                                 Mp, Np, Kp, finf, s); break;
+            case PATH_SIMT_I32_CARRIER:
+                rc = launch_pack<int, float, 2, ConvI32ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                               Mp, Np, Kp, finf, s); break;
+            case PATH_SIMT_I32_VMIN:
+                rc = launch_pack<int, int, 1, ConvI32Vmin>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
+                                                            Np, Kp, (1 << 30) - 1, s); break;
+            case PATH_SIMT_I32_SAT:
+                rc = launch_pack<int, int, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
+                                                             Np, Kp, 0x7fffffff, s); break;
+            case PATH_SIMT_I64:
+                rc = launch_pack<long long, long long, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k,
+                                                                         pa, pb, Mp, Np, Kp, 0LL, s); break;
+            case PATH_SIMT_I64_NARROW:
+                rc = launch_pack<long long, int, 1, ConvI64ToI32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                                   Mp, Np, Kp, 0, s); break;
+            case PATH_SIMT_F64_MIN: {
+                const double dinf = std::numeric_limits<double>::infinity();
+                rc = launch_pack<double, double, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa,
+                                                                   pb, Mp, Np, Kp, dinf, s); break;
+            }
+            }
+            if (rc) break;
+            launches += 2;
+            opA = pa; opB = pb;
+        }
+
+        // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
+        const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
+        void* pstate = nullptr;
+        size_t state_bytes = need_slots ? (size_t)(tiles + tiles * (S / 2)) * 4 : 0;
+        if (need_slots) {
+            if ((rc = stage_acquire(state_bytes, &pstate))) break;
+            if ((rc = cuda_status(cudaMemsetAsync(pstate, 0, state_bytes, s)))) break;
+        }
+        // per-worker lazy-temp blocks (tile sized, for SAR/STAR pairs)
+        void* wscratch = nullptr;
+        const long long tile_elems = 128LL * 128;
+        if (need_slots) {
+            if ((rc = stage_acquire((size_t)(gpu_workers * tile_elems * eb), &wscratch))) break;
+        }
+        // co3 workspace D_1..D_{S-1}: pooled (arena, reused) or raw (fresh per call)
+        void* W = nullptr;
+        size_t wbytes = 0;
+        if (P->algo == STARMM_CO3 && S > 1) {
+            wbytes = (size_t)(S - 1) * (size_t)P->m * (size_t)P->n * eb;
+            if (P->alloc == STARMM_POOLED) {
+                if ((rc = P->arena.acquire(wbytes, &W, true, &P->ws_fresh, &P->ws_reuse))) break;
+                staged.push_back({W, wbytes});
+            } else {
+                if ((rc = cuda_status(cudaMallocAsync(&W, wbytes, s)))) break;
+                ++P->raw_count;
+                P->raw_bytes += (long long)wbytes;
+            }
+            P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
+        }
+        if (init_identity && S > 1 && P->algo != STARMM_CO3) {
+            if ((rc = fill_dispatch(P->sr, C, P->m, P->n, ldc, s))) break;
+            ++launches;
+        }
+
+        WbParams w;
+        w.mode_base = P->algo; w.init_identity = init_identity ? 1 : 0;
+        w.C = C; w.ldc = ldc; w.M = P->m; w.N = P->n;
+        w.W = W; w.ldw = P->n; w.wstride = P->m * P->n;
+        w.slots = (int*)pstate;
+        w.pairs = pstate ? (int*)pstate + tiles : nullptr;
+        w.counters = P->d_counters; w.worker_used = P->d_worker_used;
+        w.scratch = wscratch; w.scratch_elems = tile_elems;
+
+        int grid = occupancy_grid(P, 1, ntasks);
+        if (is_dmma) {
+            DmmaParams dp;
+            dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
+            dp.g = g; dp.w = w;
+            rc = launch_dmma(dp, grid, s);
+        } else {
+            SimtParams sp;
+            sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = g; sp.w = w;
+            switch (path) {
+            case PATH_SIMT_F32_PAIR: rc = launch_simt<PolF32Pair, SrTropF32>(sp, grid, s); break;
+            case PATH_SIMT_I32_CARRIER: rc = launch_simt<PolF32Pair, SrTropI32>(sp, grid, s); break;
+            case PATH_SIMT_I32_VMIN: rc = launch_simt<PolI32Vmin, SrTropI32>(sp, grid, s); break;
+            case PATH_SIMT_I32_SAT: rc = launch_simt<PolI32Sat, SrTropI32>(sp, grid, s); break;
+            case PATH_SIMT_I64: rc = launch_simt<PolI64, SrInt64>(sp, grid, s); break;
+            case PATH_SIMT_I64_NARROW: rc = launch_simt<PolI64Narrow, SrInt64>(sp, grid, s); break;
+            case PATH_SIMT_F64_MIN: rc = launch_simt<PolF64Min, SrTropF64>(sp, grid, s); break;
+            }
+        }
+        if (rc) break;
+        ++launches;
+
+        // ---- co3: merge the workspace bottom-up (merge_tasks, ops.py:108-155) ----
+        if (P->algo == STARMM_CO3 && S > 1) {
+            const long long slab = P->m * P->n;
+            for (int lvl = s_log2; lvl >= 1 && !rc; --lvl) {
+                int step = 1 << (s_log2 - lvl);
+                for (int x = step; x < S && !rc; x += 2 * step) {
+                    char* src = (char*)W + (size_t)(x - 1) * slab * eb;
+                    int tgt = x - step;
+                    if (tgt == 0) rc = madd_dispatch(P->sr, C, ldc, src, P->n, P->m, P->n, 0, s);
+                    else rc = madd_dispatch(P->sr, (char*)W + (size_t)(tgt - 1) * slab * eb, P->n, src,
+                                            P->n, P->m, P->n, 0, s);
+                    ++launches;
+                }
+            }
+            if (rc) break;
+            if (P->alloc == STARMM_RAW) {
+                if ((rc = cuda_status(cudaFreeAsync(W, s)))) break;
+            }
+        }
+    } while (0);
+
+    // staging buffers go back to their LIFO stacks; stream order protects reuse
+    for (auto it = staged.rbegin(); it != staged.rend(); ++it) P->arena.release(it->p, it->bytes);
+    if (rc) return rc;
+    if (!(P->flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+
+    P->st.tasks = ntasks;
+    P->st.workers = occupancy_grid(P, 1, ntasks);
+    P->st.ksplit = S;
+    P->st.tar_levels = tar_levels;
+    P->st.kernel_launches = launches;
+    P->st.path = path;
+    P->st.executes += 1;
+    if (S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && tar_levels < s_log2)
+        P->st.pair_count += tiles * (S / 2);
+    if (prev_dev != P->device) cudaSetDevice(prev_dev);
+    return STARMM_OK;
+}
+
+int starmm_matmul(int semiring, void* out, int64_t ldo, const void* A, int64_t lda, const void* B,
+                  int64_t ldb, int64_t m, int64_t n, int64_t k, void* stream, int flags) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    starmm_plan* P = nullptr;
+    TRY(starmm_plan_create(&P, semiring, STARMM_CO2, STARMM_POOLED, m, n, k, 1, 1, 0, dev,
+                           (flags | STARMM_F_INIT_IDENTITY | STARMM_F_ALLOW_NONPOW2)));
+    int rc = starmm_execute(P, out, ldo, A, lda, B, ldb, stream);
+    starmm_plan_destroy(P);
+    return rc;
+}
+
+int starmm_madd(int semiring, void* C, int64_t ldc, const void* D, int64_t ldd, int64_t rows,
+                int64_t cols, void* stream, int flags) {
+    if (!C || !D) return STARMM_CONTRACT_VIOLATION;
+    if (ldc < cols || ldd < cols || rows < 0 || cols < 0) return STARMM_DIM_MISMATCH;
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(madd_dispatch(semiring, C, ldc, D, ldd, rows, cols, 0, s));
+    if (!(flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+    return STARMM_OK;
+}
+
+int starmm_atomic_accumulate(int semiring, void* C, int64_t ldc, const void* P_, int64_t ldp,
+                             int64_t rows, int64_t cols, void* stream, int flags) {
+    if (!C || !P_) return STARMM_CONTRACT_VIOLATION;
+    if (ldc < cols || ldp < cols || rows < 0 || cols < 0) return STARMM_DIM_MISMATCH;
+    cudaStream_t s = (cudaStream_t)stream;
+    TRY(madd_dispatch(semiring, C, ldc, P_, ldp, rows, cols, 1, s));
+    if (!(flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+    return STARMM_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,296 @@
+"""GPU parity: the CUDA path (through the C ABI, via the drop-in API) vs the
+reference's golden outputs and the pinned CPU oracle.
+
+Bar: bit-exact for int64 (+,x) and every (min,+) semiring; float64 (+,x)
+within the relative tolerance of matrices_equal (matrix.py:182-193) -- 1e-9
+for the SPEC property tests, 1e-12 for PR1 (BASELINE config 1),
+1e-10*sqrt(n) for config 4.  FMA (DMMA) rounding is why fp64 is not bitwise.
+"""
+import os
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1911_05328_b200 as sm
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SMALL = np.load(os.path.join(GOLD, "ref_small.npz"))
+CASES = [(2, 2), (2, 8), (4, 16), (8, 32), (32, 64)]
+ALGOS = {"co2": sm.co2, "co3": sm.co3, "tar": sm.tar_mm, "sar": sm.sar_mm, "star": sm.star_mm}
+SR_OF = {"int": O.SR_INT64, "float": O.SR_FP64, "tropical": O.SR_TROP_F64,
+         "tropical_f32": O.SR_TROP_F32, "tropical_i32": O.SR_TROP_I32}
+
+
+def run(algo, s, C0, A, B, cfg, mode=None):
+    C, Am, Bm = sm.Matrix(C0, s), sm.Matrix(A, s), sm.Matrix(B, s)
+    if mode is None:
+        ALGOS[algo](C, Am, Bm, s, cfg)
+    else:
+        ALGOS[algo](C, Am, Bm, s, cfg, mode=mode)
+    return C.numpy()
+
+
+def assert_match(sid, got, want, tol=1e-9):
+    if sid == "float":
+        bound = tol * np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
+        assert np.all(np.abs(got - want) <= bound), float(np.max(np.abs(got - want)))
+    else:
+        assert np.array_equal(got, want)
+
+
+# ---- the reference's own fixtures, every schedule -------------------------
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("sid", ["int", "float", "tropical"])
+@pytest.mark.parametrize("b,n", CASES)
+@pytest.mark.parametrize("workers", [1, 16])
+def test_schedules_vs_reference_golden(algo, sid, b, n, workers):
+    key = f"{sid}_n{n}_b{b}"
+    s = sm.get_semiring(sid)
+    got = run(algo, s, SMALL[key + "_C0"], SMALL[key + "_A"], SMALL[key + "_B"],
+              sm.Config(base_dim=b, workers=workers))
+    assert_match(sid, got, SMALL[f"{key}_{algo}"])
+
+
+@pytest.mark.parametrize("algo", ["co3", "tar", "sar", "star"])
+@pytest.mark.parametrize("ksplit", [0, 1, 2, 3])
+@pytest.mark.parametrize("sid", ["int", "float", "tropical", "tropical_f32", "tropical_i32"])
+def test_split_protocols_vs_oracle(algo, ksplit, sid):
+    """Force k-splits so every write-back protocol (fold / store+merge / atomic /
+    pair+lock) runs, at a size with several tiles and a ragged edge."""
+    n = 256
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(ksplit * 10 + len(algo))
+    if sid in ("int",):
+        A = rng.integers(-50, 50, (n, n)).astype(np.int64)
+        B = rng.integers(-50, 50, (n, n)).astype(np.int64)
+        C0 = rng.integers(-50, 50, (n, n)).astype(np.int64)
+    elif sid == "float":
+        A, B, C0 = rng.standard_normal((n, n)), rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    else:
+        A = rng.integers(0, 100, (n, n)).astype(s.dtype)
+        B = rng.integers(0, 100, (n, n)).astype(s.dtype)
+        C0 = rng.integers(0, 400, (n, n)).astype(s.dtype)
+        inf = O.I32_INF if sid == "tropical_i32" else np.inf
+        A[rng.random(A.shape) < 0.2] = inf
+        B[rng.random(B.shape) < 0.2] = inf
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B)
+    cfg = sm.Config(base_dim=16, workers=4, ksplit=ksplit)
+    got = run(algo, s, C0, A, B, cfg)
+    assert_match(sid, got, want)
+
+
+# ---- BASELINE config 1 (PR1) ----------------------------------------------
+def test_pr1_star_fp64_vs_reference():
+    from bench_configs import make_inputs
+    A, B, C0 = make_inputs(1)
+    want = np.load(os.path.join(GOLD, "ref_pr1.npz"))["star"]
+    got = run("star", sm.FLOAT_RING, C0, A, B, sm.Config(base_dim=32, workers=1))
+    assert sm.matrices_equal(got, want, tol=1e-12)
+
+
+# ---- the exact narrow paths and their fallbacks ---------------------------
+def _path_of(algo, s, C0, A, B, cfg):
+    with sm.Executor(cfg) as ex:
+        C, Am, Bm = sm.Matrix(C0, s), sm.Matrix(A, s), sm.Matrix(B, s)
+        sm.run_algorithm(ex, algo, C, Am, Bm, s)
+        return C.numpy(), ex.last_stats["path_name"]
+
+
+@pytest.mark.parametrize("lo,hi,expect", [(-16, 17, "simt_i64_narrow_i32"),
+                                          (-2 ** 40, 2 ** 40, "simt_i64")])
+def test_int64_paths_bitexact(lo, hi, expect):
+    n = 384
+    rng = np.random.default_rng(5)
+    A = rng.integers(lo, hi, (n, n), dtype=np.int64)
+    B = rng.integers(lo, hi, (n, n), dtype=np.int64)
+    C0 = rng.integers(lo, hi, (n, n), dtype=np.int64)
+    want = C0.copy()
+    O.gemm_fold(O.SR_INT64, want, A, B)
+    got, path = _path_of("co2", sm.INT_RING, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
+    assert path == expect
+    assert np.array_equal(got, want)
+
+
+def test_int64_wraps_mod_2_64():
+    A = np.full((2, 2), 2 ** 62, np.int64)
+    B = np.full((2, 2), 4, np.int64)
+    got = run("co2", sm.INT_RING, np.zeros((2, 2), np.int64), A, B, sm.Config(base_dim=2))
+    assert got.tolist() == [[0, 0], [0, 0]]
+
+
+@pytest.mark.parametrize("hi,expect", [(1000, "simt_i32_via_f32_carrier"),
+                                       (1 << 26, "simt_i32_viaddmnmx"),
+                                       (1 << 30, "simt_i32_saturating")])
+def test_i32_tropical_paths_bitexact(hi, expect):
+    n = 320
+    rng = np.random.default_rng(9)
+    A = rng.integers(-hi, hi, (n, n), dtype=np.int32)
+    B = rng.integers(-hi, hi, (n, n), dtype=np.int32)
+    A[rng.random(A.shape) < 0.15] = O.I32_INF
+    B[rng.random(B.shape) < 0.15] = O.I32_INF
+    C0 = rng.integers(-hi, hi, (n, n), dtype=np.int32)
+    want = C0.copy()
+    O.gemm_fold(O.SR_TROP_I32, want, A, B)
+    got, path = _path_of("co2", sm.TROPICAL_I32, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
+    assert path == expect
+    assert np.array_equal(got, want)
+
+
+def test_tropical_nan_in_C_propagates_like_np_minimum():
+    s = sm.TROPICAL
+    A = np.array([[1.0, 2.0], [3.0, 4.0]])
+    B = np.array([[0.0, np.inf], [1.0, 0.0]])
+    C0 = np.array([[np.nan, 5.0], [0.5, np.inf]])
+    want = C0.copy()
+    O.gemm_fold(O.SR_TROP_F64, want, A, B)
+    got = run("co2", s, C0, A, B, sm.Config(base_dim=2))
+    assert np.array_equal(got, want, equal_nan=True)
+
+
+# ---- ragged / non-power-of-two / region-strided ---------------------------
+@pytest.mark.parametrize("n", [1, 3, 130, 200])
+@pytest.mark.parametrize("sid", ["int", "float", "tropical_f32", "tropical_i32"])
+def test_nonpow2_sizes(n, sid):
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(n)
+    A = rng.integers(0, 30, (n, n)).astype(s.dtype)
+    B = rng.integers(0, 30, (n, n)).astype(s.dtype)
+    C0 = rng.integers(0, 60, (n, n)).astype(s.dtype)
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B)
+    got = run("star", s, C0, A, B, sm.Config(base_dim=1, workers=8, allow_nonpow2=True))
+    assert_match(sid, got, want)
+
+
+def test_pow2_precondition_kept_by_default():
+    s = sm.FLOAT_RING
+    with pytest.raises(sm.InvalidSplit):
+        run("star", s, np.zeros((48, 48)), np.zeros((48, 48)), np.zeros((48, 48)), sm.Config())
+
+
+def test_base_kernel_and_madd_on_regions():
+    s = sm.INT_RING
+    rng = np.random.default_rng(3)
+    M = rng.integers(0, 10, (8, 8)).astype(np.int64)
+    C = sm.Matrix(M.copy(), s)
+    A = sm.Matrix(rng.integers(0, 10, (8, 8)).astype(np.int64), s)
+    B = sm.Matrix(rng.integers(0, 10, (8, 8)).astype(np.int64), s)
+    cfg = sm.Config(base_dim=4)
+    cq, aq, bq = C.region().quadrant(1, 0), A.region().quadrant(0, 1), B.region().quadrant(1, 1)
+    sm.base_kernel(cq, aq, bq, s, cfg)
+    want = M.copy()
+    want[4:, :4] += A.numpy()[:4, 4:] @ B.numpy()[4:, 4:]
+    assert np.array_equal(C.numpy(), want)
+    with pytest.raises(sm.NotBaseCase):
+        sm.base_kernel(C, A, B, s, cfg)
+    sm.madd(C.region().quadrant(0, 0), A.region().quadrant(1, 1), s)
+    want[:4, :4] += A.numpy()[4:, 4:]
+    assert np.array_equal(C.numpy(), want)
+
+
+def test_naive_mm_and_semiring_hooks():
+    s = sm.INT_RING
+    out = sm.naive_mm(sm.Matrix(np.array([[1, 2], [3, 4]]), s), sm.Matrix(np.array([[5, 6], [7, 8]]), s), s)
+    assert out.numpy().tolist() == [[19, 22], [43, 50]]
+    t = sm.TROPICAL.matmul(np.array([[0.0, 1.0], [2.0, 3.0]]), np.array([[0.0, 4.0], [1.0, 0.0]]))
+    assert t.tolist() == [[0, 1], [2, 3]]
+    # rectangular panels (sampled-tile protocol)
+    rng = np.random.default_rng(1)
+    A = rng.standard_normal((37, 91))
+    B = rng.standard_normal((91, 53))
+    assert np.allclose(sm.FLOAT_RING.matmul(A, B), A @ B, rtol=1e-12, atol=1e-12)
+    C = np.ones((2, 2))
+    sm.TROPICAL.fold_add(C, np.array([[0.5, 2.0], [np.inf, -1.0]]))
+    assert C.tolist() == [[0.5, 1.0], [1.0, -1.0]]
+
+
+def test_atomic_accumulate():
+    s = sm.FLOAT_RING
+    C = sm.Matrix(np.ones((64, 64)), s)
+    P = sm.Matrix(np.full((32, 32), 2.0), s)
+    sm.atomic_accumulate(C.region().quadrant(1, 1), P.region(), s,
+                         table=sm.TileExclusionTable(64, 64, 32))
+    want = np.ones((64, 64))
+    want[32:, 32:] += 2.0
+    assert np.array_equal(C.numpy(), want)
+    with pytest.raises(sm.DimMismatch):
+        sm.atomic_accumulate(C.region(), P.region(), s)
+
+
+# ---- space / busy-leaves bookkeeping (SPEC.md:562-566 analogues) ----------
+def _stats(algo, ksplit, workers=4, n=512, mode="pooled"):
+    s = sm.FLOAT_RING
+    rng = np.random.default_rng(0)
+    A, B = rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    cfg = sm.Config(base_dim=32, workers=workers, ksplit=ksplit)
+    with sm.Executor(cfg) as ex:
+        C = sm.Matrix(np.zeros((n, n)), s)
+        sm.run_algorithm(ex, algo, C, sm.Matrix(A, s), sm.Matrix(B, s), s, mode=mode)
+        return ex.last_stats, ex.metrics.snapshot(ex.pool), ex.pool.snapshot_counts()
+
+
+def test_tar_scratch_high_water_bounded_by_workers():
+    st, snap, pool = _stats("tar", ksplit=2)
+    tile_bytes = 128 * 128 * 8
+    assert st["tar_levels"] == 2
+    assert 0 < st["pool_high_water_bytes"] <= st["workers"] * tile_bytes
+    assert st["tile_serializations"] == st["tasks"]
+
+
+def test_sar_serial_buys_no_temporaries():
+    st, snap, _ = _stats("sar", ksplit=0)
+    assert st["lazy_temp_acquires"] == 0 and st["ksplit"] == 1
+
+
+def test_sar_pairs_transition_and_lazy_temps():
+    st, snap, _ = _stats("sar", ksplit=1)
+    pairs = st["pair_count"]
+    assert pairs == (512 // 128) ** 2
+    # every first half makes Empty->FirstRunning and FirstRunning->FirstDone
+    assert st["pair_transitions"] == 2 * pairs
+    assert st["tile_serializations"] == st["tasks"]
+    assert 0 <= st["lazy_temp_acquires"] <= pairs
+    assert snap.base_case_max <= torch.cuda.get_device_properties(0).multi_processor_count
+
+
+def test_star_switch_depth_levels():
+    st, _, _ = _stats("star", ksplit=3, workers=16)    # switch_depth(16) = 2
+    assert st["tar_levels"] == 2 and st["ksplit"] == 8
+
+
+def test_co3_pooled_reuses_and_raw_allocates():
+    s = sm.INT_RING
+    n = 256
+    A = np.ones((n, n), np.int64)
+    cfg = sm.Config(base_dim=32, ksplit=1)
+    with sm.Executor(cfg) as ex:
+        for _ in range(3):
+            C = sm.Matrix(np.zeros((n, n), np.int64), s)
+            sm.run_algorithm(ex, "co3", C, sm.Matrix(A, s), sm.Matrix(A, s), s, mode="pooled")
+            assert np.all(C.numpy() == n)
+        c = ex.pool.snapshot_counts()
+        assert c["fresh_count"] >= 1 and c["reuse_count"] >= 2
+        C = sm.Matrix(np.zeros((n, n), np.int64), s)
+        sm.run_algorithm(ex, "co3", C, sm.Matrix(A, s), sm.Matrix(A, s), s, mode="raw")
+        assert np.all(C.numpy() == n)
+        assert ex.metrics.snapshot().raw_alloc_count == 1
+
+
+def test_errors_map_to_reference_exceptions():
+    s = sm.FLOAT_RING
+    with pytest.raises(sm.DimMismatch):
+        sm.co2(sm.Matrix(np.zeros((4, 4)), s), sm.Matrix(np.zeros((4, 8)), s),
+               sm.Matrix(np.zeros((8, 4)), s), s, sm.Config(base_dim=2))
+    with pytest.raises(sm.ContractViolation):
+        with sm.Executor(sm.Config(base_dim=2)) as ex:
+            z = sm.Matrix(np.zeros((4, 4)), s)
+            sm.run_algorithm(ex, "tar", z, z, z, s, mode="raw")
+    with pytest.raises(KeyError):
+        with sm.Executor(sm.Config(base_dim=2)) as ex:
+            z = sm.Matrix(np.zeros((4, 4)), s)
+            sm.run_algorithm(ex, "bogus", z, z, z, s)
