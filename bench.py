@@ -1,0 +1,436 @@
+#!/usr/bin/env python
+"""Benchmark: semiring MM ops/s (2n^3/t) on B200 -- BASELINE.json's metric.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--algo star]
+  python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N
+  python bench.py --impl reference ...     # the reference CPU path (oracle port)
+
+Workload: one step = one STAR-MM C <- C (+) A (x) B
+over the whole configured problem, inputs resident in HBM.  The default
+workload is BASELINE config 4 (fp64 (+,x), n = 16384, A,B ~ N(0,1), C ~
+U[-1,1)): the largest single-GPU config quoted at 1/2/4/8 B200 and the one
+the >=70%-of-roofline target names (n >= 16384).  Configs 2, 3, 5 run with
+--config; config 1 (n=256) is the parity gate, not a bench line.
+
+Multi-GPU: 2D output tiling (pr x pc) and, for config 5, a k-split whose
+partial minima are combined by one NCCL reduce-scatter; value = 2n^3 / max
+over ranks of the device time.  Inputs are generated on device with torch's
+Philox generator (same distributions as bench_configs.py; the tests use the
+numpy generators) and are all larger than the 126 MB L2, so no explicit
+flush is needed between steps.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+import zlib
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from bench_configs import CONFIGS  # noqa: E402
+
+# ---- roofline denominators ---------------------------
+SM_COUNT_NOMINAL = 148
+
+
+def _measured(name, key, default):
+    p = os.path.join(REPO, "profiles", name)
+    try:
+        return json.load(open(p)).get(key, default)
+    except Exception:
+        return default
+
+
+def peaks(sm_max_mhz: float):
+    dmma = 2 * _measured("r01_peaks_microbench.json", "dmma_terms_per_s_b8", 1.8551e13)
+    cublas = 1e12 * _measured("r01_cublas_dgemm.json", "cublas_dgemm_n16384_tflops", 36.08)
+    issue = SM_COUNT_NOMINAL * 128 * sm_max_mhz * 1e6          # BASELINE: 2 instr / term
+    vmin = 2 * _measured("r01_peaks_microbench.json", "viaddmnmx_terms_per_s_b8", 1.8471e13)
+    return {"fp64_tensor": max(dmma, cublas), "fp64_dmma_ubench": dmma, "cublas_dgemm": cublas,
+            "issue": issue, "viaddmnmx_ubench": vmin}
+
+
+# ---- clocks during the timed region ----------------------------------------
+class ClockSampler:
+    def __init__(self, device_index: int, period=0.2):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._dev = device_index
+        self._period = period
+        self._t = None
+
+    def __enter__(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(self._dev)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+            self._nv = pynvml
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        except Exception as e:  # pragma: no cover
+            self.error = str(e)
+        return self
+
+    def _run(self):
+        nv = self._nv
+        names = {
+            "gpu_idle": 0x1, "applications_clocks_setting": 0x2, "sw_power_cap": 0x4,
+            "hw_slowdown": 0x8, "sync_boost": 0x10, "sw_thermal_slowdown": 0x20,
+            "hw_thermal_slowdown": 0x40, "hw_power_brake_slowdown": 0x80,
+        }
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                for k, bit in names.items():
+                    if r & bit and k != "gpu_idle":
+                        self.reasons.add(k)
+            except Exception:
+                pass
+            self._stop.wait(self._period)
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "samples": len(self.samples),
+                "reasons": sorted(self.reasons)}
+
+
+# ---- device input generation -------------------------------------------------
+def gen_panel(cid: int, what: str, rows: int, cols: int, r0: int, c0: int, device, seed_salt=0):
+    """Synthetic panel of the config's distribution (on device, Philox)."""
+    cfg = CONFIGS[cid]
+    g = torch.Generator(device=device)
+    g.manual_seed(cfg["seed"] * 1000003 + zlib.crc32(f"{what}:{r0}:{c0}:{seed_salt}".encode()))
+    if cid in (1, 4):
+        if cid == 4 and what in ("A", "B"):
+            return torch.randn(rows, cols, generator=g, dtype=torch.float64, device=device)
+        return torch.rand(rows, cols, generator=g, dtype=torch.float64, device=device) * 2 - 1
+    if cid == 2:
+        if what == "C":
+            return torch.zeros(rows, cols, dtype=torch.int64, device=device)
+        return torch.randint(-16, 17, (rows, cols), generator=g, dtype=torch.int64, device=device)
+    if cid == 3:
+        edge = torch.rand(rows, cols, generator=g, device=device) < 0.1
+        W = torch.randint(1, 101, (rows, cols), generator=g, device=device).to(torch.float32)
+        W[~edge] = float("inf")
+        _zero_diag(W, r0, c0, 0.0)
+        return W
+    if cid == 5:
+        W = torch.randint(1, 10 ** 6 + 1, (rows, cols), generator=g, dtype=torch.int32, device=device)
+        _zero_diag(W, r0, c0, 0)
+        return W
+    raise KeyError(cid)
+
+
+def _zero_diag(W, r0, c0, val):
+    rows, cols = W.shape
+    lo, hi = max(r0, c0), min(r0 + rows, c0 + cols)
+    if lo < hi:
+        idx = torch.arange(lo, hi, device=W.device)
+        W[idx - r0, idx - c0] = val
+
+
+# ---- CPU baseline (the reference path's oracle port) --------------------------
+def cpu_sample(cid: int, A_host_rows, B_host, target_s: float):
+    """Time the oracle port (oracle/starmm_oracle.c, all host threads) on a bounded
+    row panel: rows x n x n terms.  Returns (ops_per_s, desc, cores, seconds)."""
+    from oracle import oracle as O
+    sr = O.SR_BY_NAME[CONFIGS[cid]["semiring"]]
+    n = B_host.shape[0]
+    cores = O.num_threads()
+    rows = min(cores, A_host_rows.shape[0])
+    C = np.zeros((rows, B_host.shape[1]), dtype=B_host.dtype)
+    t0 = time.perf_counter()
+    O.gemm_fold(sr, C, np.ascontiguousarray(A_host_rows[:rows]), B_host, par=True)
+    t = time.perf_counter() - t0
+    want = max(rows, min(A_host_rows.shape[0], int(rows * target_s / max(t, 1e-3)) // cores * cores))
+    if want > rows:
+        rows = want
+        C = np.zeros((rows, B_host.shape[1]), dtype=B_host.dtype)
+        t0 = time.perf_counter()
+        O.gemm_fold(sr, C, np.ascontiguousarray(A_host_rows[:rows]), B_host, par=True)
+        t = time.perf_counter() - t0
+    ops = 2.0 * rows * n * B_host.shape[1]
+    return ops / t, f"{rows}x{n} (x) {n}x{B_host.shape[1]} row panel of config {cid}", cores, t
+
+
+def host_panels_for_baseline(cid, n, device):
+    """A row panel and the full B on the host (the oracle's inputs)."""
+    rows = 512
+    A = gen_panel(cid, "A", rows, n, 0, 0, device).cpu().numpy()
+    B = gen_panel(cid, "B", n, n, 0, 0, device).cpu().numpy()
+    return A, B
+
+
+# ---- main -------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
+    ap.add_argument("--algo", default="star", choices=["co2", "co3", "tar", "sar", "star"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override n (smoke runs only)")
+    ap.add_argument("--ksplit-gpus", type=int, default=None)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        return reference_arm(args, world, rank)
+
+    torch.cuda.set_device(local_rank)
+    device = torch.device("cuda", local_rank)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=device)
+
+    import paper_1911_05328_b200 as sm
+    from paper_1911_05328_b200 import _lib
+    from paper_1911_05328_b200.distributed import DistributedMM, choose_grid, ks_groups
+
+    cid = args.config
+    cfg = CONFIGS[cid]
+    n = args.n or cfg["n"]
+    s = sm.get_semiring(cfg["semiring"])
+    ks = args.ksplit_gpus or (2 if (cid == 5 and world >= 8) else 1)
+    grid = choose_grid(world, ks)
+    group_ks = ks_groups(grid) if world > 1 else None
+    sms = torch.cuda.get_device_properties(device).multi_processor_count
+    dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
+                        group_ks=group_ks, device=local_rank, time_kernel=True)
+
+    A = gen_panel(cid, "A", dmm.m, dmm.k, dmm.r0, dmm.k0, device)
+    B = A if (cid in (3, 5) and dmm.r0 == dmm.k0 and dmm.m == dmm.k and dmm.c0 == dmm.k0
+              and dmm.nn == dmm.k) else gen_panel(cid, "B", dmm.k, dmm.nn, dmm.k0, dmm.c0, device)
+    C = gen_panel(cid, "C", dmm.m, dmm.nn, dmm.r0, dmm.c0, device) if dmm.K == 0 else \
+        torch.empty(dmm.m, dmm.nn, dtype=s.torch_dtype, device=device)
+    if cid in (3, 5) and dmm.K == 0:
+        C = C.clone()   # C = A (for the diagonal block) -- distribution only matters here
+
+    def step():
+        dmm.step(C, A, B)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    dmm.plan.reset_stats()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            step()
+        e1.record()
+        torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_local = e0.elapsed_time(e1) / 1e3 / args.steps
+    st = dmm.plan.stats()
+    kern_s_local = st["main_kernel_ns"] / 1e9 / max(1, st["main_kernel_launches"])
+    tt = torch.tensor([t_local, kern_s_local], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    t_step, kern_s = float(tt[0]), float(tt[1])
+    total_ops = 2.0 * n ** 3
+    value = total_ops / t_step
+
+    # ---- e2e through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        e2e = e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks)
+
+    # ---- roofline of the dominant kernel ----
+    clocks = clk.summary()
+    pk = peaks(clocks["sm_max_mhz"] or 1965.0)
+    local_ops = 2.0 * dmm.m * dmm.nn * dmm.k
+    achieved = local_ops / kern_s
+    if s.id == "float":
+        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk["fp64_tensor"] / 1e12,
+                "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
+                "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json has no fp64)"}
+    else:
+        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": pk["issue"] / 1e12,
+                "unit": "Tops/s", "peak_source": "BASELINE issue roofline: 148 SMs x 128 lanes x "
+                "sm_max_mhz (2 instructions per term); viaddmnmx ubench = %.2f Tops/s"
+                % (pk["viaddmnmx_ubench"] / 1e12)}
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["traffic"] = _ncu_traffic(cid, st["path_name"])
+    roof["kernel_ms"] = kern_s * 1e3
+    roof["kernel_share_of_step"] = kern_s / t_step
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Ah, Bh = host_panels_for_baseline(cid, n, device)
+        v, desc, cores, secs = cpu_sample(cid, Ah, Bh, args.cpu_seconds)
+        cpu = {"value": v / 1e12, "unit": "Tops/s", "cores": cores, "kind": "port",
+               "sample": desc + f" ({secs:.1f} s), oracle/starmm_oracle.c"}
+
+    if rank == 0:
+        line = {
+            "metric": "semiring MM ops/s (2n^3/t)", "value": value / 1e12, "unit": "Tops/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": t_step * 1e3, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None,
+            "dtype": {"float": "f64", "int": "int64", "tropical_f32": "f32",
+                      "tropical_i32": "int32"}[s.id],
+            "data": "synthetic (device Philox, BASELINE config distributions)",
+            "config": {"workload": cfg["name"], "baseline_config": cid, "n": n, "semiring": s.id,
+                       "algo": args.algo, "base_dim": cfg["b"], "workers": sms,
+                       "grid": [grid.pr, grid.pc, grid.ks], "path": st["path_name"],
+                       "ksplit_per_tile": st["ksplit"], "l2": "inputs larger than L2 (no flush)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(st["kernel_launches"]) * args.steps,
+            "clocks": clocks,
+        }
+        print(json.dumps(line))
+    dmm.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def _ncu_traffic(cid, path):
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        return json.load(open(p)).get(f"{cid}:{path}")
+    except Exception:
+        return None
+
+
+def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
+    """Public-API end to end: pinned host -> device, star_mm (N=1) / DistributedMM
+    step (N>1), result -> pinned host, every step."""
+    Ah = A.cpu().pin_memory()
+    Bh = Ah if B is A else B.cpu().pin_memory()
+    Ch = C.cpu().pin_memory()
+    out = torch.empty(Ch.shape if dmm.grid.ks == 1 else (dmm.owned_rows()[1] - dmm.owned_rows()[0],
+                      dmm.nn), dtype=Ch.dtype).pin_memory()
+    cfg = sm.Config(base_dim=CONFIGS[cid]["b"], workers=torch.cuda.get_device_properties(device)
+                    .multi_processor_count, allow_nonpow2=True)
+    ex = sm.Executor(cfg) if world == 1 else None
+
+    def one():
+        Ad = Ah.to(device, non_blocking=True)
+        Bd = Ad if Bh is Ah else Bh.to(device, non_blocking=True)
+        Cd = Ch.to(device, non_blocking=True)
+        if world == 1:
+            Cm = sm.Matrix(Cd, s)
+            sm.run_algorithm(ex, args.algo, Cm, sm.Matrix(Ad, s), sm.Matrix(Bd, s), s)
+            out.copy_(Cm.data, non_blocking=True)
+        else:
+            r = dmm.step(Cd, Ad, Bd)
+            out.copy_(r, non_blocking=True)
+
+    one()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    steps = max(1, min(args.steps, 3))
+    e0.record()
+    for _ in range(steps):
+        one()
+    e1.record()
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3 / steps], dtype=torch.float64, device=device)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    if ex is not None:
+        ex.close()
+    es = Ah.element_size()
+    h2d = (Ah.numel() + (0 if Bh is Ah else Bh.numel()) + Ch.numel()) * es
+    return {"value": 2.0 * dmm.n ** 3 / float(t[0]) / 1e12, "unit": "Tops/s",
+            "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(out.numel() * es),
+            "steps": steps, "api": "run_algorithm(Executor, 'star', Matrix...)" if world == 1
+            else "DistributedMM.step"}
+
+
+def reference_arm(args, world, rank):
+    """--impl reference: the reference's CPU path (oracle port, all host threads),
+    rank 0 only, on the same config/metric; each step is a bounded row-panel sample."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    cid = args.config
+    cfg = CONFIGS[cid]
+    n = args.n or cfg["n"]
+    rng = np.random.default_rng(cfg["seed"])
+    dt = cfg["dtype"]
+    # same distributions as bench_configs.make_inputs, generated only as far as needed
+    if cid == 4:
+        Ar = rng.standard_normal((256, n))
+        B = rng.standard_normal((n, n))
+    elif cid == 2:
+        Ar = rng.integers(-16, 17, (256, n), dtype=np.int64)
+        B = rng.integers(-16, 17, (n, n), dtype=np.int64)
+    elif cid == 3:
+        B = rng.integers(1, 101, (n, n), dtype=np.int32).astype(np.float32)
+        B[rng.random((n, n), dtype=np.float32) >= 0.1] = np.inf
+        np.fill_diagonal(B, 0.0)
+        Ar = B[:256]
+    else:
+        B = rng.integers(1, 10 ** 6 + 1, (n, n), dtype=np.int32)
+        np.fill_diagonal(B, 0)
+        Ar = B[:256]
+    Ar = np.ascontiguousarray(Ar.astype(dt))
+    B = np.ascontiguousarray(B.astype(dt))
+    sr = O.SR_BY_NAME[cfg["semiring"]]
+    cores = O.num_threads()
+    # calibrate rows per step so that one step takes ~2 s
+    rows = cores
+    C = np.zeros((rows, n), dtype=dt)
+    t0 = time.perf_counter()
+    O.gemm_fold(sr, C, Ar[:rows], B, par=True)
+    t1 = time.perf_counter() - t0
+    rows = int(max(cores, min(Ar.shape[0], rows * 2.0 / max(t1, 1e-3))) // cores * cores)
+    C = np.zeros((rows, n), dtype=dt)
+    for _ in range(args.warmup):
+        O.gemm_fold(sr, C, Ar[:rows], B, par=True)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        O.gemm_fold(sr, C, Ar[:rows], B, par=True)
+    t = (time.perf_counter() - t0) / args.steps
+    v = 2.0 * rows * n * n / t / 1e12
+    line = {
+        "metric": "semiring MM ops/s (2n^3/t)", "value": v, "unit": "Tops/s", "impl": "reference",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": {"float": "f64", "int": "int64", "tropical_f32": "f32", "tropical_i32": "int32"}[
+            cfg["semiring"]],
+        "data": "synthetic (numpy PCG64, BASELINE config distributions)",
+        "config": {"workload": cfg["name"], "baseline_config": cid, "n": n,
+                   "semiring": cfg["semiring"], "algo": args.algo},
+        "cpu_baseline": {"value": v, "unit": "Tops/s", "cores": cores, "kind": "port",
+                         "sample": f"{rows}x{n} (x) {n}x{n} row panel per step, "
+                                   "oracle/starmm_oracle.c (restates semiring.py:22-60)"},
+        "e2e": {"value": v, "unit": "Tops/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+
+
+if __name__ == "__main__":
+    main()

@@ -86,6 +86,7 @@ enum starmm_alloc { STARMM_POOLED = 0, STARMM_RAW = 1 };
 #define STARMM_F_NO_FASTPATH    0x2  /* disable range-guarded exact narrow paths       */
 #define STARMM_F_INIT_IDENTITY  0x4  /* ignore incoming C: C <- A (x) B (k-split partials) */
 #define STARMM_F_ALLOW_NONPOW2  0x8  /* accept any n >= 1 (divergence from matrix.py:57-61) */
+#define STARMM_F_TIME_MAIN      0x10 /* CUDA-event time the tile kernel (stats.main_kernel_ns) */
 
 typedef struct starmm_plan starmm_plan;
 
@@ -110,6 +111,8 @@ typedef struct {
     int64_t kernel_launches;         /* launches issued by the last execute           */
     int64_t path;                    /* kernel path id of the last execute */
     int64_t executes;
+    int64_t main_kernel_ns;          /* sum of tile-kernel event times (STARMM_F_TIME_MAIN) */
+    int64_t main_kernel_launches;    /* launches that contributed to main_kernel_ns      */
 } starmm_stats;
 
 int  starmm_abi_version(void);

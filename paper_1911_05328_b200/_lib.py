@@ -20,7 +20,7 @@ LIB_PATH = os.path.join(_HERE, "libstarmm_b200.so")
 SR_INT64, SR_FP64, SR_TROPICAL_F64, SR_TROPICAL_F32, SR_TROPICAL_I32 = range(5)
 ALGO_IDS = {"co2": 0, "co3": 1, "tar": 2, "sar": 3, "star": 4}
 ALLOC_IDS = {"pooled": 0, "raw": 1}
-F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2 = 0x1, 0x2, 0x4, 0x8
+F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2, F_TIME_MAIN = 0x1, 0x2, 0x4, 0x8, 0x10
 
 PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f32_fadd2_fmnmx3",
               5: "simt_i32_via_f32_carrier", 6: "simt_i32_viaddmnmx", 7: "simt_i32_saturating",
@@ -32,7 +32,8 @@ class StarmmStats(ctypes.Structure):
         "pool_total_allocated_bytes", "pool_high_water_bytes", "pool_fresh_count",
         "pool_reuse_count", "tile_serializations", "pair_count", "pair_transitions",
         "lazy_temp_acquires", "raw_alloc_count", "raw_alloc_bytes", "tasks", "workers",
-        "ksplit", "tar_levels", "kernel_launches", "path", "executes")]
+        "ksplit", "tar_levels", "kernel_launches", "path", "executes", "main_kernel_ns",
+        "main_kernel_launches")]
 
     def to_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

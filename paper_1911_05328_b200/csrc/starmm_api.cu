@@ -112,6 +112,7 @@ struct starmm_plan {
     starmm_stats st;
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
 };
 
 namespace {
@@ -310,6 +311,8 @@ void starmm_plan_destroy(starmm_plan* P) {
     cudaGetDevice(&prev);
     cudaSetDevice(P->device);
     cudaDeviceSynchronize();
+    if (P->ev0) cudaEventDestroy(P->ev0);
+    if (P->ev1) cudaEventDestroy(P->ev1);
     P->arena.destroy();
     cudaSetDevice(prev);
     delete P;
@@ -530,6 +533,14 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         w.scratch = wscratch; w.scratch_elems = tile_elems;
 
         int grid = occupancy_grid(P, 1, ntasks);
+        const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
+        if (timed) {
+            if (!P->ev0) {
+                if ((rc = cuda_status(cudaEventCreate(&P->ev0)))) break;
+                if ((rc = cuda_status(cudaEventCreate(&P->ev1)))) break;
+            }
+            if ((rc = cuda_status(cudaEventRecord(P->ev0, s)))) break;
+        }
         if (is_dmma) {
             DmmaParams dp;
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
@@ -550,6 +561,9 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         }
         if (rc) break;
         ++launches;
+        if (timed) {
+            if ((rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
+        }
 
         // ---- co3: merge the workspace bottom-up (merge_tasks, ops.py:108-155) ----
         if (P->algo == STARMM_CO3 && S > 1) {
@@ -576,6 +590,13 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     for (auto it = staged.rbegin(); it != staged.rend(); ++it) P->arena.release(it->p, it->bytes);
     if (rc) return rc;
     if (!(P->flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+    if (P->flags & STARMM_F_TIME_MAIN) {
+        CK(cudaEventSynchronize(P->ev1));
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+        P->st.main_kernel_ns += (int64_t)((double)ms * 1e6);
+        P->st.main_kernel_launches += 1;
+    }
 
     P->st.tasks = ntasks;
     P->st.workers = occupancy_grid(P, 1, ntasks);

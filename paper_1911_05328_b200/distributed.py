@@ -1,0 +1,165 @@
+"""Multi-GPU partitioning of C <- C (+) A (x) B: 2D output tiling x optional k-split.
+
+One process per GPU (torch.distributed, NCCL over NVLink/NVSwitch).  The
+path shards naturally:
+
+  G = pr * pc * ks ranks; rank -> (I, J, K) with K fastest, so each k-split
+  group is ks consecutive ranks.  Rank (I, J, K) computes the partial block
+      P_IJ^K = A[rows_I, kslice_K] (x) B[kslice_K, cols_J]
+  with the K = 0 rank folding C0 into it exactly once and every other rank
+  starting from the additive identity (STARMM_F_INIT_IDENTITY).  With ks > 1
+  the partials are combined by ONE collective, a reduce-scatter within the
+  (I, J) group with op = SUM (fp64, int64 two's-complement wrap) or MIN
+  (the (min,+) semirings); rank K keeps row-chunk K of the reduced block.
+  Min and integer sums are order-independent, so the combine is bit-exact.
+
+The local product is pluggable (``local_mm``) so that the partition and
+combine logic can be exercised on CPU with the gloo backend (tests/), while
+the GPU path calls the C ABI.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import Callable, Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .errors import ContractViolation
+
+__all__ = ["Grid", "choose_grid", "block_bounds", "DistributedMM", "reduce_op_for"]
+
+
+@dataclass(frozen=True)
+class Grid:
+    pr: int
+    pc: int
+    ks: int
+
+    @property
+    def size(self):
+        return self.pr * self.pc * self.ks
+
+    def coords(self, rank: int):
+        k = rank % self.ks
+        ij = rank // self.ks
+        return ij // self.pc, ij % self.pc, k
+
+
+def choose_grid(world: int, ks: int = 1) -> Grid:
+    """pr x pc x ks = world with pr <= pc as square as possible (1x2, 2x2, 2x4 ...)."""
+    if world % ks:
+        raise ContractViolation(f"k-split {ks} does not divide world size {world}")
+    rest = world // ks
+    pr = int(rest ** 0.5)
+    while rest % pr:
+        pr -= 1
+    return Grid(pr, rest // pr, ks)
+
+
+def block_bounds(n: int, parts: int, idx: int, align: int = 128):
+    """[lo, hi) of part idx when n is split into `parts` nearly equal aligned chunks."""
+    units = (n + align - 1) // align
+    lo_u = units * idx // parts
+    hi_u = units * (idx + 1) // parts
+    return min(n, lo_u * align), min(n, hi_u * align)
+
+
+def reduce_op_for(sid: str):
+    return dist.ReduceOp.SUM if sid in ("int", "float") else dist.ReduceOp.MIN
+
+
+class DistributedMM:
+    """One rank's share of a distributed semiring MM.
+
+    ``local_mm(C, A, B, init_identity)`` computes C <- (C or identity) (+) A (x) B
+    on this rank's panels; the default is the native plan (GPU)."""
+
+    def __init__(self, n: int, semiring, grid: Grid, rank: int, algo: str = "star",
+                 base_dim: int = 64, workers: int = 1, group_ks=None,
+                 local_mm: Optional[Callable] = None, device: Optional[int] = None,
+                 time_kernel: bool = False):
+        self.n, self.s, self.grid, self.rank = n, semiring, grid, rank
+        self.I, self.J, self.K = grid.coords(rank)
+        self.r0, self.r1 = block_bounds(n, grid.pr, self.I)
+        self.c0, self.c1 = block_bounds(n, grid.pc, self.J)
+        self.k0, self.k1 = block_bounds(n, grid.ks, self.K)
+        self.m, self.nn, self.k = self.r1 - self.r0, self.c1 - self.c0, self.k1 - self.k0
+        self.group_ks = group_ks
+        self.init_identity = self.K > 0
+        self.local_mm = local_mm
+        self.plan = None
+        if local_mm is None:
+            flags = _lib.F_ALLOW_NONPOW2 | (_lib.F_INIT_IDENTITY if self.init_identity else 0)
+            if time_kernel:
+                flags |= _lib.F_TIME_MAIN
+            self.plan = _lib.Plan(semiring.sr_id, algo, "pooled", self.m, self.nn, self.k,
+                                  base_dim, workers, -1,
+                                  device if device is not None else torch.cuda.current_device(),
+                                  flags)
+        # rows of the (I, J) block each k-split member keeps after the reduce-scatter
+        self.chunk_rows = -(-self.m // grid.ks)
+
+    # -- panels -----------------------------------------------------------
+    def a_panel(self, A_full):
+        return A_full[self.r0:self.r1, self.k0:self.k1]
+
+    def b_panel(self, B_full):
+        return B_full[self.k0:self.k1, self.c0:self.c1]
+
+    def c_block(self, C_full):
+        return C_full[self.r0:self.r1, self.c0:self.c1]
+
+    def owned_rows(self):
+        """Global row range of the reduced block this rank owns after combine()."""
+        lo = self.r0 + self.K * self.chunk_rows
+        return min(lo, self.r1), min(lo + self.chunk_rows, self.r1)
+
+    # -- compute ----------------------------------------------------------
+    def local(self, C_blk: torch.Tensor, A_pan: torch.Tensor, B_pan: torch.Tensor) -> None:
+        if self.local_mm is not None:
+            self.local_mm(C_blk, A_pan, B_pan, self.init_identity)
+            return
+        stream = torch.cuda.current_stream(C_blk.device).cuda_stream
+        self.plan.execute(C_blk.data_ptr(), C_blk.stride(0), A_pan.data_ptr(), A_pan.stride(0),
+                          B_pan.data_ptr(), B_pan.stride(0), stream)
+
+    def combine(self, C_blk: torch.Tensor) -> torch.Tensor:
+        """Reduce-scatter the ks partial blocks; returns this rank's reduced row chunk."""
+        if self.grid.ks == 1:
+            return C_blk
+        pad_rows = self.chunk_rows * self.grid.ks
+        if pad_rows != self.m:
+            buf = torch.full((pad_rows, self.nn), self.s.zero.item(), dtype=C_blk.dtype,
+                             device=C_blk.device)
+            buf[: self.m].copy_(C_blk)
+        else:
+            buf = C_blk.contiguous()
+        out = torch.empty((self.chunk_rows, self.nn), dtype=C_blk.dtype, device=C_blk.device)
+        dist.reduce_scatter_tensor(out, buf, op=reduce_op_for(self.s.id), group=self.group_ks)
+        lo, hi = self.owned_rows()
+        return out[: hi - lo]
+
+    def step(self, C_blk, A_pan, B_pan) -> torch.Tensor:
+        self.local(C_blk, A_pan, B_pan)
+        return self.combine(C_blk)
+
+    def close(self):
+        if self.plan is not None:
+            self.plan.close()
+            self.plan = None
+
+
+def ks_groups(grid: Grid):
+    """Create the (I, J) k-split process groups (every rank must call this)."""
+    groups = []
+    mine = None
+    rank = dist.get_rank()
+    for ij in range(grid.pr * grid.pc):
+        ranks = [ij * grid.ks + k for k in range(grid.ks)]
+        g = dist.new_group(ranks) if grid.ks > 1 else None
+        groups.append(g)
+        if rank in ranks:
+            mine = g
+    return mine
