@@ -6,27 +6,17 @@
 // mma.sync.m8n8k4.f64, which ptxas lowers to DMMA.8x8x4 (measured: 37.1 TF/s
 // chip peak, profiles/r01_peaks_microbench.json).
 //
-// CTA tile 128x128, k-stage 16, 8 warps (2 x 4), warp tile 64x32 (8 x 4 DMMA
-// blocks, 64 fp64 accumulators per lane).  Operands are staged global->smem
-// with 16-byte cp.async in a 4-deep ring; rows are padded so the 64-bit
-// fragment loads are bank-conflict free.  Persistent CTAs (one per SM) walk
-// the leaf-task list; the epilogue applies the schedule's write-back protocol.
+// CTA tile BM x BN, k-stage BK, WM x WN warps (warp tile (BM/WM) x (BN/WN),
+// 8x8 DMMA blocks, accumulators in registers).  Operands are staged
+// global->smem with 16-byte cp.async in a STAGES-deep ring; rows are padded so
+// the 64-bit fragment loads are bank-conflict free.  Persistent CTAs (one per
+// SM) walk the leaf-task list; the epilogue applies the schedule's write-back
+// protocol (writeback.cuh).
 #pragma once
 #include "common.cuh"
 #include "writeback.cuh"
 
 namespace starmm {
-
-namespace dmma {
-constexpr int BM = 128, BN = 128, BK = 16;
-constexpr int STAGES = 4;
-constexpr int THREADS = 256;
-constexpr int A_LD = BK + 4;      // 20 doubles = 160 B row pitch
-constexpr int B_LD = BN + 4;      // 132 doubles = 1056 B row pitch
-constexpr int A_STAGE = BM * A_LD;
-constexpr int B_STAGE = BK * B_LD;
-constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 64;
-}  // namespace dmma
 
 STARMM_DEV void cp_async16(void* smem, const void* gmem) {
     unsigned s = (unsigned)__cvta_generic_to_shared(smem);
@@ -37,27 +27,53 @@ template <int N>
 STARMM_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N)); }
 
 STARMM_DEV void dmma_884(double& c0, double& c1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+    asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                  : "+d"(c0), "+d"(c1)
                  : "d"(a), "d"(b));
 }
 
+template <int BM_, int BN_, int WM_, int WN_, int BK_, int STAGES_, int MINB_ = 1, bool DB_ = false>
+struct DmmaCfg {
+    static constexpr int BM = BM_, BN = BN_, BK = BK_, STAGES = STAGES_;
+    static constexpr int MIN_BLOCKS = MINB_;                 // co-resident CTAs per SM
+    static constexpr bool DB = DB_;                          // register double-buffered fragments
+    static constexpr int WM = WM_, WN = WN_;
+    static constexpr int THREADS = WM * WN * 32;
+    static constexpr int WTM = BM / WM, WTN = BN / WN;      // warp tile
+    static constexpr int MI = WTM / 8, NJ = WTN / 8;         // 8x8 blocks per warp
+    static constexpr int A_LD = BK + 4;                      // padded row pitch (doubles)
+    static constexpr int B_LD = BN + 4;
+    static constexpr int A_STAGE = BM * A_LD;
+    static constexpr int B_STAGE = BK * B_LD;
+    static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 64;
+    static_assert(BK % 4 == 0 && (BK * BM / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0,
+                  "cp.async chunking");
+};
+
+// The production configuration (selected by tools/sweep_dmma.cu on B200):
+// 64x128 tiles, 4 warps of 32x64, 3-stage ring, two CTAs per SM so one CTA's
+// barrier / epilogue overlaps the other's DMMA stream.
+using DmmaProd = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
+
 struct DmmaParams {
-    const double* A; long long lda;   // >= BM/BK padded, 16-byte aligned rows
+    const double* A; long long lda;   // tile-aligned (padded if needed), 16-byte rows
     const double* B; long long ldb;
     TaskGrid g;
     WbParams w;
 };
 
-__global__ void __launch_bounds__(dmma::THREADS, 1) dmma_fp64_kernel(DmmaParams p) {
-    using namespace dmma;
+template <class K>
+__global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel(DmmaParams p) {
+    constexpr int BM = K::BM, BN = K::BN, BK = K::BK, STAGES = K::STAGES;
+    constexpr int A_LD = K::A_LD, B_LD = K::B_LD, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
+    constexpr int THREADS = K::THREADS, MI = K::MI, NJ = K::NJ;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     double* As = reinterpret_cast<double*>(smem_raw);
     double* Bs = As + STAGES * A_STAGE;
     int* smem_word = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int wm = warp >> 2, wn = warp & 3;          // 2 x 4 warps
+    const int wm = warp / K::WN, wn = warp % K::WN;
     const int gi = lane >> 2, ti = lane & 3;          // fragment coordinates
     const TaskGrid& g = p.g;
     const int nk = (int)(g.kslice / BK);
@@ -75,27 +91,29 @@ __global__ void __launch_bounds__(dmma::THREADS, 1) dmma_fp64_kernel(DmmaParams 
         auto load_stage = [&](int kt, int stage) {
             const double* a = Ag + (long long)kt * BK;
             double* as = As + stage * A_STAGE;
+            constexpr int A_CH = BK / 2;                     // 16-byte chunks per A row
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {           // 128 rows x 8 chunks
+            for (int i = 0; i < BM * A_CH / THREADS; ++i) {
                 int c = tid + i * THREADS;
-                int r = c >> 3, q = c & 7;
+                int r = c / A_CH, q = c % A_CH;
                 cp_async16(as + r * A_LD + q * 2, a + (long long)r * p.lda + q * 2);
             }
             const double* b = Bg + (long long)kt * BK * p.ldb;
             double* bs = Bs + stage * B_STAGE;
+            constexpr int B_CH = BN / 2;
 #pragma unroll
-            for (int i = 0; i < 4; ++i) {           // 16 rows x 64 chunks
+            for (int i = 0; i < BK * B_CH / THREADS; ++i) {
                 int c = tid + i * THREADS;
-                int r = c >> 6, q = c & 63;
+                int r = c / B_CH, q = c % B_CH;
                 cp_async16(bs + r * B_LD + q * 2, b + (long long)r * p.ldb + q * 2);
             }
         };
 
-        double acc[8][4][2];
+        double acc[MI][NJ][2];
 #pragma unroll
-        for (int i = 0; i < 8; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-            for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
 #pragma unroll
         for (int st = 0; st < STAGES - 1; ++st) {
@@ -108,19 +126,42 @@ __global__ void __launch_bounds__(dmma::THREADS, 1) dmma_fp64_kernel(DmmaParams 
             int nxt = kt + STAGES - 1;
             if (nxt < nk) load_stage(nxt, nxt % STAGES);
             cp_async_commit();
-            const double* as = As + (kt % STAGES) * A_STAGE + (wm * 64 + gi) * A_LD + ti;
-            const double* bs = Bs + (kt % STAGES) * B_STAGE + ti * B_LD + wn * 32 + gi;
+            const double* as = As + (kt % STAGES) * A_STAGE + (wm * K::WTM + gi) * A_LD + ti;
+            const double* bs = Bs + (kt % STAGES) * B_STAGE + ti * B_LD + wn * K::WTN + gi;
+            if constexpr (K::DB) {
+                double a[2][MI], b[2][NJ];
 #pragma unroll
-            for (int kk = 0; kk < BK; kk += 4) {
-                double a[8], b[4];
+                for (int i = 0; i < MI; ++i) a[0][i] = as[i * 8 * A_LD];
 #pragma unroll
-                for (int i = 0; i < 8; ++i) a[i] = as[i * 8 * A_LD + kk];
+                for (int j = 0; j < NJ; ++j) b[0][j] = bs[j * 8];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) b[j] = bs[kk * B_LD + j * 8];
+                for (int kk = 0; kk < BK; kk += 4) {
+                    const int cur = (kk / 4) & 1;
+                    if (kk + 4 < BK) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                        for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = as[i * 8 * A_LD + kk + 4];
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                        for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = bs[(kk + 4) * B_LD + j * 8];
+                    }
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j)
+                            dmma_884(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+                }
+            } else {
+#pragma unroll
+                for (int kk = 0; kk < BK; kk += 4) {
+                    double a[MI], b[NJ];
+#pragma unroll
+                    for (int i = 0; i < MI; ++i) a[i] = as[i * 8 * A_LD + kk];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) b[j] = bs[kk * B_LD + j * 8];
+#pragma unroll
+                    for (int i = 0; i < MI; ++i)
+#pragma unroll
+                        for (int j = 0; j < NJ; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+                }
             }
         }
         cp_async_wait<0>();
@@ -129,11 +170,11 @@ __global__ void __launch_bounds__(dmma::THREADS, 1) dmma_fp64_kernel(DmmaParams 
         writeback<SrFp64, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                                   [&](auto f) {
 #pragma unroll
-            for (int i = 0; i < 8; ++i)
+            for (int i = 0; i < MI; ++i)
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    int r = wm * 64 + i * 8 + gi;
-                    int c = wn * 32 + j * 8 + ti * 2;
+                for (int j = 0; j < NJ; ++j) {
+                    int r = wm * K::WTM + i * 8 + gi;
+                    int c = wn * K::WTN + j * 8 + ti * 2;
                     f(r, c, acc[i][j][0]);
                     f(r, c + 1, acc[i][j][1]);
                 }

@@ -44,6 +44,22 @@ struct PolF32Pair {        // packed element float, G = 2, accumulator float
         c = fminf(fminf(c, v.x), v.y);
     }
 };
+struct PolF32Single {      // fp32 (min,+) one k at a time: FADD + FMNMX (ptxas may fuse k pairs)
+    using Tp = float; using Acc = float;
+    static constexpr int G = 1;
+    static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fminf(c, a + b); }
+};
+struct PolF32PairMin2 {    // FADD2 + two 2-input FMNMX
+    using Tp = float; using Acc = float;
+    static constexpr int G = 2;
+    static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
+    static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
+        float2 v = __fadd2_rn(a, b);
+        asm("min.f32 %0, %0, %1;" : "+f"(c) : "f"(v.x));
+        asm("min.f32 %0, %0, %1;" : "+f"(c) : "f"(v.y));
+    }
+};
 struct PolF64Min {
     using Tp = double; using Acc = double;
     static constexpr int G = 1;
@@ -90,6 +106,12 @@ template <> struct Finish<PolF32Pair, SrTropF32> {
 template <> struct Finish<PolF32Pair, SrTropI32> {   // fp32 carrier -> int32, +inf -> INT32_MAX
     static STARMM_DEV int out(float v) { return v == __int_as_float(0x7f800000) ? 0x7fffffff : (int)v; }
 };
+template <> struct Finish<PolF32Single, SrTropF32> {
+    static STARMM_DEV float out(float v) { return v; }
+};
+template <> struct Finish<PolF32PairMin2, SrTropF32> {
+    static STARMM_DEV float out(float v) { return v; }
+};
 template <> struct Finish<PolF64Min, SrTropF64> {
     static STARMM_DEV double out(double v) { return v; }
 };
@@ -120,8 +142,8 @@ struct SimtParams {
     WbParams w;
 };
 
-template <class Pol, class Sr>
-__global__ void __launch_bounds__(simt::THREADS, 1) simt_mm_kernel(SimtParams p) {
+template <class Pol, class Sr, int MINB = 1>
+__global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams p) {
     using namespace simt;
     using Tp = typename Pol::Tp;
     using Acc = typename Pol::Acc;

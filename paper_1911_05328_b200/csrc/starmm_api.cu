@@ -138,13 +138,14 @@ int launch_simt(const SimtParams& p, int grid, cudaStream_t s) {
 }
 
 int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
+    using K = DmmaProd;
     static bool attr_done = false;
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(dmma_fp64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                dmma::SMEM_BYTES));
+        CK(cudaFuncSetAttribute(dmma_fp64_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                K::SMEM_BYTES));
         attr_done = true;
     }
-    dmma_fp64_kernel<<<grid, dmma::THREADS, dmma::SMEM_BYTES, s>>>(p);
+    dmma_fp64_kernel<K><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -391,12 +392,14 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         }
     }
     const bool is_dmma = (path == PATH_DMMA_F64);
-    const int BK = is_dmma ? dmma::BK : simt::BK;
+    const int BK = is_dmma ? DmmaProd::BK : simt::BK;
 
     // ---- the split: leaf tasks = output tiles x k-slices ----
-    const long long tiles_m = (P->m + 127) / 128, tiles_n = (P->n + 127) / 128;
+    const int TBM = is_dmma ? DmmaProd::BM : simt::BM, TBN = is_dmma ? DmmaProd::BN : simt::BN;
+    const long long tiles_m = (P->m + TBM - 1) / TBM, tiles_n = (P->n + TBN - 1) / TBN;
     const long long tiles = tiles_m * tiles_n;
-    const int gpu_workers = P->sms;                      // one persistent CTA per SM
+    const int per_sm = is_dmma ? DmmaProd::MIN_BLOCKS : 1;
+    const int gpu_workers = P->sms * per_sm;             // persistent CTAs (the GPU workers)
     int s_log2;
     if (P->ksplit_req >= 0) {
         s_log2 = P->ksplit_req;
@@ -415,7 +418,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     if (P->algo == STARMM_TAR) tar_levels = s_log2;
     if (P->algo == STARMM_STAR) tar_levels = std::min(switch_depth(P->workers), s_log2);
 
-    const long long Mp = tiles_m * 128, Np = tiles_n * 128;
+    const long long Mp = tiles_m * TBM, Np = tiles_n * TBN;
     const long long Kp = round_up(P->k, std::max<long long>(32, (long long)BK * S));
     const long long kslice = Kp / S;
 
@@ -439,7 +442,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     long long olda = lda, oldb = ldb;
     do {
         if (is_dmma) {
-            bool direct = (P->m % 128 == 0) && (P->n % 128 == 0) && (P->k == Kp) &&
+            bool direct = (P->m % TBM == 0) && (P->n % TBN == 0) && (P->k == Kp) &&
                           (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
             if (!direct) {
                 void *pa, *pb;
@@ -499,7 +502,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         }
         // per-worker lazy-temp blocks (tile sized, for SAR/STAR pairs)
         void* wscratch = nullptr;
-        const long long tile_elems = 128LL * 128;
+        const long long tile_elems = (long long)TBM * TBN;
         if (need_slots) {
             if ((rc = stage_acquire((size_t)(gpu_workers * tile_elems * eb), &wscratch))) break;
         }
@@ -532,7 +535,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         w.counters = P->d_counters; w.worker_used = P->d_worker_used;
         w.scratch = wscratch; w.scratch_elems = tile_elems;
 
-        int grid = occupancy_grid(P, 1, ntasks);
+        int grid = occupancy_grid(P, per_sm, ntasks);
         const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
         if (timed) {
             if (!P->ev0) {
@@ -599,7 +602,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     }
 
     P->st.tasks = ntasks;
-    P->st.workers = occupancy_grid(P, 1, ntasks);
+    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * (is_dmma ? DmmaProd::MIN_BLOCKS : 1));
     P->st.ksplit = S;
     P->st.tar_levels = tar_levels;
     P->st.kernel_launches = launches;

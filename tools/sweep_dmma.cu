@@ -1,0 +1,55 @@
+// Variant sweep for the fp64 DMMA tile kernel (csrc/dmma_kernel.cuh): times each
+// (warps, BK, stages) configuration on an n^3 fp64 product with the CO2 FOLD
+// write-back, CUDA events, 1 warm-up + 3 timed launches.  Used to choose DmmaProd.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/sweep tools/sweep_dmma.cu
+#include <cstdio>
+#include <vector>
+#include "../paper_1911_05328_b200/csrc/dmma_kernel.cuh"
+using namespace starmm;
+
+template <class K>
+void run(const char* name, int n, double* A, double* B, double* C, unsigned long long* cnt, int sms,
+         int group_m = 8, bool persistent = true) {
+    DmmaParams p{};
+    p.A = A; p.lda = n; p.B = B; p.ldb = n;
+    TaskGrid& g = p.g;
+    g.tiles_m = n / K::BM; g.tiles_n = n / K::BN; g.S = 1; g.log2S = 0; g.tar_levels = 0;
+    g.group_m = group_m; g.kslice = n; g.num_tasks = g.tiles_m * g.tiles_n;
+    WbParams& w = p.w;
+    w.mode_base = 0; w.init_identity = 0; w.C = C; w.ldc = n; w.M = n; w.N = n;
+    w.counters = cnt;
+    cudaFuncSetAttribute(dmma_fp64_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dmma_fp64_kernel<K>, K::THREADS, K::SMEM_BYTES);
+    int grid = sms * (occ > 0 ? occ : 1);
+    if (grid > g.num_tasks || !persistent) grid = g.num_tasks;
+    dmma_fp64_kernel<K><<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int i = 0; i < 3; ++i) dmma_fp64_kernel<K><<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
+    cudaError_t e = cudaGetLastError();
+    printf("{\"variant\":\"%s\",\"occ\":%d,\"smem\":%d,\"ms\":%.3f,\"tflops\":%.3f,\"err\":\"%s\"}\n", name, occ,
+           K::SMEM_BYTES, ms, 2.0 * n * (double)n * n / (ms * 1e-3) / 1e12, cudaGetErrorString(e));
+    fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+    int n = argc > 1 ? atoi(argv[1]) : 16384;
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    double *A, *B, *C; unsigned long long* cnt;
+    cudaMalloc(&A, (size_t)n * n * 8); cudaMalloc(&B, (size_t)n * n * 8); cudaMalloc(&C, (size_t)n * n * 8);
+    cudaMalloc(&cnt, 64 * 8);
+    cudaMemset(A, 0, (size_t)n * n * 8); cudaMemset(B, 0, (size_t)n * n * 8); cudaMemset(C, 0, (size_t)n * n * 8);
+    using P = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
+    run<P>("64x128_s4_g8", n, A, B, C, cnt, sms, 8, true);
+    run<P>("64x128_s4_g8_nonpersistent", n, A, B, C, cnt, sms, 8, false);
+    run<P>("64x128_s4_g4", n, A, B, C, cnt, sms, 4, true);
+    run<P>("64x128_s4_g16", n, A, B, C, cnt, sms, 16, true);
+    run<P>("64x128_s4_g32", n, A, B, C, cnt, sms, 32, true);
+    run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>>("64x128_s4_g8_db", n, A, B, C, cnt, sms, 8, true);
+    run<DmmaCfg<64, 128, 1, 4, 16, 4, 2>>("64x128_1x4_s4_g8", n, A, B, C, cnt, sms, 8, true);
+    run<DmmaCfg<64, 256, 2, 4, 16, 3, 1>>("64x256_2x4_s3_occ1", n, A, B, C, cnt, sms, 8, true);
+    return 0;
+}

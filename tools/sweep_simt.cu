@@ -1,0 +1,52 @@
+// Variant sweep for the CUDA-core semiring tile kernel (csrc/simt_kernel.cuh):
+// inner-term policy x co-resident CTAs per SM, CO2 FOLD write-back, packed
+// operands of zeros (throughput only), CUDA events, 1 warm-up + 3 timed.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/sweep_simt tools/sweep_simt.cu
+#include <cstdio>
+#include "../paper_1911_05328_b200/csrc/simt_kernel.cuh"
+using namespace starmm;
+
+template <class Pol, class Sr, int MINB>
+void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long long* cnt, int sms) {
+    SimtParams p{};
+    p.Ap = Ap; p.Bp = Bp; p.Mp = n; p.Np = n;
+    TaskGrid& g = p.g;
+    g.tiles_m = n / 128; g.tiles_n = n / 128; g.S = 1; g.log2S = 0; g.group_m = 8; g.kslice = n;
+    g.num_tasks = g.tiles_m * g.tiles_n;
+    WbParams& w = p.w;
+    w.mode_base = 0; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
+    auto kern = simt_mm_kernel<Pol, Sr, MINB>;
+    constexpr int smem = simt::smem_bytes<Pol>();
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    int occ = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, simt::THREADS, smem);
+    int grid = sms * (occ > 0 ? occ : 1);
+    kern<<<grid, simt::THREADS, smem>>>(p);
+    cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    for (int i = 0; i < 3; ++i) kern<<<grid, simt::THREADS, smem>>>(p);
+    cudaEventRecord(e1); cudaEventSynchronize(e1);
+    float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
+    printf("{\"variant\":\"%s\",\"occ\":%d,\"ms\":%.3f,\"tops\":%.3f,\"err\":\"%s\"}\n", name, occ, ms,
+           2.0 * n * (double)n * n / (ms * 1e-3) / 1e12, cudaGetErrorString(cudaGetLastError()));
+    fflush(stdout);
+}
+
+int main(int argc, char** argv) {
+    int n = argc > 1 ? atoi(argv[1]) : 8192;
+    int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    void *A, *B, *C; unsigned long long* cnt;
+    size_t bytes = (size_t)n * n * 8;
+    cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
+    cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
+    run<PolF32Pair, SrTropF32, 1>("f32_fadd2_fmnmx3_occ1", n, A, B, C, cnt, sms);
+    run<PolF32Pair, SrTropF32, 2>("f32_fadd2_fmnmx3_occ2", n, A, B, C, cnt, sms);
+    run<PolF32Single, SrTropF32, 1>("f32_fadd_fmnmx_occ1", n, A, B, C, cnt, sms);
+    run<PolF32Single, SrTropF32, 2>("f32_fadd_fmnmx_occ2", n, A, B, C, cnt, sms);
+    run<PolF32PairMin2, SrTropF32, 1>("f32_fadd2_2fmnmx_occ1", n, A, B, C, cnt, sms);
+    run<PolI32Vmin, SrTropI32, 1>("i32_viaddmnmx_occ1", n, A, B, C, cnt, sms);
+    run<PolI32Vmin, SrTropI32, 2>("i32_viaddmnmx_occ2", n, A, B, C, cnt, sms);
+    run<PolI64Narrow, SrInt64, 1>("i64narrow_imad_occ1", n, A, B, C, cnt, sms);
+    run<PolI64Narrow, SrInt64, 2>("i64narrow_imad_occ2", n, A, B, C, cnt, sms);
+    return 0;
+}
