@@ -1,0 +1,183 @@
+"""CPU: the C-ABI library loads and exports every symbol include/starmm_b200.h
+declares; argument validation that needs no GPU; the drop-in host logic
+(Config, registry validation order, switch depth, errors) mirrors the reference."""
+import ctypes
+import json
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_1911_05328_b200 as sm
+from paper_1911_05328_b200 import _lib
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HEADER = os.path.join(REPO, "include", "starmm_b200.h")
+SPEC = json.load(open(os.path.join(REPO, "tests", "golden", "ref_spec.json")))
+
+
+def declared_functions():
+    txt = open(HEADER).read()
+    txt = re.sub(r"/\*.*?\*/", "", txt, flags=re.S)
+    return sorted(set(re.findall(r"\b(starmm_[a-z_0-9]+)\s*\(", txt)))
+
+
+def test_header_declares_the_boundary():
+    fns = declared_functions()
+    for f in ("starmm_plan_create", "starmm_execute", "starmm_plan_stats", "starmm_plan_destroy",
+              "starmm_matmul", "starmm_madd", "starmm_atomic_accumulate", "starmm_strerror"):
+        assert f in fns
+
+
+def test_library_exports_every_declared_symbol():
+    L = ctypes.CDLL(_lib.LIB_PATH)
+    missing = [f for f in declared_functions() if not hasattr(L, f)]
+    assert not missing, missing
+
+
+def test_abi_version_and_strerror():
+    L = _lib.lib()
+    assert L.starmm_abi_version() == 1
+    assert L.starmm_strerror(0) == b"ok"
+    assert L.starmm_strerror(2).startswith(b"InvalidSplit")
+    assert L.starmm_strerror(1).startswith(b"DimMismatch")
+
+
+def test_plan_create_validates_before_touching_a_device():
+    L = _lib.lib()
+    h = ctypes.c_void_p()
+    # unknown semiring / algo / mode -> ContractViolation (5)
+    assert L.starmm_plan_create(ctypes.byref(h), 9, 0, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 5
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 7, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 5
+    # raw mode only for co3 (registry.py:34-35)
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 2, 1, 64, 64, 64, 32, 1, -1, 0, 0) == 5
+    # base_dim must be a power of two (matrix.py:44-45)
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 64, 64, 64, 24, 1, -1, 0, 0) == 5
+    # check_problem: non-pow2 n -> InvalidSplit (2); n < b -> InvalidSplit
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 48, 48, 48, 16, 1, -1, 0, 0) == 2
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 16, 16, 16, 32, 1, -1, 0, 0) == 2
+    # non-square without ALLOW_NONPOW2 -> DimMismatch (1)
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 64, 32, 64, 16, 1, -1, 0, 0) == 1
+    # NULL plan pointer
+    assert L.starmm_plan_create(None, 0, 0, 0, 64, 64, 64, 16, 1, -1, 0, 0) == 5
+
+
+def test_status_maps_to_reference_exceptions():
+    for code, exc in [(1, sm.DimMismatch), (2, sm.InvalidSplit), (3, sm.NotBaseCase),
+                      (4, sm.AllocFailure), (5, sm.ContractViolation), (6, sm.AlignmentError),
+                      (8, sm.TooLarge), (9, sm.InternalError), (102, sm.CudaError)]:
+        with pytest.raises(exc):
+            _lib.check(code)
+    _lib.check(0)
+    assert issubclass(sm.CudaError, sm.StarMMError)
+
+
+def test_switch_depth_matches_reference():
+    for p, k in SPEC["switch_depth"].items():
+        assert sm.switch_depth(int(p)) == k
+
+
+def test_config_validation_mirrors_reference():
+    with pytest.raises(sm.ContractViolation):
+        sm.Config(base_dim=24)
+    with pytest.raises(sm.ContractViolation):
+        sm.Config(workers=0)
+    with pytest.raises(sm.ContractViolation):
+        sm.Config(cache_size=16, line_size=8)
+    with pytest.raises(sm.ContractViolation):
+        sm.Config(epsilon=2)
+    cfg = sm.Config(base_dim=32)
+    with pytest.raises(sm.InvalidSplit):
+        cfg.check_problem(48)
+    with pytest.raises(sm.InvalidSplit):
+        cfg.check_problem(16)
+    cfg.check_problem(64)
+    sm.Config(allow_nonpow2=True).check_problem(49152)
+
+
+def _cpu(data, s):
+    return sm.Matrix(data, s, device="cpu")
+
+
+def test_registry_validation_order_without_gpu():
+    s = sm.INT_RING
+    z = _cpu(np.zeros((4, 4), np.int64), s)
+    with sm.Executor(sm.Config(base_dim=2)) as ex:
+        with pytest.raises(KeyError):
+            sm.run_algorithm(ex, "nope", z, z, z, s)
+        with pytest.raises(sm.ContractViolation):
+            sm.run_algorithm(ex, "co2", z, z, z, s, mode="weird")
+        with pytest.raises(sm.ContractViolation):
+            sm.run_algorithm(ex, "star", z, z, z, s, mode="raw")
+        with pytest.raises(sm.DimMismatch):
+            sm.run_algorithm(ex, "co2", z, _cpu(np.zeros((4, 2), np.int64), s), z, s)
+        with pytest.raises(sm.DimMismatch):
+            sm.run_algorithm(ex, "co2", z, z, z, sm.FLOAT_RING)
+        with pytest.raises(sm.NoAdditiveInverse):
+            t = _cpu(np.zeros((4, 4)), sm.TROPICAL)
+            sm.run_algorithm(ex, "strassen", t, t, t, sm.TROPICAL)
+        with pytest.raises(sm.ContractViolation):   # Strassen family is out of scope
+            sm.run_algorithm(ex, "strassen", z, z, z, s)
+    with sm.Executor(sm.Config(base_dim=8)) as ex:
+        with pytest.raises(sm.InvalidSplit):
+            sm.run_algorithm(ex, "co2", z, z, z, s)
+
+
+def test_regions_and_quadrants():
+    s = sm.FLOAT_RING
+    M = _cpu(np.arange(16.0).reshape(4, 4), s)
+    q = sm.quadrant(M.region(), 0, 1)
+    assert (q.row0, q.col0, q.rows, q.cols) == (0, 2, 2, 2)
+    assert q.view().tolist() == [[2.0, 3.0], [6.0, 7.0]]
+    assert q.data_ptr() == M.data.data_ptr() + 2 * 8
+    with pytest.raises(sm.InvalidSplit):
+        sm.MatrixRegion(M, 0, 0, 3, 3).quadrant(0, 0)
+    with pytest.raises(sm.AlignmentError):
+        sm.MatrixRegion(M, 1, 0, 2, 2).tile_range(2)
+    with pytest.raises(sm.DimMismatch):
+        sm.MatrixRegion(M, 3, 3, 2, 2)
+
+
+def test_matrices_equal_semantics():
+    a = np.array([[1.0, 2.0]])
+    assert sm.matrices_equal(a, a + 1e-12)
+    assert not sm.matrices_equal(a, a + 1e-6)
+    # raw float arrays take the tolerance branch, where inf - inf is NaN: the
+    # reference returns False here too (matrix.py:188-191)
+    assert not sm.matrices_equal(np.array([[np.inf]]), np.array([[np.inf]]))
+    with pytest.raises(sm.DimMismatch):
+        sm.matrices_equal(a, np.zeros((2, 2)))
+
+
+def test_host_pool_lifo_and_contracts():
+    p = sm.Pool(2, device="cpu")
+    h1 = p.acquire(0, 16)
+    p.release(h1)
+    h2 = p.acquire(0, 16)
+    assert h2 is h1                                 # LIFO reuse (pool.py:97)
+    assert p.snapshot_counts()["fresh_count"] == 1 and p.snapshot_counts()["reuse_count"] == 1
+    with pytest.raises(sm.ContractViolation):
+        p.release(h2, worker=1)
+    p.release(h2)
+    with pytest.raises(sm.ContractViolation):
+        p.release(h2)                               # double release
+    with pytest.raises(sm.ContractViolation):
+        sm.Pool(1, discipline="random")
+    f = sm.Pool(1, discipline="fifo", device="cpu")
+    a, b = f.acquire(0, 4), f.acquire(0, 4)
+    f.release(a)
+    f.release(b)
+    assert f.acquire(0, 4) is a                     # FIFO sabotage hook hands back the oldest
+
+
+def test_semiring_elementwise_ops():
+    assert sm.INT_RING.add(2, 3) == 5 and sm.INT_RING.mul(2, 3) == 6
+    assert sm.TROPICAL.add(2.0, 3.0) == 2.0 and sm.TROPICAL.mul(2.0, 3.0) == 5.0
+    assert sm.TROPICAL_I32.mul(np.int32(2 ** 31 - 1), np.int32(-5)) == 2 ** 31 - 1
+    assert sm.INT_RING.neg(5) == -5
+    with pytest.raises(sm.NoAdditiveInverse):
+        sm.TROPICAL.neg(1.0)
+    with pytest.raises(KeyError):
+        sm.get_semiring("bogus")
+    assert sm.get_semiring("tropical_f32").dtype == np.float32
