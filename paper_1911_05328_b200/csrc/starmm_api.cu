@@ -401,10 +401,10 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     const int per_sm = is_dmma ? DmmaProd::MIN_BLOCKS : 1;
     const int gpu_workers = P->sms * per_sm;             // persistent CTAs (the GPU workers)
     int s_log2;
-    if (P->ksplit_req >= 0) {
+    if (P->algo == STARMM_CO2) {
+        s_log2 = 0;                // k-halves serialised (classic.py:125-128): never split
+    } else if (P->ksplit_req >= 0) {
         s_log2 = P->ksplit_req;
-    } else if (P->algo == STARMM_CO2) {
-        s_log2 = 0;                                      // k-halves serialised (classic.py:125-128)
     } else {
         s_log2 = 1;                                      // sibling k-halves concurrent
         while ((tiles << s_log2) < gpu_workers) ++s_log2;  // ... and enough leaves to fill the GPU

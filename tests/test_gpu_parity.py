@@ -55,7 +55,7 @@ def test_schedules_vs_reference_golden(algo, sid, b, n, workers):
     assert_match(sid, got, SMALL[f"{key}_{algo}"])
 
 
-@pytest.mark.parametrize("algo", ["co3", "tar", "sar", "star"])
+@pytest.mark.parametrize("algo", ["co2", "co3", "tar", "sar", "star"])
 @pytest.mark.parametrize("ksplit", [0, 1, 2, 3])
 @pytest.mark.parametrize("sid", ["int", "float", "tropical", "tropical_f32", "tropical_i32"])
 def test_split_protocols_vs_oracle(algo, ksplit, sid):
