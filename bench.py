@@ -172,7 +172,7 @@ def cpu_sample(cid: int, A_host_rows, B_host, target_s: float):
 
 def host_panels_for_baseline(cid, n, device):
     """A row panel and the full B on the host (the oracle's inputs)."""
-    rows = 512
+    rows = min(n, 4096)
     A = gen_panel(cid, "A", rows, n, 0, 0, device).cpu().numpy()
     B = gen_panel(cid, "B", n, n, 0, 0, device).cpu().numpy()
     return A, B
