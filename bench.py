@@ -51,13 +51,38 @@ def _measured(name, key, default):
         return default
 
 
+def _packed(op_prefix, default):
+    p = os.path.join(REPO, "profiles", "r01_packed_ops_microbench.jsonl")
+    try:
+        for line in open(p):
+            d = json.loads(line)
+            if d["op"].startswith(op_prefix):
+                return d["terms_per_s"]
+    except Exception:
+        pass
+    return default
+
+
 def peaks(sm_max_mhz: float):
+    """Roofline denominators in ops/s (1 term = 2 ops), all measured on this pool's B200s
+    (profiles/r01_*); 'issue' is BASELINE's nominal CUDA-core roofline."""
     dmma = 2 * _measured("r01_peaks_microbench.json", "dmma_terms_per_s_b8", 1.8551e13)
     cublas = 1e12 * _measured("r01_cublas_dgemm.json", "cublas_dgemm_n16384_tflops", 36.08)
     issue = SM_COUNT_NOMINAL * 128 * sm_max_mhz * 1e6          # BASELINE: 2 instr / term
     vmin = 2 * _measured("r01_peaks_microbench.json", "viaddmnmx_terms_per_s_b8", 1.8471e13)
     return {"fp64_tensor": max(dmma, cublas), "fp64_dmma_ubench": dmma, "cublas_dgemm": cublas,
-            "issue": issue, "viaddmnmx_ubench": vmin}
+            "issue": issue, "viaddmnmx_ubench": vmin,
+            "idp4a_ubench": 2 * _packed("dp4a", 7.4066e13),
+            "viaddmnmx_s16x2_ubench": 2 * _packed("viaddmnmx_s16x2", 3.6974e13)}
+
+
+# path -> (roofline key, instruction mix) for the dominant kernel
+PATH_PEAK = {
+    "dmma_f64": ("fp64_tensor", "DMMA.8x8x4 (FP64 tensor core)"),
+    "simt_i64_dp4a": ("idp4a_ubench", "IDP.4A: 4 int8 terms per lane-op"),
+    "simt_f32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
+    "simt_i32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
+}
 
 
 # ---- clocks during the timed region ----------------------------------------
@@ -267,15 +292,21 @@ def main():
     pk = peaks(clocks["sm_max_mhz"] or 1965.0)
     local_ops = 2.0 * dmm.m * dmm.nn * dmm.k
     achieved = local_ops / kern_s
-    if s.id == "float":
-        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk["fp64_tensor"] / 1e12,
+    key, mix = PATH_PEAK.get(st["path_name"], ("issue", "1 lane-op per term (FADD2+FMNMX3 / "
+                                                 "VIADDMNMX / IMAD), 64 terms/clk/SM"))
+    if key == "fp64_tensor":
+        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
                 "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
-                "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json has no fp64)"}
+                "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json "
+                "has no fp64 entry)"}
     else:
-        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": pk["issue"] / 1e12,
-                "unit": "Tops/s", "peak_source": "BASELINE issue roofline: 148 SMs x 128 lanes x "
-                "sm_max_mhz (2 instructions per term); viaddmnmx ubench = %.2f Tops/s"
-                % (pk["viaddmnmx_ubench"] / 1e12)}
+        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
+                "unit": "Tops/s", "peak_source": ("measured instruction-mix peak, "
+                "profiles/r01_packed_ops_microbench.jsonl / r01_peaks_microbench.json"
+                if key != "issue" else "BASELINE issue roofline: 148 SMs x 128 lanes x sm_max_mhz")}
+        roof["baseline_issue_roofline"] = pk["issue"] / 1e12
+        roof["frac_of_baseline_issue_roofline"] = achieved / pk["issue"]
+    roof["instruction_mix"] = mix
     roof["frac"] = roof["achieved"] / roof["peak"]
     roof["traffic"] = _ncu_traffic(cid, st["path_name"])
     roof["kernel_ms"] = kern_s * 1e3

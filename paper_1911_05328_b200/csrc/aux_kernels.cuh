@@ -36,6 +36,44 @@ __global__ void range_absmax_kernel(const T* X, long long rows, long long cols, 
     if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
 }
 
+// Range + integrality guard for the 16-bit (min,+) path: out[0] = max |x| over
+// finite entries (rounded up), out[1] = 1 if any entry is non-integral, NaN,
+// -inf, or (for int32) would not be exact.  +inf / INT32_MAX are skipped.
+template <class T>
+__global__ void range_minplus_kernel(const T* X, long long rows, long long cols, long long ld,
+                                     unsigned long long* out) {
+    unsigned long long m = 0;
+    unsigned bad = 0;
+    long long total = rows * cols;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cols, c = idx - r * cols;
+        T v = X[r * ld + c];
+        if constexpr (sizeof(T) == 4 && ((T)0.5 != 0)) {          // float
+            float f = (float)v;
+            if (f == __int_as_float(0x7f800000)) continue;
+            if (!(f == rintf(f)) || fabsf(f) > 1e9f) { bad = 1; continue; }
+            unsigned long long a = (unsigned long long)fabsf(f);
+            m = a > m ? a : m;
+        } else {                                                    // int32
+            if ((long long)v == 0x7fffffffLL) continue;
+            long long sv = (long long)v;
+            unsigned long long a = (unsigned long long)(sv < 0 ? -sv : sv);
+            m = a > m ? a : m;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+        m = v > m ? v : m;
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        if (m) atomicMax(&out[0], m);
+        if (bad) atomicOr(&out[1], 1ull);
+    }
+}
+
 // ---- packing ---------------------------------------------------------------
 // Element conversion into the packed domain, with the pad value (annihilator
 // of the product, so padded k terms contribute the additive identity).
@@ -53,6 +91,67 @@ struct ConvI32Vmin {    // int32 tropical -> VIADDMNMX encoding, INT32_MAX -> 2^
 struct ConvI64ToI32 {   // int64 ring, range-guarded narrow path
     static STARMM_DEV int cvt(long long x) { return (int)x; }
 };
+// (min,+) -> int16 encoding (+inf -> 16383), duplicated into both halves (A operand)
+template <class T> STARMM_DEV unsigned s16_enc(T x);
+template <> STARMM_DEV unsigned s16_enc<float>(float x) {
+    return x == __int_as_float(0x7f800000) ? 16383u : ((unsigned)(int)x & 0xffffu);
+}
+template <> STARMM_DEV unsigned s16_enc<int>(int x) {
+    return x == 0x7fffffff ? 16383u : ((unsigned)x & 0xffffu);
+}
+struct ConvS16Dup {
+    template <class T> static STARMM_DEV unsigned cvt(T x) { unsigned e = s16_enc<T>(x); return e | (e << 16); }
+};
+
+// int64 ring -> s8x4 words along k: A (rows x kdim) -> P[kp/4][rowsp]
+__global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long kdim, long long lda,
+                                   int* P, long long rowsp, long long kp) {
+    long long total = (kp / 4) * rowsp;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long kw = idx / rowsp, r = idx - kw * rowsp;
+        unsigned w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            long long k = kw * 4 + i;
+            long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
+            w |= ((unsigned)(v & 0xff)) << (8 * i);
+        }
+        P[idx] = (int)w;
+    }
+}
+// B (kdim x cols) -> P[kp/4][colsp]
+__global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
+                                   int* P, long long colsp, long long kp) {
+    long long total = (kp / 4) * colsp;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long kw = idx / colsp, c = idx - kw * colsp;
+        unsigned w = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            long long k = kw * 4 + i;
+            long long v = (c < cols && k < kdim) ? B[k * ldb + c] : 0;
+            w |= ((unsigned)(v & 0xff)) << (8 * i);
+        }
+        P[idx] = (int)w;
+    }
+}
+// (min,+) B (kdim x cols) -> P[kp][colsp/2] words (enc(B[k][2w]), enc(B[k][2w+1]))
+template <class T>
+__global__ void pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, long long ldb,
+                                    unsigned* P, long long colsp, long long kp) {
+    long long wpr = colsp / 2;
+    long long total = kp * wpr;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long k = idx / wpr, w = idx - k * wpr;
+        long long c0 = 2 * w;
+        unsigned lo = (k < kdim && c0 < cols) ? s16_enc<T>(B[k * ldb + c0]) : 16383u;
+        unsigned hi = (k < kdim && c0 + 1 < cols) ? s16_enc<T>(B[k * ldb + c0 + 1]) : 16383u;
+        P[idx] = lo | (hi << 16);
+    }
+}
 
 // A (rows x kdim, ld) -> P[kp/G][rowsp][G], transposing through a 32x32 smem tile
 // so that both the global reads and the packed writes are coalesced.

@@ -23,9 +23,15 @@
 // annihilator, so a k-stage is a contiguous slab that 16-byte cp.async copies
 // verbatim and every thread reads its operands with conflict-free LDS.128.
 //
-// CTA tile 128x128, 256 threads, 8x8 outputs per thread, k-stage 16, 3-deep
-// cp.async ring.  Warps are 4 (rows) x 8 (cols) threads so A reads broadcast
-// across 8 lanes and B reads across 4.
+//   PolI8Dp4a    int64 (+,x) when |x| <= 127 and K*max|a|*max|b| < 2^31: IDP.4A
+//                (dp4a) over four packed int8 k terms -- 4 terms per lane-op.
+//   PolS16x2Min  integer-valued (min,+) with |x| <= 4096: VIADDMNMX.S16x2 on two
+//                output columns per lane-op.
+//
+// CTA tile 128 x (128*OUTS), 256 threads, 8x8 accumulators per thread (each
+// accumulator holds OUTS outputs), k-stage Pol::BK, 3-deep cp.async ring.  Warps
+// are 4 (rows) x 8 (cols) threads so A reads broadcast across 8 lanes and B
+// reads across 4.
 #pragma once
 #include "common.cuh"
 #include "writeback.cuh"
@@ -37,6 +43,7 @@ namespace starmm {
 struct PolF32Pair {        // packed element float, G = 2, accumulator float
     using Tp = float; using Acc = float;
     static constexpr int G = 2;
+    static constexpr int KSTEP = 2, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     // a = (A[i][k], A[i][k+1]), b = (B[k][j], B[k+1][j])
     static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
@@ -47,12 +54,14 @@ struct PolF32Pair {        // packed element float, G = 2, accumulator float
 struct PolF32Single {      // fp32 (min,+) one k at a time: FADD + FMNMX (ptxas may fuse k pairs)
     using Tp = float; using Acc = float;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fminf(c, a + b); }
 };
 struct PolF32PairMin2 {    // FADD2 + two 2-input FMNMX
     using Tp = float; using Acc = float;
     static constexpr int G = 2;
+    static constexpr int KSTEP = 2, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
         float2 v = __fadd2_rn(a, b);
@@ -63,18 +72,21 @@ struct PolF32PairMin2 {    // FADD2 + two 2-input FMNMX
 struct PolF64Min {
     using Tp = double; using Acc = double;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return __longlong_as_double(0x7ff0000000000000ULL); }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fmin(c, a + b); }
 };
 struct PolI32Vmin {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return 0x7fffffff; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s32(a, b, c); }
 };
 struct PolI32Sat {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return 0x7fffffff; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
         long long s = (long long)a + (long long)b;
@@ -86,6 +98,7 @@ struct PolI32Sat {
 struct PolI64 {
     using Tp = long long; using Acc = unsigned long long;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return 0ull; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
         c += (unsigned long long)a * (unsigned long long)b;
@@ -94,9 +107,31 @@ struct PolI64 {
 struct PolI64Narrow {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
+    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static STARMM_DEV Acc init() { return 0; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c += a * b; }
 };
+
+// int64 (+,x) when every |x| <= 127 and K*max|a|*max|b| < 2^31 (range guard):
+// four k terms per IDP.4A (dp4a: int8x4 dot + int32 accumulate) -- exact, and
+// 4 terms per lane-instruction (255 terms/clk/SM measured, tools/microbench/packed.cu).
+struct PolI8Dp4a {
+    using Tp = int; using Acc = int;            // Tp packs A[i][4q..4q+3] / B[4q..4q+3][j] as s8x4
+    static constexpr int G = 1, KSTEP = 4, OUTS = 1, BK = 64;
+    static STARMM_DEV Acc init() { return 0; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __dp4a(a, b, c); }
+};
+// (min,+) on integer-valued data with every finite |x| <= 4096 (range guard):
+// VIADDMNMX.S16x2 computes min(a+b, c) for two output COLUMNS at once (a is
+// duplicated into both halves at packing time); +inf is encoded 16383, so no
+// sum can overflow int16 and any result > 8192 involved +inf.  127 terms/clk/SM.
+struct PolS16x2Min {
+    using Tp = unsigned; using Acc = unsigned;
+    static constexpr int G = 1, KSTEP = 1, OUTS = 2, BK = 32;
+    static STARMM_DEV Acc init() { return 0x7fff7fffu; }
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s16x2(a, b, c); }
+};
+constexpr int S16_INF_ENC = 16383, S16_FINITE_MAX = 4096, S16_INF_THRESHOLD = 8192;
 
 // Accumulator -> output element conversion per (policy, output semiring).
 template <class Pol, class Sr> struct Finish;
@@ -127,17 +162,35 @@ template <> struct Finish<PolI64, SrInt64> {
 template <> struct Finish<PolI64Narrow, SrInt64> {
     static STARMM_DEV long long out(int v) { return (long long)v; }
 };
+template <> struct Finish<PolI8Dp4a, SrInt64> {
+    static STARMM_DEV long long out(int v) { return (long long)v; }
+};
+template <> struct Finish<PolS16x2Min, SrTropF32> {
+    static STARMM_DEV float out2(unsigned v, int h) {
+        int x = (int)(short)(h ? (v >> 16) : (v & 0xffffu));
+        return x > S16_INF_THRESHOLD ? __int_as_float(0x7f800000) : (float)x;
+    }
+};
+template <> struct Finish<PolS16x2Min, SrTropI32> {
+    static STARMM_DEV int out2(unsigned v, int h) {
+        int x = (int)(short)(h ? (v >> 16) : (v & 0xffffu));
+        return x > S16_INF_THRESHOLD ? 0x7fffffff : x;
+    }
+};
 
 namespace simt {
-constexpr int BM = 128, BN = 128, BK = 16, STAGES = 3, THREADS = 256;
+constexpr int BM = 128, BNW = 128, STAGES = 3, THREADS = 256;   // BNW: B positions per tile row
+template <class Pol> constexpr int bn() { return BNW * Pol::OUTS; }   // output columns per tile
 template <class Pol>
-constexpr int smem_bytes() { return STAGES * (BM + BN) * BK * (int)sizeof(typename Pol::Tp) + 64; }
+constexpr int smem_bytes() {
+    return STAGES * (BM + BNW) * (Pol::BK / Pol::KSTEP) * Pol::G * (int)sizeof(typename Pol::Tp) + 64;
+}
 }  // namespace simt
 
 struct SimtParams {
-    const void* Ap;   // packed [Kp/G][Mp][G]
-    const void* Bp;   // packed [Kp/G][Np][G]
-    long long Mp, Np; // padded extents (multiples of 128)
+    const void* Ap;   // packed [Kp/KSTEP][Mp][G]
+    const void* Bp;   // packed [Kp/KSTEP][Np/OUTS][G]
+    long long Mp, Np; // padded extents (multiples of the tile)
     TaskGrid g;
     WbParams w;
 };
@@ -147,12 +200,13 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     using namespace simt;
     using Tp = typename Pol::Tp;
     using Acc = typename Pol::Acc;
-    constexpr int G = Pol::G;
-    constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // x-positions per 16-byte load
+    constexpr int G = Pol::G, KSTEP = Pol::KSTEP, OUTS = Pol::OUTS, BK = Pol::BK;
+    constexpr int BN = BNW * OUTS;                      // output columns per tile
+    constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // positions per 16-byte load
     constexpr int NQ = 8 / VEC;                         // 16-byte loads per operand per k-group
-    constexpr int KG = BK / G;                          // k-groups per stage
+    constexpr int KG = BK / KSTEP;                      // k-groups per stage
     constexpr int A_STAGE = KG * BM * G;                // elements
-    constexpr int B_STAGE = KG * BN * G;
+    constexpr int B_STAGE = KG * BNW * G;
     constexpr int CHUNK = 16 / (int)sizeof(Tp);         // elements per cp.async
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Tp* As = reinterpret_cast<Tp*>(smem_raw);
@@ -174,10 +228,11 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         int pair_seen = PAIR_EMPTY;
         if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
 
-        // k-group row kg of A covers Mp*G contiguous elements
-        const long long kg0 = (long long)s * g.kslice / G;
+        // k-group row kg of A covers Mp*G contiguous elements, of B (Np/OUTS)*G
+        const long long kg0 = (long long)s * g.kslice / KSTEP;
+        const long long Nw = p.Np / OUTS;
         const Tp* Ag = Ap + kg0 * p.Mp * G + (long long)tm * BM * G;
-        const Tp* Bg = Bp + kg0 * p.Np * G + (long long)tn * BN * G;
+        const Tp* Bg = Bp + kg0 * Nw * G + (long long)tn * BNW * G;
 
         auto load_stage = [&](int kt, int stage) {
             const long long kgs = (long long)kt * KG;
@@ -190,7 +245,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                 int c = tid + i * THREADS;
                 int r = c / ROW_CHUNKS, q = c % ROW_CHUNKS;
                 cp_async16(as + r * BM * G + q * CHUNK, Ag + (kgs + r) * p.Mp * G + q * CHUNK);
-                cp_async16(bs + r * BN * G + q * CHUNK, Bg + (kgs + r) * p.Np * G + q * CHUNK);
+                cp_async16(bs + r * BNW * G + q * CHUNK, Bg + (kgs + r) * Nw * G + q * CHUNK);
             }
         };
 
@@ -222,7 +277,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                     *reinterpret_cast<int4*>(&a[q * VEC * G]) =
                         *reinterpret_cast<const int4*>(as + kg * BM * G + q * 16 * VEC * G);
                     *reinterpret_cast<int4*>(&b[q * VEC * G]) =
-                        *reinterpret_cast<const int4*>(bs + kg * BN * G + q * 16 * VEC * G);
+                        *reinterpret_cast<const int4*>(bs + kg * BNW * G + q * 16 * VEC * G);
                 }
 #pragma unroll
                 for (int i = 0; i < 8; ++i)
@@ -248,8 +303,13 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     int r = (i / VEC) * 16 * VEC + ty * VEC + (i % VEC);
-                    int c = (j / VEC) * 16 * VEC + tx * VEC + (j % VEC);
-                    f(r, c, (T)Finish<Pol, Sr>::out(acc[i][j]));
+                    int w = (j / VEC) * 16 * VEC + tx * VEC + (j % VEC);   // B position
+                    if constexpr (OUTS == 1) {
+                        f(r, w, (T)Finish<Pol, Sr>::out(acc[i][j]));
+                    } else {
+                        f(r, 2 * w, (T)Finish<Pol, Sr>::out2(acc[i][j], 0));
+                        f(r, 2 * w + 1, (T)Finish<Pol, Sr>::out2(acc[i][j], 1));
+                    }
                 }
         });
     }

@@ -120,8 +120,44 @@ namespace {
 // ---- kernel instantiation table ----------------------------------------------
 enum PathId : int {
     PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
-    PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8
+    PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
+    PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11
 };
+
+// Tile / packing geometry of one kernel path (mirrors the device-side constants).
+struct PathShape {
+    int bm, bn, bk, per_sm;
+    long long a_bytes_per_km;   // packed A bytes per (k, m) element, x1000 for dp4a's 1 byte
+    long long b_bytes_per_kn;
+};
+template <class Pol>
+PathShape simt_shape() {
+    PathShape sh;
+    sh.bm = simt::BM; sh.bn = simt::bn<Pol>(); sh.bk = Pol::BK; sh.per_sm = 1;
+    // bytes of packed operand per original (k, x) element
+    sh.a_bytes_per_km = (long long)Pol::G * sizeof(typename Pol::Tp) * 1000 / Pol::KSTEP;
+    sh.b_bytes_per_kn = (long long)Pol::G * sizeof(typename Pol::Tp) * 1000 / (Pol::KSTEP * Pol::OUTS);
+    return sh;
+}
+PathShape path_shape(int path) {
+    switch (path) {
+    case PATH_DMMA_F64: {
+        PathShape sh{DmmaProd::BM, DmmaProd::BN, DmmaProd::BK, DmmaProd::MIN_BLOCKS, 8000, 8000};
+        return sh;
+    }
+    case PATH_SIMT_I64: return simt_shape<PolI64>();
+    case PATH_SIMT_I64_NARROW: return simt_shape<PolI64Narrow>();
+    case PATH_SIMT_F32_PAIR: return simt_shape<PolF32Pair>();
+    case PATH_SIMT_I32_CARRIER: return simt_shape<PolF32Pair>();
+    case PATH_SIMT_I32_VMIN: return simt_shape<PolI32Vmin>();
+    case PATH_SIMT_I32_SAT: return simt_shape<PolI32Sat>();
+    case PATH_SIMT_F64_MIN: return simt_shape<PolF64Min>();
+    case PATH_SIMT_I64_DP4A: return simt_shape<PolI8Dp4a>();
+    case PATH_SIMT_F32_S16X2: return simt_shape<PolS16x2Min>();
+    case PATH_SIMT_I32_S16X2: return simt_shape<PolS16x2Min>();
+    }
+    return simt_shape<PolI64>();
+}
 
 template <class Pol, class Sr>
 int launch_simt(const SimtParams& p, int grid, cudaStream_t s) {
@@ -210,6 +246,25 @@ int launch_pack(const void* A, long long lda, const void* B, long long ldb, long
 int occupancy_grid(starmm_plan* P, int per_sm, long long tasks) {
     long long g = (long long)P->sms * per_sm;
     return (int)std::max<long long>(1, std::min<long long>(g, tasks));
+}
+
+// (max finite |x|, non-integral flag) of A and B for the 16-bit (min,+) path.
+template <class T>
+int range_minplus_pair(starmm_plan* P, const void* A, long long lda, const void* B, long long ldb,
+                       cudaStream_t s, unsigned long long* mx, bool* bad) {
+    CK(cudaMemsetAsync(P->d_range, 0, 2 * sizeof(unsigned long long), s));
+    range_minplus_kernel<T><<<grid_blocks(P->m * P->k), 256, 0, s>>>((const T*)A, P->m, P->k, lda,
+                                                                    P->d_range);
+    CK(cudaGetLastError());
+    range_minplus_kernel<T><<<grid_blocks(P->k * P->n), 256, 0, s>>>((const T*)B, P->k, P->n, ldb,
+                                                                    P->d_range);
+    CK(cudaGetLastError());
+    unsigned long long h[2];
+    CK(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *mx = h[0];
+    *bad = h[1] != 0;
+    return STARMM_OK;
 }
 
 // max |x| of A and B via the range kernels; returns host values.
@@ -367,9 +422,17 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     // ---- path selection (range guards are exact-by-construction checks) ----
     int path = 0;
     if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
-    else if (P->sr == STARMM_SR_TROPICAL_F32) path = PATH_SIMT_F32_PAIR;
     else if (P->sr == STARMM_SR_TROPICAL_F64) path = PATH_SIMT_F64_MIN;
-    else if (P->sr == STARMM_SR_INT64) {
+    else if (P->sr == STARMM_SR_TROPICAL_F32) {
+        path = PATH_SIMT_F32_PAIR;
+        if (fast_ok) {
+            unsigned long long mx; bool bad;
+            TRY(range_minplus_pair<float>(P, A, lda, B, ldb, s, &mx, &bad));
+            launches += 2;
+            // integer-valued with |x| <= 4096: int16 sums cannot overflow, exact
+            if (!bad && mx <= (unsigned long long)S16_FINITE_MAX) path = PATH_SIMT_F32_S16X2;
+        }
+    } else if (P->sr == STARMM_SR_INT64) {
         path = PATH_SIMT_I64;
         if (fast_ok) {
             unsigned long long ma, mb;
@@ -378,7 +441,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
             // exact iff every partial sum fits int32: K * max|a| * max|b| < 2^31
             long double bound = (long double)P->k * (long double)ma * (long double)mb;
             if (ma < (1ull << 31) && mb < (1ull << 31) && bound < 2147483648.0L)
-                path = PATH_SIMT_I64_NARROW;
+                path = (ma <= 127 && mb <= 127) ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64_NARROW;
         }
     } else {  // tropical_i32
         path = PATH_SIMT_I32_SAT;
@@ -387,18 +450,20 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
             TRY(range_pair<int>(P, A, lda, B, ldb, 1, s, &ma, &mb));
             launches += 2;
             unsigned long long mx = std::max(ma, mb);
-            if (mx <= (1ull << 23)) path = PATH_SIMT_I32_CARRIER;      // fp32-exact sums
-            else if (mx < (1ull << 28)) path = PATH_SIMT_I32_VMIN;     // no int32 overflow
+            if (mx <= (unsigned long long)S16_FINITE_MAX) path = PATH_SIMT_I32_S16X2;  // int16 exact
+            else if (mx <= (1ull << 23)) path = PATH_SIMT_I32_CARRIER;                // fp32-exact sums
+            else if (mx < (1ull << 28)) path = PATH_SIMT_I32_VMIN;                    // no int32 overflow
         }
     }
     const bool is_dmma = (path == PATH_DMMA_F64);
-    const int BK = is_dmma ? DmmaProd::BK : simt::BK;
+    const PathShape shape = path_shape(path);
+    const int BK = shape.bk;
 
     // ---- the split: leaf tasks = output tiles x k-slices ----
-    const int TBM = is_dmma ? DmmaProd::BM : simt::BM, TBN = is_dmma ? DmmaProd::BN : simt::BN;
+    const int TBM = shape.bm, TBN = shape.bn;
     const long long tiles_m = (P->m + TBM - 1) / TBM, tiles_n = (P->n + TBN - 1) / TBN;
     const long long tiles = tiles_m * tiles_n;
-    const int per_sm = is_dmma ? DmmaProd::MIN_BLOCKS : 1;
+    const int per_sm = shape.per_sm;
     const int gpu_workers = P->sms * per_sm;             // persistent CTAs (the GPU workers)
     int s_log2;
     if (P->algo == STARMM_CO2) {
@@ -424,7 +489,10 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
 
     TaskGrid g;
     g.tiles_m = (int)tiles_m; g.tiles_n = (int)tiles_n; g.S = S; g.log2S = s_log2;
-    g.tar_levels = tar_levels; g.group_m = 8; g.kslice = kslice;
+    g.tar_levels = tar_levels; g.kslice = kslice;
+    // raster groups sized so one wave of resident CTAs covers a near-square block of
+    // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
+    g.group_m = is_dmma ? 24 : 12;
     const long long ntasks = tiles * S;
     if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
     g.num_tasks = (int)ntasks;
@@ -457,11 +525,11 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
                 opA = pa; opB = pb; olda = Kp; oldb = Np;
             }
         } else {
-            int pe = (path == PATH_SIMT_I64 || path == PATH_SIMT_F64_MIN) ? 8 : 4;
             void *pa, *pb;
-            if ((rc = stage_acquire((size_t)(Mp * Kp * pe), &pa))) break;
-            if ((rc = stage_acquire((size_t)(Kp * Np * pe), &pb))) break;
+            if ((rc = stage_acquire((size_t)(Mp * Kp * shape.a_bytes_per_km / 1000), &pa))) break;
+            if ((rc = stage_acquire((size_t)(Kp * Np * shape.b_bytes_per_kn / 1000), &pb))) break;
             const float finf = std::numeric_limits<float>::infinity();
+            const unsigned s16pad = 16383u | (16383u << 16);
             switch (path) {
             case PATH_SIMT_F32_PAIR:
                 rc = launch_pack<float, float, 2, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
@@ -485,6 +553,30 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
                 const double dinf = std::numeric_limits<double>::infinity();
                 rc = launch_pack<double, double, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa,
                                                                    pb, Mp, Np, Kp, dinf, s); break;
+            }
+            case PATH_SIMT_I64_DP4A:
+                pack_a_s8x4_kernel<<<grid_blocks((Kp / 4) * Mp), 256, 0, s>>>(
+                    (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp);
+                pack_b_s8x4_kernel<<<grid_blocks((Kp / 4) * Np), 256, 0, s>>>(
+                    (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp);
+                rc = cuda_status(cudaGetLastError());
+                break;
+            case PATH_SIMT_F32_S16X2:
+            case PATH_SIMT_I32_S16X2: {
+                dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
+                if (path == PATH_SIMT_F32_S16X2) {
+                    pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                        (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad);
+                    pack_b_s16x2_kernel<float><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                        (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp);
+                } else {
+                    pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                        (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad);
+                    pack_b_s16x2_kernel<int><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                        (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp);
+                }
+                rc = cuda_status(cudaGetLastError());
+                break;
             }
             }
             if (rc) break;
@@ -560,6 +652,9 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
             case PATH_SIMT_I64: rc = launch_simt<PolI64, SrInt64>(sp, grid, s); break;
             case PATH_SIMT_I64_NARROW: rc = launch_simt<PolI64Narrow, SrInt64>(sp, grid, s); break;
             case PATH_SIMT_F64_MIN: rc = launch_simt<PolF64Min, SrTropF64>(sp, grid, s); break;
+            case PATH_SIMT_I64_DP4A: rc = launch_simt<PolI8Dp4a, SrInt64>(sp, grid, s); break;
+            case PATH_SIMT_F32_S16X2: rc = launch_simt<PolS16x2Min, SrTropF32>(sp, grid, s); break;
+            case PATH_SIMT_I32_S16X2: rc = launch_simt<PolS16x2Min, SrTropI32>(sp, grid, s); break;
             }
         }
         if (rc) break;
@@ -602,7 +697,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     }
 
     P->st.tasks = ntasks;
-    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * (is_dmma ? DmmaProd::MIN_BLOCKS : 1));
+    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * shape.per_sm);
     P->st.ksplit = S;
     P->st.tar_levels = tar_levels;
     P->st.kernel_launches = launches;

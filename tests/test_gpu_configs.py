@@ -63,7 +63,7 @@ def _check_tiles(cid, A, B, C0, Cdev, count):
 
 def test_config2_int64_n4096():
     A, B, C0, C, Am, Bm, st = _run(2)
-    assert st["path_name"] == "simt_i64_narrow_i32"
+    assert st["path_name"] == "simt_i64_dp4a"
     _check_tiles(2, A, B, C0, C.data, count=64)
     # checksum of checksums, exact mod 2^64 (torch int64 arithmetic wraps)
     lhs = C.data.sum()
@@ -86,6 +86,7 @@ def test_config2_general_int64_kernel_full_size():
 
 def test_config3_tropical_f32_n8192():
     A, B, C0, C, Am, Bm, st = _run(3)
+    assert st["path_name"] == "simt_f32_s16x2_viaddmnmx"
     _check_tiles(3, A, B, C0, C.data, count=32)
     # idempotence: folding the same product again changes nothing
     first = C.data.clone()
@@ -93,11 +94,14 @@ def test_config3_tropical_f32_n8192():
     with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
         sm.run_algorithm(ex, "star", C, Am, Bm, s)
     assert torch.equal(C.data, first)
-    # schedule invariance (exact semiring): co2 and tar give the same bits
-    for algo in ("co2", "tar"):
+    # schedule invariance (exact semiring): co2 and tar give the same bits, and so
+    # does the general fp32 FADD2/FMNMX3 kernel (fast path off)
+    for algo, fast in (("co2", True), ("tar", True), ("star", False)):
         C2 = sm.Matrix(C0, s)
-        with sm.Executor(sm.Config(base_dim=64, workers=148, ksplit=1)) as ex:
+        with sm.Executor(sm.Config(base_dim=64, workers=148, ksplit=1, fastpath=fast)) as ex:
             sm.run_algorithm(ex, algo, C2, Am, Bm, s)
+            if not fast:
+                assert ex.last_stats["path_name"] == "simt_f32_fadd2_fmnmx3"
         assert torch.equal(C2.data, first), algo
 
 

@@ -101,7 +101,9 @@ def _path_of(algo, s, C0, A, B, cfg):
         return C.numpy(), ex.last_stats["path_name"]
 
 
-@pytest.mark.parametrize("lo,hi,expect", [(-16, 17, "simt_i64_narrow_i32"),
+@pytest.mark.parametrize("lo,hi,expect", [(-16, 17, "simt_i64_dp4a"),
+                                          (-127, 128, "simt_i64_dp4a"),
+                                          (-1000, 1001, "simt_i64_narrow_i32"),
                                           (-2 ** 40, 2 ** 40, "simt_i64")])
 def test_int64_paths_bitexact(lo, hi, expect):
     n = 384
@@ -123,7 +125,9 @@ def test_int64_wraps_mod_2_64():
     assert got.tolist() == [[0, 0], [0, 0]]
 
 
-@pytest.mark.parametrize("hi,expect", [(1000, "simt_i32_via_f32_carrier"),
+@pytest.mark.parametrize("hi,expect", [(1000, "simt_i32_s16x2_viaddmnmx"),
+                                       (4096, "simt_i32_s16x2_viaddmnmx"),
+                                       (100000, "simt_i32_via_f32_carrier"),
                                        (1 << 26, "simt_i32_viaddmnmx"),
                                        (1 << 30, "simt_i32_saturating")])
 def test_i32_tropical_paths_bitexact(hi, expect):
@@ -137,6 +141,32 @@ def test_i32_tropical_paths_bitexact(hi, expect):
     want = C0.copy()
     O.gemm_fold(O.SR_TROP_I32, want, A, B)
     got, path = _path_of("co2", sm.TROPICAL_I32, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
+    assert path == expect
+    assert np.array_equal(got, want)
+
+
+@pytest.mark.parametrize("kind,expect", [("int_small", "simt_f32_s16x2_viaddmnmx"),
+                                         ("int_4096", "simt_f32_s16x2_viaddmnmx"),
+                                         ("int_large", "simt_f32_fadd2_fmnmx3"),
+                                         ("fractional", "simt_f32_fadd2_fmnmx3"),
+                                         ("neg_inf", "simt_f32_fadd2_fmnmx3")])
+def test_f32_tropical_paths_bitexact(kind, expect):
+    n = 288
+    rng = np.random.default_rng(13)
+    hi = {"int_small": 100, "int_4096": 4096, "int_large": 5000}.get(kind, 100)
+    A = rng.integers(-hi, hi + 1, (n, n)).astype(np.float32)
+    B = rng.integers(-hi, hi + 1, (n, n)).astype(np.float32)
+    if kind == "fractional":
+        A += 0.25
+    if kind == "neg_inf":
+        A[3, 5] = -np.inf
+    A[rng.random(A.shape) < 0.2] = np.inf
+    B[rng.random(B.shape) < 0.2] = np.inf
+    C0 = rng.integers(-2 * hi, 2 * hi, (n, n)).astype(np.float32)
+    C0[rng.random(C0.shape) < 0.1] = np.inf
+    want = C0.copy()
+    O.gemm_fold(O.SR_TROP_F32, want, A, B)
+    got, path = _path_of("co2", sm.TROPICAL_F32, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
     assert path == expect
     assert np.array_equal(got, want)
 

@@ -43,13 +43,11 @@ int main(int argc, char** argv) {
     cudaMalloc(&cnt, 64 * 8);
     cudaMemset(A, 0, (size_t)n * n * 8); cudaMemset(B, 0, (size_t)n * n * 8); cudaMemset(C, 0, (size_t)n * n * 8);
     using P = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
-    run<P>("64x128_s4_g8", n, A, B, C, cnt, sms, 8, true);
-    run<P>("64x128_s4_g8_nonpersistent", n, A, B, C, cnt, sms, 8, false);
-    run<P>("64x128_s4_g4", n, A, B, C, cnt, sms, 4, true);
-    run<P>("64x128_s4_g16", n, A, B, C, cnt, sms, 16, true);
-    run<P>("64x128_s4_g32", n, A, B, C, cnt, sms, 32, true);
-    run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>>("64x128_s4_g8_db", n, A, B, C, cnt, sms, 8, true);
-    run<DmmaCfg<64, 128, 1, 4, 16, 4, 2>>("64x128_1x4_s4_g8", n, A, B, C, cnt, sms, 8, true);
-    run<DmmaCfg<64, 256, 2, 4, 16, 3, 1>>("64x256_2x4_s3_occ1", n, A, B, C, cnt, sms, 8, true);
+    int only_g = argc > 2 ? atoi(argv[2]) : 0;
+    for (int gm : {4, 8, 16, 24, 32, 64}) {
+        if (only_g && gm != only_g) continue;
+        char name[64]; snprintf(name, sizeof name, "64x128_s4_g%d", gm);
+        run<P>(name, n, A, B, C, cnt, sms, gm, true);
+    }
     return 0;
 }

@@ -11,7 +11,7 @@ void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long lon
     SimtParams p{};
     p.Ap = Ap; p.Bp = Bp; p.Mp = n; p.Np = n;
     TaskGrid& g = p.g;
-    g.tiles_m = n / 128; g.tiles_n = n / 128; g.S = 1; g.log2S = 0; g.group_m = 8; g.kslice = n;
+    g.tiles_m = n / 128; g.tiles_n = n / simt::bn<Pol>(); g.S = 1; g.log2S = 0; g.group_m = 8; g.kslice = n;
     g.num_tasks = g.tiles_m * g.tiles_n;
     WbParams& w = p.w;
     w.mode_base = 0; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
@@ -39,6 +39,8 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
+    run<PolI8Dp4a, SrInt64, 1>("i64_dp4a_occ1", n, A, B, C, cnt, sms);
+    run<PolS16x2Min, SrTropF32, 1>("minplus_s16x2_occ1", n, A, B, C, cnt, sms);
     run<PolF32Pair, SrTropF32, 1>("f32_fadd2_fmnmx3_occ1", n, A, B, C, cnt, sms);
     run<PolF32Pair, SrTropF32, 2>("f32_fadd2_fmnmx3_occ2", n, A, B, C, cnt, sms);
     run<PolF32Single, SrTropF32, 1>("f32_fadd_fmnmx_occ1", n, A, B, C, cnt, sms);
