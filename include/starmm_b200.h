@@ -126,6 +126,13 @@ int  starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mo
                         int ksplit_log2 /* -1 = auto */, int device, int flags);
 int  starmm_execute(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,
                     const void* B, int64_t ldb, void* stream);
+/* Same computation with C, A and B in HOST memory (pinned for full overlap):
+ * B is uploaded once, A/C stream through in blocks of `block_rows` rows (0 = auto)
+ * overlapping the tile kernels, finished C blocks stream back.  Blocking.
+ * The reference's entry points take host (numpy) matrices (classic.py:294-316);
+ * this is their host-buffer form. */
+int  starmm_execute_host(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,
+                         const void* B, int64_t ldb, void* stream, int64_t block_rows);
 int  starmm_plan_stats(starmm_plan* plan, starmm_stats* out);
 int  starmm_plan_reset_stats(starmm_plan* plan);
 void starmm_plan_destroy(starmm_plan* plan);

@@ -78,6 +78,8 @@ def lib():
         L.starmm_plan_create.restype = ci
         L.starmm_execute.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp]
         L.starmm_execute.restype = ci
+        L.starmm_execute_host.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64]
+        L.starmm_execute_host.restype = ci
         L.starmm_plan_stats.argtypes = [vp, ctypes.POINTER(StarmmStats)]
         L.starmm_plan_stats.restype = ci
         L.starmm_plan_reset_stats.argtypes = [vp]
@@ -124,6 +126,11 @@ class Plan:
                 stream: int) -> None:
         check(lib().starmm_execute(self._h, C_ptr, ldc, A_ptr, lda, B_ptr, ldb, stream),
               "starmm_execute")
+
+    def execute_host(self, C_ptr: int, ldc: int, A_ptr: int, lda: int, B_ptr: int, ldb: int,
+                     stream: int, block_rows: int = 0) -> None:
+        check(lib().starmm_execute_host(self._h, C_ptr, ldc, A_ptr, lda, B_ptr, ldb, stream,
+                                        block_rows), "starmm_execute_host")
 
     def stats(self) -> dict:
         st = StarmmStats()

@@ -29,7 +29,7 @@ from .matrix import Matrix
 
 __all__ = [
     "co2", "co3", "tar_mm", "sar_mm", "star_mm",
-    "atomic_accumulate", "switch_depth",
+    "atomic_accumulate", "switch_depth", "host_mm",
     "PAIR_EMPTY", "PAIR_FIRST_RUNNING", "PAIR_FIRST_DONE",
 ]
 
@@ -110,3 +110,26 @@ def star_mm(C, A, B, s, cfg):
     """tar above the switch depth (ceil of half log2 p), sar below it."""
     _run_public("star", C, A, B, s, cfg)
 
+
+
+def host_mm(algo, C, A, B, s, cfg, mode="pooled"):
+    """C <- C (+) A (x) B for HOST-resident operands (the reference's entry points take
+    host numpy matrices, classic.py:294-316).  C, A, B: 2-D CPU tensors (pinned memory
+    overlaps the transfers with the tile kernels) or numpy arrays; C is updated in place.
+    Same validation as run_algorithm (registry.py:28-42)."""
+    from .registry import ALGORITHMS, CLASSICAL, _MODAL
+    from .runtime import Executor
+    if algo not in ALGORITHMS:
+        raise KeyError(f"unknown algorithm {algo!r}; choose from {ALGORITHMS}")
+    if algo not in CLASSICAL:
+        raise ContractViolation(f"{algo}: only the classical schedules have a host path")
+    if mode not in ("pooled", "raw"):
+        raise ContractViolation(f"unknown mode {mode!r}")
+    if mode == "raw" and algo not in _MODAL:
+        raise ContractViolation(f"{algo} does not take an allocation mode")
+    n = C.shape[0]
+    if not (A.shape[0] == A.shape[1] == B.shape[0] == B.shape[1] == C.shape[1] == n):
+        raise DimMismatch("A, B, C must be square with one common dimension")
+    cfg.check_problem(n)
+    with Executor(cfg) as ex:
+        return ex.execute_host(algo, C, A, B, s, mode=mode)

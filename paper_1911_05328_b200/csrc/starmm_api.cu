@@ -404,8 +404,8 @@ int starmm_plan_stats(starmm_plan* P, starmm_stats* out) {
     return STARMM_OK;
 }
 
-int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
-                   int64_t ldb, void* stream) {
+static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, void* stream, bool force_async) {
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
     const int eb = elem_bytes(P->sr);
@@ -471,8 +471,12 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     } else if (P->ksplit_req >= 0) {
         s_log2 = P->ksplit_req;
     } else {
-        s_log2 = 1;                                      // sibling k-halves concurrent
-        while ((tiles << s_log2) < gpu_workers) ++s_log2;  // ... and enough leaves to fill the GPU
+        // Work-first, like the reference's work-stealing runtime: sibling k-halves only
+        // run concurrently when the output tiles alone cannot keep every persistent CTA
+        // busy for several waves; otherwise each worker runs its tile's k range serially
+        // (the in-place, temporary-free order of serial TAR/SAR).
+        s_log2 = 0;
+        while ((tiles << s_log2) < 4LL * gpu_workers) ++s_log2;
     }
     // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels than
     // the recursion has (log2(k / b))
@@ -687,7 +691,7 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
     // staging buffers go back to their LIFO stacks; stream order protects reuse
     for (auto it = staged.rbegin(); it != staged.rend(); ++it) P->arena.release(it->p, it->bytes);
     if (rc) return rc;
-    if (!(P->flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+    if (!(P->flags & STARMM_F_ASYNC) && !force_async) CK(cudaStreamSynchronize(s));
     if (P->flags & STARMM_F_TIME_MAIN) {
         CK(cudaEventSynchronize(P->ev1));
         float ms = 0.f;
@@ -707,6 +711,99 @@ int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t 
         P->st.pair_count += tiles * (S / 2);
     if (prev_dev != P->device) cudaSetDevice(prev_dev);
     return STARMM_OK;
+}
+
+int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
+                   int64_t ldb, void* stream) {
+    return execute_impl(P, C, ldc, A, lda, B, ldb, stream, false);
+}
+
+// Host-buffer execution: B is uploaded once; A and C stream through the device in
+// row blocks on a copy stream while the previous block computes on `stream`, and
+// finished C blocks stream back on a second copy stream (H2D and D2H overlap each
+// other and the tile kernels).  Each block is an ordinary execute of an
+// (R x n x k) sub-problem, so paths, schedules and guards are unchanged.
+int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
+                        const void* B, int64_t ldb, void* stream, int64_t block_rows) {
+    if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
+    if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
+    int prev_dev = 0;
+    CK(cudaGetDevice(&prev_dev));
+    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
+    const size_t eb = (size_t)elem_bytes(P->sr);
+    const long long m = P->m, n = P->n, k = P->k;
+    // auto: ~one block per 2e12 semiring ops (>= ~30 ms of B200 work, so per-block
+    // guards / packing stay negligible), at most 8 blocks
+    long long auto_blocks = std::max<long long>(1, std::min<long long>(
+        8, (long long)(2.0 * (double)m * (double)n * (double)k / 2e12)));
+    long long R = block_rows > 0 ? block_rows
+                                 : std::max<long long>(128, round_up((m + auto_blocks - 1) / auto_blocks, 128));
+    R = std::min(R, m);
+    const long long nblk = (m + R - 1) / R;
+    const bool same_ab = (A == B) && (m == k) && (n == k) && (lda == ldb);
+    cudaStream_t cs = (cudaStream_t)stream;
+    cudaStream_t up = nullptr, down = nullptr;
+    CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
+    CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    std::vector<cudaEvent_t> ev_in(nblk + 1), ev_done(nblk);
+    for (auto& e : ev_in) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    void *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    long long fr = 0, ru = 0;
+    const size_t a_bytes = (size_t)m * k * eb, b_bytes = (size_t)k * n * eb, c_bytes = (size_t)m * n * eb;
+    int rc = STARMM_OK;
+    do {
+        if ((rc = P->arena.acquire(a_bytes, &dA, false, &fr, &ru))) break;
+        if (!same_ab && (rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
+        if (same_ab) dB = dA;
+        if ((rc = P->arena.acquire(c_bytes, &dC, false, &fr, &ru))) break;
+        // uploads: B first (every block needs all of it; when B aliases A that is all
+        // of A), then the A/C row blocks in order
+        if ((rc = cuda_status(cudaMemcpy2DAsync(dB, n * eb, B, ldb * eb, n * eb, k,
+                                                cudaMemcpyHostToDevice, up)))) break;
+        if ((rc = cuda_status(cudaEventRecord(ev_in[0], up)))) break;
+        for (long long b = 0; b < nblk && !rc; ++b) {
+            long long r0 = b * R, rows = std::min(R, m - r0);
+            if (!same_ab)
+                rc = cuda_status(cudaMemcpy2DAsync((char*)dA + r0 * k * eb, k * eb,
+                                                   (const char*)A + r0 * lda * eb, lda * eb, k * eb, rows,
+                                                   cudaMemcpyHostToDevice, up));
+            if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)dC + r0 * n * eb, n * eb,
+                                                        (const char*)C + r0 * ldc * eb, ldc * eb, n * eb,
+                                                        rows, cudaMemcpyHostToDevice, up));
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_in[b + 1], up));
+        }
+        if (rc) break;
+        if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[0], 0)))) break;
+        const long long saved_m = P->m;
+        for (long long b = 0; b < nblk && !rc; ++b) {
+            long long r0 = b * R, rows = std::min(R, m - r0);
+            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[b + 1], 0)))) break;
+            P->m = rows;
+            rc = execute_impl(P, (char*)dC + r0 * n * eb, n, (char*)dA + r0 * k * eb, k, dB, n, cs, true);
+            P->m = saved_m;
+            if (rc) break;
+            if ((rc = cuda_status(cudaEventRecord(ev_done[b], cs)))) break;
+            if ((rc = cuda_status(cudaStreamWaitEvent(down, ev_done[b], 0)))) break;
+            rc = cuda_status(cudaMemcpy2DAsync((char*)C + r0 * ldc * eb, ldc * eb, (char*)dC + r0 * n * eb,
+                                               n * eb, n * eb, rows, cudaMemcpyDeviceToHost, down));
+        }
+        P->m = saved_m;
+        if (rc) break;
+        if ((rc = cuda_status(cudaStreamSynchronize(down)))) break;
+        rc = cuda_status(cudaStreamSynchronize(cs));
+    } while (0);
+    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(down);
+    if (dC) P->arena.release(dC, c_bytes);
+    if (dB && !same_ab) P->arena.release(dB, b_bytes);
+    if (dA) P->arena.release(dA, a_bytes);
+    for (auto& e : ev_in) cudaEventDestroy(e);
+    for (auto& e : ev_done) cudaEventDestroy(e);
+    cudaStreamDestroy(up);
+    cudaStreamDestroy(down);
+    if (prev_dev != P->device) cudaSetDevice(prev_dev);
+    return rc;
 }
 
 int starmm_matmul(int semiring, void* out, int64_t ldo, const void* A, int64_t lda, const void* B,

@@ -16,7 +16,7 @@ import threading
 import torch
 
 from . import _lib
-from .errors import ContractViolation
+from .errors import ContractViolation, DimMismatch
 from .matrix import Matrix
 from .metrics import Metrics
 from .pool import Pool
@@ -110,6 +110,39 @@ class Executor:
         with torch.cuda.device(Cd.device):
             plan.execute(Cd.data_ptr(), Cd.stride(0), Ad.data_ptr(), Ad.stride(0),
                          Bd.data_ptr(), Bd.stride(0), stream)
+        st = plan.stats()
+        self.last_stats = st
+        self.pool.absorb_device(st)
+        self.metrics.absorb_device(st, s.dtype.itemsize)
+        return st
+
+    def execute_host(self, algo, C, A, B, s, mode="pooled", flags=0, block_rows=0):
+        """C <- C (+) A (x) B with C, A, B in HOST memory (CPU torch tensors, pinned for
+        full copy/compute overlap, or numpy arrays): starmm_execute_host streams row
+        blocks through the device.  C is updated in place."""
+        import numpy as np
+        ts = []
+        for x in (C, A, B):
+            if isinstance(x, np.ndarray):
+                x = torch.from_numpy(x)
+            if x.device.type != "cpu" or x.dtype != s.torch_dtype or x.dim() != 2:
+                raise DimMismatch(f"host buffers must be 2-D CPU {s.torch_dtype} tensors")
+            if x.shape[1] > 1 and x.stride(1) != 1:
+                raise DimMismatch("row-major host buffers are required")
+            ts.append(x)
+        Ct, At, Bt = ts
+        m, n = Ct.shape
+        k = At.shape[1]
+        if At.shape[0] != m or Bt.shape != (k, n):
+            raise DimMismatch("A, B, C shapes do not compose")
+        plan = self.plan(s, algo, mode, m, n, k, flags)
+        plan.reset_stats()
+        dev = torch.device("cuda", self.device)
+        stream = torch.cuda.current_stream(dev).cuda_stream
+        with torch.cuda.device(dev):
+            plan.execute_host(Ct.data_ptr(), max(1, Ct.stride(0)), At.data_ptr(),
+                              max(1, At.stride(0)), Bt.data_ptr(), max(1, Bt.stride(0)), stream,
+                              block_rows)
         st = plan.stats()
         self.last_stats = st
         self.pool.absorb_device(st)

@@ -325,3 +325,40 @@ def test_errors_map_to_reference_exceptions():
         with sm.Executor(sm.Config(base_dim=2)) as ex:
             z = sm.Matrix(np.zeros((4, 4)), s)
             sm.run_algorithm(ex, "bogus", z, z, z, s)
+
+
+# ---- host-buffer entry point (starmm_execute_host) ------------------------
+@pytest.mark.parametrize("sid", ["int", "float", "tropical_f32", "tropical_i32"])
+@pytest.mark.parametrize("pinned,block_rows", [(True, 0), (True, 128), (False, 200)])
+def test_host_path_streams_row_blocks(sid, pinned, block_rows):
+    n = 512
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(21)
+    A = rng.integers(-20, 20, (n, n)).astype(s.dtype)
+    B = rng.integers(-20, 20, (n, n)).astype(s.dtype)
+    C0 = rng.integers(-20, 20, (n, n)).astype(s.dtype)
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B)
+    At, Bt, Ct = (torch.from_numpy(x.copy()) for x in (A, B, C0))
+    if pinned:
+        At, Bt, Ct = At.pin_memory(), Bt.pin_memory(), Ct.pin_memory()
+    with sm.Executor(sm.Config(base_dim=32, workers=148)) as ex:
+        ex.execute_host("star", Ct, At, Bt, s, block_rows=block_rows)
+        if block_rows:
+            assert ex.last_stats["executes"] == -(-n // block_rows)
+    assert_match(sid, Ct.numpy(), want)
+
+
+def test_host_path_aliased_operands_and_public_api():
+    n = 384
+    s = sm.TROPICAL_I32
+    rng = np.random.default_rng(4)
+    W = rng.integers(1, 10 ** 6, (n, n), dtype=np.int32)
+    np.fill_diagonal(W, 0)
+    C = W.copy()
+    sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64, workers=148, allow_nonpow2=True))
+    want = W.copy()
+    O.gemm_fold(O.SR_TROP_I32, want, W, W)
+    assert np.array_equal(C, want)
+    with pytest.raises(sm.InvalidSplit):
+        sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64))
