@@ -74,6 +74,43 @@ __global__ void range_minplus_kernel(const T* X, long long rows, long long cols,
     }
 }
 
+// Running range guard fused into the packers (one read of A and B instead of two):
+// out[0] = max |x| over the real (non-padding) elements read, +inf / INT32_MAX
+// excluded; out[1] |= 1 if a float is non-integral, NaN or -inf.
+struct RangeAcc {
+    unsigned long long m = 0;
+    unsigned bad = 0;
+    STARMM_DEV void add(long long v) {
+        unsigned long long a = v < 0 ? (unsigned long long)(-(v + 1)) + 1ull : (unsigned long long)v;
+        m = a > m ? a : m;
+    }
+    STARMM_DEV void add(int v) {
+        if (v == 0x7fffffff) return;
+        unsigned long long a = (unsigned long long)(v < 0 ? -(long long)v : (long long)v);
+        m = a > m ? a : m;
+    }
+    STARMM_DEV void add(float f) {
+        if (f == __int_as_float(0x7f800000)) return;
+        if (!(f == rintf(f)) || fabsf(f) > 1e9f) { bad = 1; return; }
+        unsigned long long a = (unsigned long long)fabsf(f);
+        m = a > m ? a : m;
+    }
+    STARMM_DEV void add(double) {}
+    // every thread of the launch must call flush (uses full-warp shuffles)
+    STARMM_DEV void flush(unsigned long long* out) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
+            m = v > m ? v : m;
+            bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+        }
+        if ((threadIdx.x & 31) == 0) {
+            if (m) atomicMax(&out[0], m);
+            if (bad) atomicOr(&out[1], 1ull);
+        }
+    }
+};
+
 // ---- packing ---------------------------------------------------------------
 // Element conversion into the packed domain, with the pad value (annihilator
 // of the product, so padded k terms contribute the additive identity).
@@ -105,7 +142,8 @@ struct ConvS16Dup {
 
 // int64 ring -> s8x4 words along k: A (rows x kdim) -> P[kp/4][rowsp]
 __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long kdim, long long lda,
-                                   int* P, long long rowsp, long long kp) {
+                                   int* P, long long rowsp, long long kp, unsigned long long* range) {
+    RangeAcc acc;
     long long total = (kp / 4) * rowsp;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -115,14 +153,17 @@ __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long
         for (int i = 0; i < 4; ++i) {
             long long k = kw * 4 + i;
             long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
+            acc.add(v);
             w |= ((unsigned)(v & 0xff)) << (8 * i);
         }
         P[idx] = (int)w;
     }
+    if (range) acc.flush(range);
 }
 // B (kdim x cols) -> P[kp/4][colsp]
 __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
-                                   int* P, long long colsp, long long kp) {
+                                   int* P, long long colsp, long long kp, unsigned long long* range) {
+    RangeAcc acc;
     long long total = (kp / 4) * colsp;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -132,39 +173,53 @@ __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long
         for (int i = 0; i < 4; ++i) {
             long long k = kw * 4 + i;
             long long v = (c < cols && k < kdim) ? B[k * ldb + c] : 0;
+            acc.add(v);
             w |= ((unsigned)(v & 0xff)) << (8 * i);
         }
         P[idx] = (int)w;
     }
+    if (range) acc.flush(range);
 }
 // (min,+) B (kdim x cols) -> P[kp][colsp/2] words (enc(B[k][2w]), enc(B[k][2w+1]))
 template <class T>
 __global__ void pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, long long ldb,
-                                    unsigned* P, long long colsp, long long kp) {
+                                    unsigned* P, long long colsp, long long kp, unsigned long long* range) {
+    RangeAcc acc;
     long long wpr = colsp / 2;
     long long total = kp * wpr;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
         long long k = idx / wpr, w = idx - k * wpr;
         long long c0 = 2 * w;
-        unsigned lo = (k < kdim && c0 < cols) ? s16_enc<T>(B[k * ldb + c0]) : 16383u;
-        unsigned hi = (k < kdim && c0 + 1 < cols) ? s16_enc<T>(B[k * ldb + c0 + 1]) : 16383u;
+        unsigned lo = 16383u, hi = 16383u;
+        if (k < kdim && c0 < cols) { T v = B[k * ldb + c0]; acc.add(v); lo = s16_enc<T>(v); }
+        if (k < kdim && c0 + 1 < cols) { T v = B[k * ldb + c0 + 1]; acc.add(v); hi = s16_enc<T>(v); }
         P[idx] = lo | (hi << 16);
     }
+    if (range) acc.flush(range);
 }
 
 // A (rows x kdim, ld) -> P[kp/G][rowsp][G], transposing through a 32x32 smem tile
 // so that both the global reads and the packed writes are coalesced.
 template <class Tin, class Tp, int G, class Conv>
 __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long long lda,
-                              Tp* P, long long rowsp, long long kp, Tp pad) {
+                              Tp* P, long long rowsp, long long kp, Tp pad,
+                              unsigned long long* range = nullptr) {
     __shared__ Tp tile[32][33];
+    RangeAcc acc;
     long long r0 = (long long)blockIdx.y * 32, k0 = (long long)blockIdx.x * 32;
     int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
     for (int i = ty; i < 32; i += 8) {
         long long r = r0 + i, k = k0 + tx;
-        tile[i][tx] = (r < rows && k < kdim) ? (Tp)Conv::cvt(A[r * lda + k]) : pad;
+        Tp v = pad;
+        if (r < rows && k < kdim) {
+            Tin x = A[r * lda + k];
+            acc.add(x);
+            v = (Tp)Conv::cvt(x);
+        }
+        tile[i][tx] = v;
     }
+    if (range) acc.flush(range);
     __syncthreads();
     // write: packed index for (k, r): ((k/G) * rowsp + r) * G + k%G
     for (int i = ty; i < 32; i += 8) {

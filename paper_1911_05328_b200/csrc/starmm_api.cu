@@ -419,87 +419,65 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const bool fast_ok = !(P->flags & STARMM_F_NO_FASTPATH);
     int launches = 0;
 
-    // ---- path selection (range guards are exact-by-construction checks) ----
+    // ---- path selection -------------------------------------------------------
+    // Range-guarded exact narrow paths are chosen optimistically: the operands are
+    // packed for the fastest kernel while the packers reduce max|x| (and float
+    // integrality) in the same pass; if the guard fails they are re-packed for the
+    // path the observed range allows.
     int path = 0;
+    bool guard_pending = false;
     if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
     else if (P->sr == STARMM_SR_TROPICAL_F64) path = PATH_SIMT_F64_MIN;
-    else if (P->sr == STARMM_SR_TROPICAL_F32) {
-        path = PATH_SIMT_F32_PAIR;
-        if (fast_ok) {
-            unsigned long long mx; bool bad;
-            TRY(range_minplus_pair<float>(P, A, lda, B, ldb, s, &mx, &bad));
-            launches += 2;
-            // integer-valued with |x| <= 4096: int16 sums cannot overflow, exact
-            if (!bad && mx <= (unsigned long long)S16_FINITE_MAX) path = PATH_SIMT_F32_S16X2;
-        }
-    } else if (P->sr == STARMM_SR_INT64) {
-        path = PATH_SIMT_I64;
-        if (fast_ok) {
-            unsigned long long ma, mb;
-            TRY(range_pair<long long>(P, A, lda, B, ldb, 0, s, &ma, &mb));
-            launches += 2;
-            // exact iff every partial sum fits int32: K * max|a| * max|b| < 2^31
-            long double bound = (long double)P->k * (long double)ma * (long double)mb;
-            if (ma < (1ull << 31) && mb < (1ull << 31) && bound < 2147483648.0L)
-                path = (ma <= 127 && mb <= 127) ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64_NARROW;
-        }
-    } else {  // tropical_i32
-        path = PATH_SIMT_I32_SAT;
-        if (fast_ok) {
-            unsigned long long ma, mb;
-            TRY(range_pair<int>(P, A, lda, B, ldb, 1, s, &ma, &mb));
-            launches += 2;
-            unsigned long long mx = std::max(ma, mb);
-            if (mx <= (unsigned long long)S16_FINITE_MAX) path = PATH_SIMT_I32_S16X2;  // int16 exact
-            else if (mx <= (1ull << 23)) path = PATH_SIMT_I32_CARRIER;                // fp32-exact sums
-            else if (mx < (1ull << 28)) path = PATH_SIMT_I32_VMIN;                    // no int32 overflow
-        }
-    }
-    const bool is_dmma = (path == PATH_DMMA_F64);
-    const PathShape shape = path_shape(path);
-    const int BK = shape.bk;
+    else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
+    else if (P->sr == STARMM_SR_INT64) { path = fast_ok ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64; guard_pending = fast_ok; }
+    else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
 
-    // ---- the split: leaf tasks = output tiles x k-slices ----
-    const int TBM = shape.bm, TBN = shape.bn;
-    const long long tiles_m = (P->m + TBM - 1) / TBM, tiles_n = (P->n + TBN - 1) / TBN;
-    const long long tiles = tiles_m * tiles_n;
-    const int per_sm = shape.per_sm;
-    const int gpu_workers = P->sms * per_sm;             // persistent CTAs (the GPU workers)
-    int s_log2;
-    if (P->algo == STARMM_CO2) {
-        s_log2 = 0;                // k-halves serialised (classic.py:125-128): never split
-    } else if (P->ksplit_req >= 0) {
-        s_log2 = P->ksplit_req;
-    } else {
-        // Work-first, like the reference's work-stealing runtime: sibling k-halves only
-        // run concurrently when the output tiles alone cannot keep every persistent CTA
-        // busy for several waves; otherwise each worker runs its tile's k range serially
-        // (the in-place, temporary-free order of serial TAR/SAR).
-        s_log2 = 0;
-        while ((tiles << s_log2) < 4LL * gpu_workers) ++s_log2;
-    }
-    // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels than
-    // the recursion has (log2(k / b))
-    while (s_log2 > 0 && ((P->k >> s_log2) < std::max(P->base_dim, BK) || (P->k >> s_log2) < 1))
-        --s_log2;
-    const int S = 1 << s_log2;
-    int tar_levels = 0;
-    if (P->algo == STARMM_TAR) tar_levels = s_log2;
-    if (P->algo == STARMM_STAR) tar_levels = std::min(switch_depth(P->workers), s_log2);
-
-    const long long Mp = tiles_m * TBM, Np = tiles_n * TBN;
-    const long long Kp = round_up(P->k, std::max<long long>(32, (long long)BK * S));
-    const long long kslice = Kp / S;
-
+    // geometry of the chosen path (re-derived if the guard changes the path)
+    bool is_dmma = false;
+    PathShape shape;
+    int BK = 0, TBM = 0, TBN = 0, per_sm = 1, gpu_workers = 0, s_log2 = 0, S = 1, tar_levels = 0;
+    long long tiles_m = 0, tiles_n = 0, tiles = 0, Mp = 0, Np = 0, Kp = 0, kslice = 0, ntasks = 0;
     TaskGrid g;
-    g.tiles_m = (int)tiles_m; g.tiles_n = (int)tiles_n; g.S = S; g.log2S = s_log2;
-    g.tar_levels = tar_levels; g.kslice = kslice;
-    // raster groups sized so one wave of resident CTAs covers a near-square block of
-    // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
-    g.group_m = is_dmma ? 24 : 12;
-    const long long ntasks = tiles * S;
-    if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
-    g.num_tasks = (int)ntasks;
+    auto plan_geometry = [&]() -> int {
+        is_dmma = (path == PATH_DMMA_F64);
+        shape = path_shape(path);
+        BK = shape.bk; TBM = shape.bm; TBN = shape.bn; per_sm = shape.per_sm;
+        tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
+        tiles = tiles_m * tiles_n;
+        gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
+        if (P->algo == STARMM_CO2) {
+            s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
+        } else if (P->ksplit_req >= 0) {
+            s_log2 = P->ksplit_req;
+        } else {
+            // Work-first, like the reference's work-stealing runtime: sibling k-halves only
+            // run concurrently when the output tiles alone cannot keep every persistent CTA
+            // busy for several waves; otherwise each worker runs its tile's k range serially
+            // (the in-place, temporary-free order of serial TAR/SAR).
+            s_log2 = 0;
+            while ((tiles << s_log2) < 4LL * gpu_workers) ++s_log2;
+        }
+        // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels
+        // than the recursion has (log2(k / b))
+        while (s_log2 > 0 && ((P->k >> s_log2) < std::max(P->base_dim, BK) || (P->k >> s_log2) < 1))
+            --s_log2;
+        S = 1 << s_log2;
+        tar_levels = 0;
+        if (P->algo == STARMM_TAR) tar_levels = s_log2;
+        if (P->algo == STARMM_STAR) tar_levels = std::min(switch_depth(P->workers), s_log2);
+        Mp = tiles_m * TBM; Np = tiles_n * TBN;
+        Kp = round_up(P->k, std::max<long long>(32, (long long)BK * S));
+        kslice = Kp / S;
+        g.tiles_m = (int)tiles_m; g.tiles_n = (int)tiles_n; g.S = S; g.log2S = s_log2;
+        g.tar_levels = tar_levels; g.kslice = kslice;
+        // raster groups sized so one wave of resident CTAs covers a near-square block of
+        // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
+        g.group_m = is_dmma ? 24 : 12;
+        ntasks = tiles * S;
+        if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
+        g.num_tasks = (int)ntasks;
+        return STARMM_OK;
+    };
 
     // ---- staging buffers from the arena (not counted as algorithm temps) ----
     std::vector<Block> staged;
@@ -513,6 +491,10 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const void* opA = A; const void* opB = B;
     long long olda = lda, oldb = ldb;
     do {
+      for (;;) {
+        if ((rc = plan_geometry())) break;
+        unsigned long long* rng = guard_pending ? P->d_range : nullptr;
+        if (rng && (rc = cuda_status(cudaMemsetAsync(rng, 0, 2 * sizeof(unsigned long long), s)))) break;
         if (is_dmma) {
             bool direct = (P->m % TBM == 0) && (P->n % TBN == 0) && (P->k == Kp) &&
                           (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
@@ -560,9 +542,9 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             }
             case PATH_SIMT_I64_DP4A:
                 pack_a_s8x4_kernel<<<grid_blocks((Kp / 4) * Mp), 256, 0, s>>>(
-                    (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp);
+                    (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
                 pack_b_s8x4_kernel<<<grid_blocks((Kp / 4) * Np), 256, 0, s>>>(
-                    (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp);
+                    (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
             case PATH_SIMT_F32_S16X2:
@@ -570,14 +552,14 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                 dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
                 if (path == PATH_SIMT_F32_S16X2) {
                     pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
-                        (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad);
+                        (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
                     pack_b_s16x2_kernel<float><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
-                        (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp);
+                        (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
                 } else {
                     pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
-                        (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad);
+                        (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
                     pack_b_s16x2_kernel<int><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
-                        (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp);
+                        (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
                 }
                 rc = cuda_status(cudaGetLastError());
                 break;
@@ -587,6 +569,35 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             launches += 2;
             opA = pa; opB = pb;
         }
+        if (!guard_pending) break;
+        // ---- the fused guard: decide the exact path the observed range allows ----
+        unsigned long long h[2];
+        if ((rc = cuda_status(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s)))) break;
+        if ((rc = cuda_status(cudaStreamSynchronize(s)))) break;
+        guard_pending = false;
+        const unsigned long long mx = h[0];
+        const bool bad = h[1] != 0;
+        int actual = path;
+        if (P->sr == STARMM_SR_INT64) {
+            // exact iff every int32 partial sum fits: K * max|a| * max|b| < 2^31
+            long double bound = (long double)P->k * (long double)mx * (long double)mx;
+            if (mx <= 127 && bound < 2147483648.0L) actual = PATH_SIMT_I64_DP4A;
+            else if (mx < (1ull << 31) && bound < 2147483648.0L) actual = PATH_SIMT_I64_NARROW;
+            else actual = PATH_SIMT_I64;
+        } else if (P->sr == STARMM_SR_TROPICAL_F32) {
+            // integer-valued with |x| <= 4096: int16 sums cannot overflow, exact
+            actual = (!bad && mx <= (unsigned long long)S16_FINITE_MAX) ? PATH_SIMT_F32_S16X2
+                                                                         : PATH_SIMT_F32_PAIR;
+        } else {
+            if (mx <= (unsigned long long)S16_FINITE_MAX) actual = PATH_SIMT_I32_S16X2;   // int16 exact
+            else if (mx <= (1ull << 23)) actual = PATH_SIMT_I32_CARRIER;                 // fp32-exact sums
+            else if (mx < (1ull << 28)) actual = PATH_SIMT_I32_VMIN;                     // no overflow
+            else actual = PATH_SIMT_I32_SAT;
+        }
+        if (actual == path) break;
+        path = actual;                  // re-pack for the path the range allows
+      }
+      if (rc) break;
 
         // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
         const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
