@@ -25,7 +25,8 @@ F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2, F_TIME_MAIN = 0x1, 0x2
 PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f32_fadd2_fmnmx3",
               5: "simt_i32_via_f32_carrier", 6: "simt_i32_viaddmnmx", 7: "simt_i32_saturating",
               8: "simt_f64_min", 9: "simt_i64_dp4a", 10: "simt_f32_s16x2_viaddmnmx",
-              11: "simt_i32_s16x2_viaddmnmx"}
+              11: "simt_i32_s16x2_viaddmnmx", 12: "simt_f64trop_s16x2_viaddmnmx",
+              13: "simt_f64trop_via_f32_carrier"}
 
 
 class StarmmStats(ctypes.Structure):

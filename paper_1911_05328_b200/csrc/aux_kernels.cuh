@@ -95,7 +95,12 @@ struct RangeAcc {
         unsigned long long a = (unsigned long long)fabsf(f);
         m = a > m ? a : m;
     }
-    STARMM_DEV void add(double) {}
+    STARMM_DEV void add(double d) {
+        if (d == __longlong_as_double(0x7ff0000000000000LL)) return;
+        if (!(d == rint(d)) || fabs(d) > 1e9) { bad = 1; return; }
+        unsigned long long a = (unsigned long long)fabs(d);
+        m = a > m ? a : m;
+    }
     // every thread of the launch must call flush (uses full-warp shuffles)
     STARMM_DEV void flush(unsigned long long* out) {
 #pragma unroll
@@ -122,6 +127,9 @@ struct ConvI32ToF32 {   // int32 tropical -> fp32 carrier, INT32_MAX -> +inf
         return x == 0x7fffffff ? __int_as_float(0x7f800000) : (float)x;
     }
 };
+struct ConvF64ToF32 {   // float64 tropical with integer values |x| <= 2^23 -> fp32 carrier (exact)
+    static STARMM_DEV float cvt(double x) { return (float)x; }
+};
 struct ConvI32Vmin {    // int32 tropical -> VIADDMNMX encoding, INT32_MAX -> 2^30 - 1
     static STARMM_DEV int cvt(int x) { return x == 0x7fffffff ? (1 << 30) - 1 : x; }
 };
@@ -132,6 +140,9 @@ struct ConvI64ToI32 {   // int64 ring, range-guarded narrow path
 template <class T> STARMM_DEV unsigned s16_enc(T x);
 template <> STARMM_DEV unsigned s16_enc<float>(float x) {
     return x == __int_as_float(0x7f800000) ? 16383u : ((unsigned)(int)x & 0xffffu);
+}
+template <> STARMM_DEV unsigned s16_enc<double>(double x) {
+    return x == __longlong_as_double(0x7ff0000000000000LL) ? 16383u : ((unsigned)(int)x & 0xffffu);
 }
 template <> STARMM_DEV unsigned s16_enc<int>(int x) {
     return x == 0x7fffffff ? 16383u : ((unsigned)x & 0xffffu);

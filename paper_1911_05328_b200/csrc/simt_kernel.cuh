@@ -171,6 +171,15 @@ template <> struct Finish<PolS16x2Min, SrTropF32> {
         return x > S16_INF_THRESHOLD ? __int_as_float(0x7f800000) : (float)x;
     }
 };
+template <> struct Finish<PolS16x2Min, SrTropF64> {
+    static STARMM_DEV double out2(unsigned v, int h) {
+        int x = (int)(short)(h ? (v >> 16) : (v & 0xffffu));
+        return x > S16_INF_THRESHOLD ? __longlong_as_double(0x7ff0000000000000LL) : (double)x;
+    }
+};
+template <> struct Finish<PolF32Pair, SrTropF64> {   // fp32 carrier of integer-valued float64
+    static STARMM_DEV double out(float v) { return (double)v; }
+};
 template <> struct Finish<PolS16x2Min, SrTropI32> {
     static STARMM_DEV int out2(unsigned v, int h) {
         int x = (int)(short)(h ? (v >> 16) : (v & 0xffffu));

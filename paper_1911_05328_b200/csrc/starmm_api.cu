@@ -121,7 +121,8 @@ namespace {
 enum PathId : int {
     PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
     PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
-    PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11
+    PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11,
+    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13
 };
 
 // Tile / packing geometry of one kernel path (mirrors the device-side constants).
@@ -155,6 +156,8 @@ PathShape path_shape(int path) {
     case PATH_SIMT_I64_DP4A: return simt_shape<PolI8Dp4a>();
     case PATH_SIMT_F32_S16X2: return simt_shape<PolS16x2Min>();
     case PATH_SIMT_I32_S16X2: return simt_shape<PolS16x2Min>();
+    case PATH_SIMT_F64T_S16X2: return simt_shape<PolS16x2Min>();
+    case PATH_SIMT_F64T_CARRIER: return simt_shape<PolF32Pair>();
     }
     return simt_shape<PolI64>();
 }
@@ -427,7 +430,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     int path = 0;
     bool guard_pending = false;
     if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
-    else if (P->sr == STARMM_SR_TROPICAL_F64) path = PATH_SIMT_F64_MIN;
+    else if (P->sr == STARMM_SR_TROPICAL_F64) { path = fast_ok ? PATH_SIMT_F64T_S16X2 : PATH_SIMT_F64_MIN; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_INT64) { path = fast_ok ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64; guard_pending = fast_ok; }
     else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
@@ -547,10 +550,19 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
+            case PATH_SIMT_F64T_CARRIER:
+                rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                                  Mp, Np, Kp, finf, s); break;
             case PATH_SIMT_F32_S16X2:
-            case PATH_SIMT_I32_S16X2: {
+            case PATH_SIMT_I32_S16X2:
+            case PATH_SIMT_F64T_S16X2: {
                 dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
-                if (path == PATH_SIMT_F32_S16X2) {
+                if (path == PATH_SIMT_F64T_S16X2) {
+                    pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                        (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
+                    pack_b_s16x2_kernel<double><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                        (const double*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
+                } else if (path == PATH_SIMT_F32_S16X2) {
                     pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                         (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
                     pack_b_s16x2_kernel<float><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
@@ -584,6 +596,12 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             if (mx <= 127 && bound < 2147483648.0L) actual = PATH_SIMT_I64_DP4A;
             else if (mx < (1ull << 31) && bound < 2147483648.0L) actual = PATH_SIMT_I64_NARROW;
             else actual = PATH_SIMT_I64;
+        } else if (P->sr == STARMM_SR_TROPICAL_F64) {
+            // integer-valued float64: int16 when |x| <= 4096, else fp32 carrier while all
+            // sums stay below 2^24 (exact), else the float64 kernel
+            if (!bad && mx <= (unsigned long long)S16_FINITE_MAX) actual = PATH_SIMT_F64T_S16X2;
+            else if (!bad && mx <= (1ull << 23)) actual = PATH_SIMT_F64T_CARRIER;
+            else actual = PATH_SIMT_F64_MIN;
         } else if (P->sr == STARMM_SR_TROPICAL_F32) {
             // integer-valued with |x| <= 4096: int16 sums cannot overflow, exact
             actual = (!bad && mx <= (unsigned long long)S16_FINITE_MAX) ? PATH_SIMT_F32_S16X2
@@ -670,6 +688,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             case PATH_SIMT_I64_DP4A: rc = launch_simt<PolI8Dp4a, SrInt64>(sp, grid, s); break;
             case PATH_SIMT_F32_S16X2: rc = launch_simt<PolS16x2Min, SrTropF32>(sp, grid, s); break;
             case PATH_SIMT_I32_S16X2: rc = launch_simt<PolS16x2Min, SrTropI32>(sp, grid, s); break;
+            case PATH_SIMT_F64T_S16X2: rc = launch_simt<PolS16x2Min, SrTropF64>(sp, grid, s); break;
+            case PATH_SIMT_F64T_CARRIER: rc = launch_simt<PolF32Pair, SrTropF64>(sp, grid, s); break;
             }
         }
         if (rc) break;

@@ -171,6 +171,29 @@ def test_f32_tropical_paths_bitexact(kind, expect):
     assert np.array_equal(got, want)
 
 
+@pytest.mark.parametrize("hi,frac,expect", [(50, False, "simt_f64trop_s16x2_viaddmnmx"),
+                                            (100000, False, "simt_f64trop_via_f32_carrier"),
+                                            (1 << 24, False, "simt_f64_min"),
+                                            (50, True, "simt_f64_min")])
+def test_reference_tropical_f64_paths_bitexact(hi, frac, expect):
+    """The reference's own float64 (min,+) semiring: integer-valued inputs take the exact
+    narrow kernels, anything else the float64 kernel -- identical bits either way."""
+    n = 272
+    rng = np.random.default_rng(17)
+    A = rng.integers(-hi, hi + 1, (n, n)).astype(np.float64)
+    B = rng.integers(-hi, hi + 1, (n, n)).astype(np.float64)
+    if frac:
+        B += 0.5
+    A[rng.random(A.shape) < 0.1] = np.inf
+    B[rng.random(B.shape) < 0.1] = np.inf
+    C0 = rng.integers(-hi, hi + 1, (n, n)).astype(np.float64)
+    want = C0.copy()
+    O.gemm_fold(O.SR_TROP_F64, want, A, B)
+    got, path = _path_of("co2", sm.TROPICAL, C0, A, B, sm.Config(base_dim=16, allow_nonpow2=True))
+    assert path == expect
+    assert np.array_equal(got, want)
+
+
 def test_tropical_nan_in_C_propagates_like_np_minimum():
     s = sm.TROPICAL
     A = np.array([[1.0, 2.0], [3.0, 4.0]])
