@@ -214,6 +214,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=None, help="override n (smoke runs only)")
     ap.add_argument("--ksplit-gpus", type=int, default=None)
+    ap.add_argument("--combine", default="fused", choices=["fused", "nccl"],
+                    help="k-split combine across GPUs (only when the grid has ks > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -243,7 +245,8 @@ def main():
     group_ks = ks_groups(grid) if world > 1 else None
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
-                        group_ks=group_ks, device=local_rank, time_kernel=True)
+                        group_ks=group_ks, device=local_rank, time_kernel=True,
+                        combine=args.combine)
 
     A = gen_panel(cid, "A", dmm.m, dmm.k, dmm.r0, dmm.k0, device)
     B = A if (cid in (3, 5) and dmm.r0 == dmm.k0 and dmm.m == dmm.k and dmm.c0 == dmm.k0
@@ -331,6 +334,7 @@ def main():
             "config": {"workload": cfg["name"], "baseline_config": cid, "n": n, "semiring": s.id,
                        "algo": args.algo, "base_dim": cfg["b"], "workers": sms,
                        "grid": [grid.pr, grid.pc, grid.ks], "path": st["path_name"],
+                       "combine": dmm.combine_mode if grid.ks > 1 else "none",
                        "ksplit_per_tile": st["ksplit"], "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
             "cpu_baseline": cpu,

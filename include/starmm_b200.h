@@ -133,6 +133,20 @@ int  starmm_execute(starmm_plan* plan, void* C, int64_t ldc, const void* A, int6
  * this is their host-buffer form. */
 int  starmm_execute_host(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,
                          const void* B, int64_t ldb, void* stream, int64_t block_rows);
+/* Fused k-split combine across GPUs: when set, every output tile
+ * is folded with the semiring's atomic-madd (red.min.s32 / red.add.f64 / red.add.u64,
+ * CAS for float minima) directly into the OWNER's rows over NVLink peer memory:
+ * rows [p*rows_per_part, (p+1)*rows_per_part) of this plan's output live at
+ * bases[p] (leading dimension ld).  The owners pre-load C0 in their rows; the
+ * reduce-scatter of the reference design disappears into the tile epilogue.
+ * This is TAR's accumulate_region (ops.py:76-101) across GPUs.  nparts <= 8;
+ * nparts = 0 restores local write-back.  Not valid for co3. */
+int  starmm_plan_set_peers(starmm_plan* plan, int nparts, void* const* bases, int64_t ld,
+                           int64_t rows_per_part);
+/* CUDA IPC for the peer mapping (handles are 64 opaque bytes, exchanged by the host). */
+int  starmm_ipc_handle(const void* dptr, void* handle_out);
+int  starmm_ipc_open(const void* handle, void** dptr_out);
+int  starmm_ipc_close(void* dptr);
 int  starmm_plan_stats(starmm_plan* plan, starmm_stats* out);
 int  starmm_plan_reset_stats(starmm_plan* plan);
 void starmm_plan_destroy(starmm_plan* plan);

@@ -81,6 +81,14 @@ def lib():
         L.starmm_execute.restype = ci
         L.starmm_execute_host.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64]
         L.starmm_execute_host.restype = ci
+        L.starmm_plan_set_peers.argtypes = [vp, ci, ctypes.POINTER(vp), i64, i64]
+        L.starmm_plan_set_peers.restype = ci
+        L.starmm_ipc_handle.argtypes = [vp, ctypes.c_char_p]
+        L.starmm_ipc_handle.restype = ci
+        L.starmm_ipc_open.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
+        L.starmm_ipc_open.restype = ci
+        L.starmm_ipc_close.argtypes = [vp]
+        L.starmm_ipc_close.restype = ci
         L.starmm_plan_stats.argtypes = [vp, ctypes.POINTER(StarmmStats)]
         L.starmm_plan_stats.restype = ci
         L.starmm_plan_reset_stats.argtypes = [vp]
@@ -133,6 +141,12 @@ class Plan:
         check(lib().starmm_execute_host(self._h, C_ptr, ldc, A_ptr, lda, B_ptr, ldb, stream,
                                         block_rows), "starmm_execute_host")
 
+    def set_peers(self, bases, ld: int, rows_per_part: int) -> None:
+        """Route every tile's atomic-madd to the owner part's buffer (fused k-split combine)."""
+        arr = (ctypes.c_void_p * max(1, len(bases)))(*[ctypes.c_void_p(b) for b in bases])
+        check(lib().starmm_plan_set_peers(self._h, len(bases), arr, ld, rows_per_part),
+              "starmm_plan_set_peers")
+
     def stats(self) -> dict:
         st = StarmmStats()
         check(lib().starmm_plan_stats(self._h, ctypes.byref(st)), "starmm_plan_stats")
@@ -153,3 +167,19 @@ class Plan:
             self.close()
         except Exception:
             pass
+
+
+def ipc_handle(ptr: int) -> bytes:
+    buf = ctypes.create_string_buffer(64)
+    check(lib().starmm_ipc_handle(ptr, buf), "starmm_ipc_handle")
+    return buf.raw
+
+
+def ipc_open(handle: bytes) -> int:
+    out = ctypes.c_void_p()
+    check(lib().starmm_ipc_open(handle, ctypes.byref(out)), "starmm_ipc_open")
+    return int(out.value)
+
+
+def ipc_close(ptr: int) -> None:
+    check(lib().starmm_ipc_close(ptr), "starmm_ipc_close")

@@ -146,10 +146,17 @@ struct WbParams {
     unsigned long long* counters;
     unsigned* worker_used;    // per worker: has this worker's scratch block been issued
     void* scratch; long long scratch_elems;      // per-worker lazy temp block (tile-sized)
+    // k-split combine across GPUs (starmm_plan_set_peers): output row r is folded with
+    // the atomic-madd into part p = r / remote_rows, which lives at remote_base[p]
+    // (an NVLink-mapped peer buffer, or a local one), leading dimension remote_ld.
+    int remote_parts;
+    long long remote_rows, remote_ld;
+    void* remote_base[8];
 };
 
 // Which protocol a given task uses (host mirrors this in DESIGN.md).
 STARMM_DEV int task_mode(const WbParams& w, const TaskGrid& g, int s) {
+    if (w.remote_parts > 0) return WB_RED;   // TAR across GPUs: every tile is atomic-madd'ed
     switch (w.mode_base) {
     case 0: return w.init_identity ? WB_STORE : WB_FOLD;                     // co2
     case 1: return (s == 0) ? (w.init_identity ? WB_STORE : WB_FOLD) : WB_STORE;  // co3

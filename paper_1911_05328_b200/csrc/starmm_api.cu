@@ -113,6 +113,10 @@ struct starmm_plan {
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
+    // peer destinations of the fused k-split combine (starmm_plan_set_peers)
+    int remote_parts = 0;
+    long long remote_rows = 0, remote_ld = 0;
+    void* remote_base[8] = {};
 };
 
 namespace {
@@ -646,7 +650,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             }
             P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
         }
-        if (init_identity && S > 1 && P->algo != STARMM_CO3) {
+        if (init_identity && S > 1 && P->algo != STARMM_CO3 && P->remote_parts == 0) {
             if ((rc = fill_dispatch(P->sr, C, P->m, P->n, ldc, s))) break;
             ++launches;
         }
@@ -659,6 +663,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         w.pairs = pstate ? (int*)pstate + tiles : nullptr;
         w.counters = P->d_counters; w.worker_used = P->d_worker_used;
         w.scratch = wscratch; w.scratch_elems = tile_elems;
+        w.remote_parts = P->remote_parts; w.remote_rows = P->remote_rows; w.remote_ld = P->remote_ld;
+        for (int i = 0; i < 8; ++i) w.remote_base[i] = P->remote_base[i];
 
         int grid = occupancy_grid(P, per_sm, ntasks);
         const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
@@ -747,6 +753,45 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
 int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
                    int64_t ldb, void* stream) {
     return execute_impl(P, C, ldc, A, lda, B, ldb, stream, false);
+}
+
+int starmm_plan_set_peers(starmm_plan* P, int nparts, void* const* bases, int64_t ld,
+                          int64_t rows_per_part) {
+    if (!P || nparts < 0 || nparts > 8) return STARMM_CONTRACT_VIOLATION;
+    if (nparts == 0) { P->remote_parts = 0; return STARMM_OK; }
+    if (!bases || rows_per_part < 1 || ld < P->n) return STARMM_CONTRACT_VIOLATION;
+    if (P->algo == STARMM_CO3) return STARMM_CONTRACT_VIOLATION;   // co3 merges its own workspace
+    if ((long long)nparts * rows_per_part < P->m) return STARMM_DIM_MISMATCH;
+    for (int i = 0; i < nparts; ++i) {
+        if (!bases[i]) return STARMM_CONTRACT_VIOLATION;
+        P->remote_base[i] = bases[i];
+    }
+    P->remote_parts = nparts;
+    P->remote_rows = rows_per_part;
+    P->remote_ld = ld;
+    return STARMM_OK;
+}
+
+int starmm_ipc_handle(const void* dptr, void* handle_out) {
+    if (!dptr || !handle_out) return STARMM_CONTRACT_VIOLATION;
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, const_cast<void*>(dptr)));
+    memcpy(handle_out, &h, sizeof(h));
+    return STARMM_OK;
+}
+
+int starmm_ipc_open(const void* handle, void** dptr_out) {
+    if (!handle || !dptr_out) return STARMM_CONTRACT_VIOLATION;
+    cudaIpcMemHandle_t h;
+    memcpy(&h, handle, sizeof(h));
+    CK(cudaIpcOpenMemHandle(dptr_out, h, cudaIpcMemLazyEnablePeerAccess));
+    return STARMM_OK;
+}
+
+int starmm_ipc_close(void* dptr) {
+    if (!dptr) return STARMM_CONTRACT_VIOLATION;
+    CK(cudaIpcCloseMemHandle(dptr));
+    return STARMM_OK;
 }
 
 // Host-buffer execution: B is uploaded once; A and C stream through the device in

@@ -59,15 +59,28 @@ STARMM_DEV void writeback(const WbParams& w, const TaskGrid& g, int tm, int tn, 
     const long long tile_bytes = (long long)BM * BN * (long long)sizeof(T);
     if (mode == WB_RED) {
         // TAR leaf (classic.py:160-167): the accumulator registers are this
-        // worker's b x b block; merge it with per-element atomic-madd.
+        // worker's b x b block; merge it with per-element atomic-madd -- into the
+        // local C, or (k-split across GPUs) straight into the owner GPU's rows over
+        // NVLink peer memory: the combine is fused into the tile epilogue.
         if (threadIdx.x == 0) {
             pool_acquire(w, worker, tile_bytes);
             counter_add(w, CNT_SERIALIZATIONS, 1);
         }
-        each([&](int r, int c, T v) {
-            long long gr = m0 + r, gc = n0 + c;
-            if (gr < M && gc < N) Sr::atomic_fold(&C[gr * ldc + gc], v);
-        });
+        if (w.remote_parts > 0) {
+            each([&](int r, int c, T v) {
+                long long gr = m0 + r, gc = n0 + c;
+                if (gr < M && gc < N) {
+                    int part = (int)(gr / w.remote_rows);
+                    T* dst = reinterpret_cast<T*>(w.remote_base[part]);
+                    Sr::atomic_fold(&dst[(gr - part * w.remote_rows) * w.remote_ld + gc], v);
+                }
+            });
+        } else {
+            each([&](int r, int c, T v) {
+                long long gr = m0 + r, gc = n0 + c;
+                if (gr < M && gc < N) Sr::atomic_fold(&C[gr * ldc + gc], v);
+            });
+        }
         __syncthreads();
         if (threadIdx.x == 0) pool_release(w, tile_bytes);
         return;

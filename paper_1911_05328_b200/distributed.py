@@ -13,6 +13,15 @@ path shards naturally:
   (the (min,+) semirings); rank K keeps row-chunk K of the reduced block.
   Min and integer sums are order-independent, so the combine is bit-exact.
 
+Two combines for ks > 1:
+  combine="fused" (default on GPUs) -- the reduce-scatter disappears into the
+      tile epilogue: each owner exposes its row chunk to the k-split group over
+      CUDA IPC (NVLink peer memory), pre-loads C0 there, and every rank's tile
+      kernel folds its partial tiles straight into the owners' rows with the
+      semiring's atomic-madd (starmm_plan_set_peers) -- TAR's accumulate_region
+      (ops.py:76-101) across GPUs, overlapped tile by tile with the math;
+  combine="nccl" -- partial blocks + one NCCL reduce-scatter (the baseline).
+
 The local product is pluggable (``local_mm``) so that the partition and
 combine logic can be exercised on CPU with the gloo backend (tests/), while
 the GPU path calls the C ABI.
@@ -79,7 +88,7 @@ class DistributedMM:
     def __init__(self, n: int, semiring, grid: Grid, rank: int, algo: str = "star",
                  base_dim: int = 64, workers: int = 1, group_ks=None,
                  local_mm: Optional[Callable] = None, device: Optional[int] = None,
-                 time_kernel: bool = False):
+                 time_kernel: bool = False, combine: str = "nccl"):
         self.n, self.s, self.grid, self.rank = n, semiring, grid, rank
         self.I, self.J, self.K = grid.coords(rank)
         self.r0, self.r1 = block_bounds(n, grid.pr, self.I)
@@ -91,7 +100,11 @@ class DistributedMM:
         self.local_mm = local_mm
         self.plan = None
         if local_mm is None:
-            flags = _lib.F_ALLOW_NONPOW2 | (_lib.F_INIT_IDENTITY if self.init_identity else 0)
+            fused = combine == "fused" and grid.ks > 1
+            # the fused combine folds every partial into the owners' rows, so no rank
+            # needs an identity-initialised local block
+            flags = _lib.F_ALLOW_NONPOW2 | (_lib.F_INIT_IDENTITY
+                                            if (self.init_identity and not fused) else 0)
             if time_kernel:
                 flags |= _lib.F_TIME_MAIN
             self.plan = _lib.Plan(semiring.sr_id, algo, "pooled", self.m, self.nn, self.k,
@@ -100,6 +113,26 @@ class DistributedMM:
                                   flags)
         # rows of the (I, J) block each k-split member keeps after the reduce-scatter
         self.chunk_rows = -(-self.m // grid.ks)
+        self.combine_mode = combine if (grid.ks > 1 and local_mm is None) else "nccl"
+        self.owned = None
+        self._peer_tensors = []
+        if self.combine_mode == "fused":
+            self._setup_fused(device if device is not None else torch.cuda.current_device())
+
+    # -- fused combine: owners' rows shared over CUDA IPC ----------------------
+    def _setup_fused(self, device):
+        from torch.multiprocessing.reductions import reduce_tensor
+        self.owned = torch.empty((self.chunk_rows, self.nn), dtype=self.s.torch_dtype,
+                                 device=torch.device("cuda", device))
+        mine = reduce_tensor(self.owned)
+        shared = [None] * self.grid.ks
+        dist.all_gather_object(shared, mine, group=self.group_ks)
+        peers = []
+        for j, (rebuild, args) in enumerate(shared):
+            t = self.owned if j == self.K else rebuild(*args)
+            peers.append(t)
+        self._peer_tensors = peers            # keep the mappings alive
+        self.plan.set_peers([t.data_ptr() for t in peers], self.nn, self.chunk_rows)
 
     # -- panels -----------------------------------------------------------
     def a_panel(self, A_full):
@@ -142,8 +175,26 @@ class DistributedMM:
         return out[: hi - lo]
 
     def step(self, C_blk, A_pan, B_pan) -> torch.Tensor:
+        if self.combine_mode == "fused":
+            return self.step_fused(C_blk, A_pan, B_pan)
         self.local(C_blk, A_pan, B_pan)
         return self.combine(C_blk)
+
+    def step_fused(self, C_blk, A_pan, B_pan) -> torch.Tensor:
+        """Owner pre-loads C0 into its shared rows; after a group barrier every rank's
+        tile kernel atomically folds its partial tiles into the owners' rows; a second
+        barrier closes the step.  Returns this rank's reduced rows."""
+        lo, hi = self.owned_rows()
+        r = hi - lo
+        # C0 is folded exactly once: by the owner of each row chunk (C_blk holds C0 of
+        # the (I, J) block on every member; only the owner's rows are loaded)
+        self.owned[:r].copy_(C_blk[lo - self.r0:hi - self.r0])
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group_ks)
+        self.local(C_blk, A_pan, B_pan)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group_ks)
+        return self.owned[:r]
 
     def close(self):
         if self.plan is not None:

@@ -385,3 +385,40 @@ def test_host_path_aliased_operands_and_public_api():
     assert np.array_equal(C, want)
     with pytest.raises(sm.InvalidSplit):
         sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64))
+
+
+# ---- fused k-split combine (starmm_plan_set_peers), emulated on one GPU -----
+@pytest.mark.parametrize("sid", ["int", "float", "tropical_f32", "tropical_i32"])
+@pytest.mark.parametrize("ks", [2, 4])
+def test_fused_ksplit_combine_single_gpu_emulation(sid, ks):
+    """Exactly the kernel path of DistributedMM(combine="fused"): ks 'virtual ranks',
+    each with its own k-slice plan, fold their partial tiles with the atomic-madd into
+    the owners' row chunks (here local buffers instead of NVLink-mapped peers).  The
+    virtual ranks run one after another, so nothing waits on anything."""
+    from paper_1911_05328_b200 import _lib
+    from paper_1911_05328_b200.distributed import block_bounds
+    n = 256 * ks          # every virtual rank gets a non-empty, 128-aligned k-slice
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(ks)
+    A = rng.integers(-30, 30, (n, n)).astype(s.dtype)
+    B = rng.integers(-30, 30, (n, n)).astype(s.dtype)
+    C0 = rng.integers(-30, 30, (n, n)).astype(s.dtype)
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B)
+    chunk = -(-n // ks)
+    owned = [torch.from_numpy(np.ascontiguousarray(C0[j * chunk:(j + 1) * chunk])).cuda()
+             for j in range(ks)]
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    scratch = torch.empty((n, n), dtype=s.torch_dtype, device="cuda")
+    for K in range(ks):
+        k0, k1 = block_bounds(n, ks, K)
+        plan = _lib.Plan(s.sr_id, "star", "pooled", n, n, k1 - k0, 32, 148, -1, 0,
+                         _lib.F_ALLOW_NONPOW2)
+        plan.set_peers([t.data_ptr() for t in owned], n, chunk)
+        Ap = Ad[:, k0:k1]
+        Bp = Bd[k0:k1]
+        plan.execute(scratch.data_ptr(), n, Ap.data_ptr(), Ap.stride(0), Bp.data_ptr(),
+                     Bp.stride(0), torch.cuda.current_stream().cuda_stream)
+        plan.close()
+    got = torch.cat(owned, 0).cpu().numpy()
+    assert_match(sid, got, want)
