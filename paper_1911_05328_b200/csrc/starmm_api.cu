@@ -11,6 +11,7 @@
 //                               blocks never cleared, fresh/reuse/high-water counters
 //   co3 merge ................. ops.merge_tasks (ops.py:108-155)
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <vector>
@@ -808,10 +809,10 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (prev_dev != P->device) CK(cudaSetDevice(P->device));
     const size_t eb = (size_t)elem_bytes(P->sr);
     const long long m = P->m, n = P->n, k = P->k;
-    // auto: ~one block per 2e12 semiring ops (>= ~30 ms of B200 work, so per-block
-    // guards / packing stay negligible), at most 8 blocks
+    // auto: ~one block per 1e12 semiring ops (>= ~15 ms of B200 work, so per-block
+    // guards / packing stay negligible), at most 16 blocks
     long long auto_blocks = std::max<long long>(1, std::min<long long>(
-        8, (long long)(2.0 * (double)m * (double)n * (double)k / 2e12)));
+        16, (long long)(2.0 * (double)m * (double)n * (double)k / 1e12)));
     long long R = block_rows > 0 ? block_rows
                                  : std::max<long long>(128, round_up((m + auto_blocks - 1) / auto_blocks, 128));
     R = std::min(R, m);
@@ -821,7 +822,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     cudaStream_t up = nullptr, down = nullptr;
     CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev_in(nblk + 1), ev_done(nblk);
+    std::vector<cudaEvent_t> ev_in(nblk), ev_done(nblk);
     for (auto& e : ev_in) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     void *dA = nullptr, *dB = nullptr, *dC = nullptr;
@@ -833,32 +834,66 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if (!same_ab && (rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
         if (same_ab) dB = dA;
         if ((rc = P->arena.acquire(c_bytes, &dC, false, &fr, &ru))) break;
-        // uploads: B first (every block needs all of it; when B aliases A that is all
-        // of A), then the A/C row blocks in order
-        if ((rc = cuda_status(cudaMemcpy2DAsync(dB, n * eb, B, ldb * eb, n * eb, k,
-                                                cudaMemcpyHostToDevice, up)))) break;
-        if ((rc = cuda_status(cudaEventRecord(ev_in[0], up)))) break;
-        for (long long b = 0; b < nblk && !rc; ++b) {
-            long long r0 = b * R, rows = std::min(R, m - r0);
-            if (!same_ab)
-                rc = cuda_status(cudaMemcpy2DAsync((char*)dA + r0 * k * eb, k * eb,
-                                                   (const char*)A + r0 * lda * eb, lda * eb, k * eb, rows,
-                                                   cudaMemcpyHostToDevice, up));
-            if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)dC + r0 * n * eb, n * eb,
-                                                        (const char*)C + r0 * ldc * eb, ldc * eb, n * eb,
-                                                        rows, cudaMemcpyHostToDevice, up));
-            if (!rc) rc = cuda_status(cudaEventRecord(ev_in[b + 1], up));
+        // Upload order on `up`: block 0 of A and C, then B in k-chunks of R rows (when
+        // B aliases A those chunks ARE A's row blocks), then the remaining A/C blocks.
+        // Block 0 computes chunk by chunk as B arrives -- C0 (+)= sum_kc A0[:,kc] (x)
+        // B[kc,:] is exact by associativity -- so only the first chunk's transfer is
+        // exposed; later blocks need all of B and find it resident.
+        const long long KC = R;   // tools/e2e_ab.py: 299 ms vs 328 ms unchunked (config 4)
+        const long long nkc = (k + KC - 1) / KC;
+        std::vector<cudaEvent_t> ev_kc(nkc);
+        for (auto& e : ev_kc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        auto up_rows = [&](void* dst, const void* src, long long ld_src, long long cols, long long r0,
+                           long long rows) {
+            return cuda_status(cudaMemcpy2DAsync((char*)dst + r0 * cols * eb, cols * eb,
+                                                 (const char*)src + r0 * ld_src * eb, ld_src * eb,
+                                                 cols * eb, rows, cudaMemcpyHostToDevice, up));
+        };
+        const long long rows0 = std::min(R, m);
+        if (!same_ab && (rc = up_rows(dA, A, lda, k, 0, rows0))) break;
+        if ((rc = up_rows(dC, C, ldc, n, 0, rows0))) break;
+        if ((rc = cuda_status(cudaEventRecord(ev_in[0], up)))) break;     // A0, C0 resident
+        for (long long c = 0; c < nkc && !rc; ++c) {
+            long long k0 = c * KC, kr = std::min(KC, k - k0);
+            if (same_ab) {
+                if (c > 0) rc = up_rows(dA, A, lda, k, k0, kr);               // A row block c
+            } else {
+                rc = up_rows(dB, B, ldb, n, k0, kr);
+            }
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_kc[c], up));
         }
+        for (long long b = 1; b < nblk && !rc; ++b) {
+            long long r0 = b * R, rows = std::min(R, m - r0);
+            if (!same_ab) rc = up_rows(dA, A, lda, k, r0, rows);
+            if (!rc) rc = up_rows(dC, C, ldc, n, r0, rows);
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_in[b], up));
+        }
+        if (rc) { for (auto& e : ev_kc) cudaEventDestroy(e); break; }
+        const long long saved_m = P->m, saved_k = P->k;
+        const int saved_flags = P->flags;
+        // block 0, chunk by chunk
+        if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[0], 0)))) { for (auto& e : ev_kc) cudaEventDestroy(e); break; }
+        for (long long c = 0; c < nkc && !rc; ++c) {
+            long long k0 = c * KC, kr = std::min(KC, k - k0);
+            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_kc[c], 0)))) break;
+            P->m = rows0;
+            P->k = kr;
+            if (c > 0) P->flags &= ~STARMM_F_INIT_IDENTITY;   // later chunks fold into C
+            rc = execute_impl(P, dC, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true);
+            P->m = saved_m; P->k = saved_k; P->flags = saved_flags;
+        }
+        for (auto& e : ev_kc) cudaEventDestroy(e);
         if (rc) break;
-        if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[0], 0)))) break;
-        const long long saved_m = P->m;
         for (long long b = 0; b < nblk && !rc; ++b) {
             long long r0 = b * R, rows = std::min(R, m - r0);
-            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[b + 1], 0)))) break;
-            P->m = rows;
-            rc = execute_impl(P, (char*)dC + r0 * n * eb, n, (char*)dA + r0 * k * eb, k, dB, n, cs, true);
-            P->m = saved_m;
-            if (rc) break;
+            if (b > 0) {
+                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[b], 0)))) break;
+                P->m = rows;
+                rc = execute_impl(P, (char*)dC + r0 * n * eb, n, (char*)dA + r0 * k * eb, k, dB, n, cs,
+                                  true);
+                P->m = saved_m;
+                if (rc) break;
+            }
             if ((rc = cuda_status(cudaEventRecord(ev_done[b], cs)))) break;
             if ((rc = cuda_status(cudaStreamWaitEvent(down, ev_done[b], 0)))) break;
             rc = cuda_status(cudaMemcpy2DAsync((char*)C + r0 * ldc * eb, ldc * eb, (char*)dC + r0 * n * eb,

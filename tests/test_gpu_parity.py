@@ -368,7 +368,9 @@ def test_host_path_streams_row_blocks(sid, pinned, block_rows):
     with sm.Executor(sm.Config(base_dim=32, workers=148)) as ex:
         ex.execute_host("star", Ct, At, Bt, s, block_rows=block_rows)
         if block_rows:
-            assert ex.last_stats["executes"] == -(-n // block_rows)
+            # row blocks + the first block's k-chunks (computed as B streams in)
+            nb = -(-n // block_rows)
+            assert ex.last_stats["executes"] == (nb - 1) + nb
     assert_match(sid, Ct.numpy(), want)
 
 
