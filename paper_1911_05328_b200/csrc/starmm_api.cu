@@ -850,7 +850,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                                                  cols * eb, rows, cudaMemcpyHostToDevice, up));
         };
         const long long rows0 = std::min(R, m);
-        if (!same_ab && (rc = up_rows(dA, A, lda, k, 0, rows0))) break;
+        if ((rc = up_rows(dA, A, lda, k, 0, rows0))) break;    // (= B's chunk 0 when aliased)
         if ((rc = up_rows(dC, C, ldc, n, 0, rows0))) break;
         if ((rc = cuda_status(cudaEventRecord(ev_in[0], up)))) break;     // A0, C0 resident
         for (long long c = 0; c < nkc && !rc; ++c) {
