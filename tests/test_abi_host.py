@@ -181,3 +181,27 @@ def test_semiring_elementwise_ops():
     with pytest.raises(KeyError):
         sm.get_semiring("bogus")
     assert sm.get_semiring("tropical_f32").dtype == np.float32
+
+
+def test_fixture_text_roundtrip_matches_reference_format(tmp_path):
+    s = sm.TROPICAL
+    M = sm.Matrix(np.array([[0.0, np.inf], [2.0, 3.5]]), s, device="cpu")
+    p = tmp_path / "m.txt"
+    sm.save_matrix_text(M, p)
+    assert p.read_text() == "2 2 tropical\n0 inf\n2 3.5\n"
+    back = sm.load_matrix_text(p, device="cpu")
+    assert back.semiring is s and np.array_equal(back.numpy(), M.numpy())
+    I = sm.Matrix(np.array([[1, -2]], dtype=np.int64), sm.INT_RING, device="cpu")
+    sm.save_matrix_text(I, p)
+    assert p.read_text() == "1 2 int\n1 -2\n"
+    with pytest.raises(sm.DimMismatch):
+        p.write_text("2 2 int\n1 2 3\n")
+        sm.load_matrix_text(p, device="cpu")
+
+
+def test_cli_invalid_inputs_exit_2():
+    from paper_1911_05328_b200.cli import main
+    assert main(["analyze"]) == 2
+    assert main(["simulate"]) == 2
+    assert main(["run", "--algo", "bogus"]) == 2
+    assert main(["bench", "--algos", "strassen"]) == 2

@@ -424,3 +424,19 @@ def test_fused_ksplit_combine_single_gpu_emulation(sid, ks):
         plan.close()
     got = torch.cat(owned, 0).cpu().numpy()
     assert_match(sid, got, want)
+
+
+# ---- CLI ---------------------------------------------------
+def test_cli_run_verify_bench(tmp_path, capsys):
+    from paper_1911_05328_b200.cli import main
+    assert main(["run", "--algo", "co2", "--n", "64", "--b", "8", "--semiring", "int", "--seed", "1"]) == 0
+    assert main(["run", "--algo", "strassen", "--semiring", "tropical"]) == 2   # NoAdditiveInverse
+    assert main(["run", "--algo", "tar", "--n", "3", "--b", "1"]) == 2          # InvalidSplit
+    assert main(["verify", "--suite", "space"]) == 0
+    assert main(["verify", "--suite", "correctness", "--seeds", "1"]) == 0
+    out = tmp_path / "b.csv"
+    assert main(["bench", "--algos", "co2,co3,tar,star", "--n", "512", "--b", "64", "--reps",
+                 "2", "--out", str(out)]) == 0
+    rows = out.read_text().strip().split("\n")
+    assert rows[0] == "algo,n,b,p,median_ns,speedup_vs_co2_pct,speedup_vs_co3_pct"
+    assert len(rows) == 1 + 4
