@@ -45,14 +45,15 @@ struct DmmaCfg {
     static constexpr int B_LD = BN + 4;
     static constexpr int A_STAGE = BM * A_LD;
     static constexpr int B_STAGE = BK * B_LD;
-    static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 64;
+    static constexpr int SMEM_BYTES = STAGES * (A_STAGE + B_STAGE) * 8 + 16 * STAGES + 64;
     static_assert(BK % 4 == 0 && (BK * BM / 2) % THREADS == 0 && (BK * BN / 2) % THREADS == 0,
                   "cp.async chunking");
 };
 
 // The production configuration (selected by tools/sweep_dmma.cu on B200):
-// 64x128 tiles, 4 warps of 32x64, 3-stage ring, two CTAs per SM so one CTA's
-// barrier / epilogue overlaps the other's DMMA stream.
+// 64x128 tiles, 4 warps of 32x64, 4-stage ring, two CTAs per SM so one CTA's
+// stage boundaries / epilogue overlap the other's DMMA stream; launched as the
+// mbarrier-pipelined dmma_fp64_kernel_mb (below).
 using DmmaProd = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
 
 struct DmmaParams {
@@ -166,6 +167,140 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel(Dm
         }
         cp_async_wait<0>();
         __syncthreads();
+
+        writeback<SrFp64, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
+                                  [&](auto f) {
+#pragma unroll
+            for (int i = 0; i < MI; ++i)
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) {
+                    int r = wm * K::WTM + i * 8 + gi;
+                    int c = wn * K::WTN + j * 8 + ti * 2;
+                    f(r, c, acc[i][j][0]);
+                    f(r, c + 1, acc[i][j][1]);
+                }
+        });
+    }
+}
+
+// ---- mbarrier-pipelined variant ------------------------------------------------
+// Same tiles and fragments; the CTA-wide __syncthreads of every k-stage is replaced by
+// two mbarriers per ring slot: full[s] completes when every thread's cp.async into the
+// slot has landed (cp.async.mbarrier.arrive.noinc), empty[s] when every thread has read
+// it.  Warps drift up to a stage apart instead of meeting at each stage boundary.
+STARMM_DEV void mbar_init(unsigned long long* bar, unsigned count) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(a), "r"(count));
+}
+STARMM_DEV void mbar_arrive(unsigned long long* bar) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}\n" ::"r"(a)
+                 : "memory");
+}
+STARMM_DEV void mbar_cp_async_arrive(unsigned long long* bar) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(a) : "memory");
+}
+STARMM_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
+    unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT_%=;\n\t}\n" ::"r"(a), "r"(parity) : "memory");
+}
+
+template <class K>
+__global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb(DmmaParams p) {
+    constexpr int BM = K::BM, BN = K::BN, BK = K::BK, STAGES = K::STAGES;
+    constexpr int A_LD = K::A_LD, B_LD = K::B_LD, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
+    constexpr int THREADS = K::THREADS, MI = K::MI, NJ = K::NJ;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    double* As = reinterpret_cast<double*>(smem_raw);
+    double* Bs = As + STAGES * A_STAGE;
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(Bs + STAGES * B_STAGE);
+    unsigned long long* empty = full + STAGES;
+    int* smem_word = reinterpret_cast<int*>(empty + STAGES);
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int wm = warp / K::WN, wn = warp % K::WN;
+    const int gi = lane >> 2, ti = lane & 3;
+    const TaskGrid& g = p.g;
+    const int nk = (int)(g.kslice / BK);
+    if (tid == 0) {
+        for (int st = 0; st < STAGES; ++st) {
+            mbar_init(&full[st], THREADS);
+            mbar_init(&empty[st], THREADS);
+        }
+    }
+    __syncthreads();
+    long long gk = 0;   // global stage counter: slot = gk % STAGES, use = gk / STAGES
+
+    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
+        int tm, tn, s, tile;
+        decode_task(g, t, tm, tn, s, tile);
+        const int mode = task_mode(p.w, g, s);
+        int pair_seen = PAIR_EMPTY;
+        if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
+
+        const double* Ag = p.A + (long long)tm * BM * p.lda + (long long)s * g.kslice;
+        const double* Bg = p.B + (long long)s * g.kslice * p.ldb + (long long)tn * BN;
+
+        auto fill = [&](int kt) {   // k-stage kt of this task into slot (gk + kt) % STAGES
+            const long long gidx = gk + kt;
+            const int slot = (int)(gidx % STAGES);
+            if (gidx >= STAGES) mbar_wait(&empty[slot], (unsigned)(((gidx / STAGES) - 1) & 1));
+            const double* a = Ag + (long long)kt * BK;
+            double* as = As + slot * A_STAGE;
+            constexpr int A_CH = BK / 2;
+#pragma unroll
+            for (int i = 0; i < BM * A_CH / THREADS; ++i) {
+                int c = tid + i * THREADS;
+                int r = c / A_CH, q = c % A_CH;
+                cp_async16(as + r * A_LD + q * 2, a + (long long)r * p.lda + q * 2);
+            }
+            const double* b = Bg + (long long)kt * BK * p.ldb;
+            double* bs = Bs + slot * B_STAGE;
+            constexpr int B_CH = BN / 2;
+#pragma unroll
+            for (int i = 0; i < BK * B_CH / THREADS; ++i) {
+                int c = tid + i * THREADS;
+                int r = c / B_CH, q = c % B_CH;
+                cp_async16(bs + r * B_LD + q * 2, b + (long long)r * p.ldb + q * 2);
+            }
+            mbar_cp_async_arrive(&full[slot]);
+        };
+
+        double acc[MI][NJ][2];
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+            for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+        for (int st = 0; st < STAGES - 1 && st < nk; ++st) fill(st);
+        for (int kt = 0; kt < nk; ++kt) {
+            const long long gidx = gk + kt;
+            const int slot = (int)(gidx % STAGES);
+            mbar_wait(&full[slot], (unsigned)((gidx / STAGES) & 1));
+            const double* as = As + slot * A_STAGE + (wm * K::WTM + gi) * A_LD + ti;
+            const double* bs = Bs + slot * B_STAGE + ti * B_LD + wn * K::WTN + gi;
+#pragma unroll
+            for (int kk = 0; kk < BK; kk += 4) {
+                double a[MI], b[NJ];
+#pragma unroll
+                for (int i = 0; i < MI; ++i) a[i] = as[i * 8 * A_LD + kk];
+#pragma unroll
+                for (int j = 0; j < NJ; ++j) b[j] = bs[kk * B_LD + j * 8];
+#pragma unroll
+                for (int i = 0; i < MI; ++i)
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) dmma_884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            }
+            mbar_arrive(&empty[slot]);
+            const int nxt = kt + STAGES - 1;
+            if (nxt < nk) fill(nxt);
+        }
+        gk += nk;
 
         writeback<SrFp64, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                                   [&](auto f) {

@@ -7,7 +7,7 @@
 #include "../paper_1911_05328_b200/csrc/dmma_kernel.cuh"
 using namespace starmm;
 
-template <class K>
+template <class K, bool MB = false>
 void run(const char* name, int n, double* A, double* B, double* C, unsigned long long* cnt, int sms,
          int group_m = 8, bool persistent = true) {
     DmmaParams p{};
@@ -18,15 +18,16 @@ void run(const char* name, int n, double* A, double* B, double* C, unsigned long
     WbParams& w = p.w;
     w.mode_base = 0; w.init_identity = 0; w.C = C; w.ldc = n; w.M = n; w.N = n;
     w.counters = cnt;
-    cudaFuncSetAttribute(dmma_fp64_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+    auto kern = MB ? dmma_fp64_kernel_mb<K> : dmma_fp64_kernel<K>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
     int occ = 0;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, dmma_fp64_kernel<K>, K::THREADS, K::SMEM_BYTES);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K::THREADS, K::SMEM_BYTES);
     int grid = sms * (occ > 0 ? occ : 1);
     if (grid > g.num_tasks || !persistent) grid = g.num_tasks;
-    dmma_fp64_kernel<K><<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
+    kern<<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    for (int i = 0; i < 3; ++i) dmma_fp64_kernel<K><<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
+    for (int i = 0; i < 3; ++i) kern<<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
     cudaError_t e = cudaGetLastError();
@@ -43,11 +44,10 @@ int main(int argc, char** argv) {
     cudaMalloc(&cnt, 64 * 8);
     cudaMemset(A, 0, (size_t)n * n * 8); cudaMemset(B, 0, (size_t)n * n * 8); cudaMemset(C, 0, (size_t)n * n * 8);
     using P = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
-    int only_g = argc > 2 ? atoi(argv[2]) : 0;
-    for (int gm : {4, 8, 16, 24, 32, 64}) {
-        if (only_g && gm != only_g) continue;
-        char name[64]; snprintf(name, sizeof name, "64x128_s4_g%d", gm);
-        run<P>(name, n, A, B, C, cnt, sms, gm, true);
-    }
+    run<P>("sync_64x128_s4", n, A, B, C, cnt, sms, 24, true);
+    run<P, true>("mbar_64x128_s4", n, A, B, C, cnt, sms, 24, true);
+    run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
+    run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
+    run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
     return 0;
 }
