@@ -192,7 +192,8 @@ constexpr int BM = 128, BNW = 128, STAGES = 3, THREADS = 256;   // BNW: B positi
 template <class Pol> constexpr int bn() { return BNW * Pol::OUTS; }   // output columns per tile
 template <class Pol>
 constexpr int smem_bytes() {
-    return STAGES * (BM + BNW) * (Pol::BK / Pol::KSTEP) * Pol::G * (int)sizeof(typename Pol::Tp) + 64;
+    return STAGES * (BM + BNW) * (Pol::BK / Pol::KSTEP) * Pol::G * (int)sizeof(typename Pol::Tp) +
+           16 * STAGES + 64;
 }
 }  // namespace simt
 
@@ -204,7 +205,7 @@ struct SimtParams {
     WbParams w;
 };
 
-template <class Pol, class Sr, int MINB = 1>
+template <class Pol, class Sr, int MINB = 1, bool MB = false>
 __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams p) {
     using namespace simt;
     using Tp = typename Pol::Tp;
@@ -220,7 +221,9 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Tp* As = reinterpret_cast<Tp*>(smem_raw);
     Tp* Bs = As + STAGES * A_STAGE;
-    int* smem_word = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
+    unsigned long long* full = reinterpret_cast<unsigned long long*>(Bs + STAGES * B_STAGE);
+    unsigned long long* empty = full + STAGES;
+    int* smem_word = reinterpret_cast<int*>(empty + STAGES);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ty = (warp >> 1) * 4 + (lane >> 3);      // 0..15
@@ -229,6 +232,18 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     const int nk = (int)(g.kslice / BK);
     const Tp* Ap = reinterpret_cast<const Tp*>(p.Ap);
     const Tp* Bp = reinterpret_cast<const Tp*>(p.Bp);
+    if constexpr (MB) {          // mbarrier ring (see dmma_fp64_kernel_mb); off by default:
+                                 // tools/sweep_simt.cu shows the spin costs these
+                                 // issue-bound loops 2-6%
+        if (tid == 0) {
+            for (int st = 0; st < STAGES; ++st) {
+                mbar_init(&full[st], THREADS);
+                mbar_init(&empty[st], THREADS);
+            }
+        }
+        __syncthreads();
+    }
+    long long gk = 0;
 
     for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
         int tm, tn, s, tile;
@@ -264,19 +279,9 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = Pol::init();
 
-#pragma unroll
-        for (int st = 0; st < STAGES - 1; ++st) {
-            if (st < nk) load_stage(st, st);
-            cp_async_commit();
-        }
-        for (int kt = 0; kt < nk; ++kt) {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            int nxt = kt + STAGES - 1;
-            if (nxt < nk) load_stage(nxt, nxt % STAGES);
-            cp_async_commit();
-            const Tp* as = As + (kt % STAGES) * A_STAGE + ty * VEC * G;
-            const Tp* bs = Bs + (kt % STAGES) * B_STAGE + tx * VEC * G;
+        auto compute_stage = [&](int slot) {
+            const Tp* as = As + slot * A_STAGE + ty * VEC * G;
+            const Tp* bs = Bs + slot * B_STAGE + tx * VEC * G;
 #pragma unroll
             for (int kg = 0; kg < KG; ++kg) {
                 // 8 row operands / 8 column operands, each G elements wide
@@ -300,10 +305,42 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                         }
                     }
             }
+        };
+        if constexpr (MB) {
+            auto fill = [&](int kt) {
+                const long long gidx = gk + kt;
+                const int slot = (int)(gidx % STAGES);
+                if (gidx >= STAGES) mbar_wait(&empty[slot], (unsigned)(((gidx / STAGES) - 1) & 1));
+                load_stage(kt, slot);
+                mbar_cp_async_arrive(&full[slot]);
+            };
+            for (int st = 0; st < STAGES - 1 && st < nk; ++st) fill(st);
+            for (int kt = 0; kt < nk; ++kt) {
+                const long long gidx = gk + kt;
+                const int slot = (int)(gidx % STAGES);
+                mbar_wait(&full[slot], (unsigned)((gidx / STAGES) & 1));
+                compute_stage(slot);
+                mbar_arrive(&empty[slot]);
+                if (kt + STAGES - 1 < nk) fill(kt + STAGES - 1);
+            }
+            gk += nk;
+        } else {
+#pragma unroll
+            for (int st = 0; st < STAGES - 1; ++st) {
+                if (st < nk) load_stage(st, st);
+                cp_async_commit();
+            }
+            for (int kt = 0; kt < nk; ++kt) {
+                cp_async_wait<STAGES - 2>();
+                __syncthreads();
+                int nxt = kt + STAGES - 1;
+                if (nxt < nk) load_stage(nxt, nxt % STAGES);
+                cp_async_commit();
+                compute_stage(kt % STAGES);
+            }
+            cp_async_wait<0>();
+            __syncthreads();
         }
-        cp_async_wait<0>();
-        __syncthreads();
-
         using T = typename Sr::T;
         writeback<Sr, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                               [&](auto f) {

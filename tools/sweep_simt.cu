@@ -6,7 +6,7 @@
 #include "../paper_1911_05328_b200/csrc/simt_kernel.cuh"
 using namespace starmm;
 
-template <class Pol, class Sr, int MINB>
+template <class Pol, class Sr, int MINB, bool MB = true>
 void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long long* cnt, int sms) {
     SimtParams p{};
     p.Ap = Ap; p.Bp = Bp; p.Mp = n; p.Np = n;
@@ -15,7 +15,7 @@ void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long lon
     g.num_tasks = g.tiles_m * g.tiles_n;
     WbParams& w = p.w;
     w.mode_base = 0; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
-    auto kern = simt_mm_kernel<Pol, Sr, MINB>;
+    auto kern = simt_mm_kernel<Pol, Sr, MINB, MB>;
     constexpr int smem = simt::smem_bytes<Pol>();
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int occ = 0;
@@ -39,16 +39,12 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
-    run<PolI8Dp4a, SrInt64, 1>("i64_dp4a_occ1", n, A, B, C, cnt, sms);
-    run<PolS16x2Min, SrTropF32, 1>("minplus_s16x2_occ1", n, A, B, C, cnt, sms);
-    run<PolF32Pair, SrTropF32, 1>("f32_fadd2_fmnmx3_occ1", n, A, B, C, cnt, sms);
-    run<PolF32Pair, SrTropF32, 2>("f32_fadd2_fmnmx3_occ2", n, A, B, C, cnt, sms);
-    run<PolF32Single, SrTropF32, 1>("f32_fadd_fmnmx_occ1", n, A, B, C, cnt, sms);
-    run<PolF32Single, SrTropF32, 2>("f32_fadd_fmnmx_occ2", n, A, B, C, cnt, sms);
-    run<PolF32PairMin2, SrTropF32, 1>("f32_fadd2_2fmnmx_occ1", n, A, B, C, cnt, sms);
-    run<PolI32Vmin, SrTropI32, 1>("i32_viaddmnmx_occ1", n, A, B, C, cnt, sms);
-    run<PolI32Vmin, SrTropI32, 2>("i32_viaddmnmx_occ2", n, A, B, C, cnt, sms);
-    run<PolI64Narrow, SrInt64, 1>("i64narrow_imad_occ1", n, A, B, C, cnt, sms);
-    run<PolI64Narrow, SrInt64, 2>("i64narrow_imad_occ2", n, A, B, C, cnt, sms);
+    run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_sync", n, A, B, C, cnt, sms);
+    run<PolI8Dp4a, SrInt64, 1, true>("i64_dp4a_mbar", n, A, B, C, cnt, sms);
+    run<PolS16x2Min, SrTropF32, 1, false>("minplus_s16x2_sync", n, A, B, C, cnt, sms);
+    run<PolS16x2Min, SrTropF32, 1, true>("minplus_s16x2_mbar", n, A, B, C, cnt, sms);
+    run<PolF32Pair, SrTropF32, 1, false>("f32_fadd2_fmnmx3_sync", n, A, B, C, cnt, sms);
+    run<PolF32Pair, SrTropF32, 1, true>("f32_fadd2_fmnmx3_mbar", n, A, B, C, cnt, sms);
+    run<PolI64Narrow, SrInt64, 1, true>("i64narrow_imad_mbar", n, A, B, C, cnt, sms);
     return 0;
 }
