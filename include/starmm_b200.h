@@ -31,6 +31,8 @@
  *                        ops.accumulate_region (ops.py:76-101): concurrent-safe
  *                        C <- C (+) P (hardware atomics / per-tile slots).
  *   starmm_strerror      str(exception) for the status taxonomy.
+ *   STARMM_STRASSEN..    strassen_parallel / sar_strassen / star_strassen_1/2
+ *                        (strassen.py:211-235) via starmm_execute.
  *
  * Matrices are row-major with a leading dimension in ELEMENTS (ld >= cols),
  * like MatrixRegion.row_stride (matrix.py:144-146).  The caller owns A, B and
@@ -73,9 +75,12 @@ enum starmm_semiring {
     STARMM_SR_TROPICAL_I32 = 4    /* "tropical_i32": int32 (min,+), INT32_MAX=+inf */
 };
 
-/* ---- schedules (registry.py:11 CLASSICAL) ------------------------------ */
+/* ---- schedules (registry.py:11-13 CLASSICAL + STRASSEN_FAMILY) ---------- */
 enum starmm_algo {
-    STARMM_CO2 = 0, STARMM_CO3 = 1, STARMM_TAR = 2, STARMM_SAR = 3, STARMM_STAR = 4
+    STARMM_CO2 = 0, STARMM_CO3 = 1, STARMM_TAR = 2, STARMM_SAR = 3, STARMM_STAR = 4,
+    /* the fast family (strassen.py): rings only, OVERWRITES C with A (x) B */
+    STARMM_STRASSEN = 5, STARMM_SAR_STRASSEN = 6, STARMM_STAR_STRASSEN_1 = 7,
+    STARMM_STAR_STRASSEN_2 = 8
 };
 
 /* ---- allocation modes (registry.py:20,32-33) ---------------------------- */
@@ -147,6 +152,10 @@ int  starmm_plan_set_peers(starmm_plan* plan, int nparts, void* const* bases, in
 int  starmm_ipc_handle(const void* dptr, void* handle_out);
 int  starmm_ipc_open(const void* handle, void** dptr_out);
 int  starmm_ipc_close(void* dptr);
+/* Strassen family: recursion stops (classical tile kernel) once the half size would
+ * drop below max(base_dim, leaf); default leaf 1024 keeps GPU leaves large.
+ * Replaces strassen._strassen_root's "C.rows == ex.cfg.base_dim" test (strassen.py:184-207). */
+int  starmm_plan_set_strassen_leaf(starmm_plan* plan, int64_t leaf);
 int  starmm_plan_stats(starmm_plan* plan, starmm_stats* out);
 int  starmm_plan_reset_stats(starmm_plan* plan);
 void starmm_plan_destroy(starmm_plan* plan);

@@ -18,7 +18,8 @@ LIB_PATH = os.path.join(_HERE, "libstarmm_b200.so")
 
 # enums (include/starmm_b200.h)
 SR_INT64, SR_FP64, SR_TROPICAL_F64, SR_TROPICAL_F32, SR_TROPICAL_I32 = range(5)
-ALGO_IDS = {"co2": 0, "co3": 1, "tar": 2, "sar": 3, "star": 4}
+ALGO_IDS = {"co2": 0, "co3": 1, "tar": 2, "sar": 3, "star": 4, "strassen": 5, "sar-strassen": 6,
+            "star-strassen-1": 7, "star-strassen-2": 8}
 ALLOC_IDS = {"pooled": 0, "raw": 1}
 F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2, F_TIME_MAIN = 0x1, 0x2, 0x4, 0x8, 0x10
 
@@ -81,6 +82,8 @@ def lib():
         L.starmm_execute.restype = ci
         L.starmm_execute_host.argtypes = [vp, vp, i64, vp, i64, vp, i64, vp, i64]
         L.starmm_execute_host.restype = ci
+        L.starmm_plan_set_strassen_leaf.argtypes = [vp, i64]
+        L.starmm_plan_set_strassen_leaf.restype = ci
         L.starmm_plan_set_peers.argtypes = [vp, ci, ctypes.POINTER(vp), i64, i64]
         L.starmm_plan_set_peers.restype = ci
         L.starmm_ipc_handle.argtypes = [vp, ctypes.c_char_p]
@@ -140,6 +143,9 @@ class Plan:
                      stream: int, block_rows: int = 0) -> None:
         check(lib().starmm_execute_host(self._h, C_ptr, ldc, A_ptr, lda, B_ptr, ldb, stream,
                                         block_rows), "starmm_execute_host")
+
+    def set_strassen_leaf(self, leaf: int) -> None:
+        check(lib().starmm_plan_set_strassen_leaf(self._h, int(leaf)), "starmm_plan_set_strassen_leaf")
 
     def set_peers(self, bases, ld: int, rows_per_part: int) -> None:
         """Route every tile's atomic-madd to the owner part's buffer (fused k-split combine)."""

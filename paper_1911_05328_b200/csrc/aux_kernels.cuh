@@ -294,3 +294,36 @@ __global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr:
 }
 
 }  // namespace starmm
+
+namespace starmm {
+
+// ---- ring combinations for the Strassen family (strassen.py:29-58) ---------
+// dst <- beta*dst + ax*X + ay*Y with coefficients in {-1, 0, 1}; int64 uses
+// unsigned arithmetic so every step wraps mod 2^64 exactly like numpy's int64
+// (the ring is Z/2^64, where Strassen's subtractions are exact).
+template <class T> STARMM_DEV T ring_mac(T acc, int c, T x);
+template <> STARMM_DEV long long ring_mac<long long>(long long acc, int c, long long x) {
+    unsigned long long a = (unsigned long long)acc, v = (unsigned long long)x;
+    return (long long)(c > 0 ? a + v : (c < 0 ? a - v : a));
+}
+template <> STARMM_DEV double ring_mac<double>(double acc, int c, double x) {
+    return c > 0 ? acc + x : (c < 0 ? acc - x : acc);
+}
+
+template <class T>
+__global__ void ring_combine_kernel(T* D, long long ldd, const T* X, long long ldx, const T* Y,
+                                    long long ldy, long long rows, long long cols, int beta, int ax,
+                                    int ay) {
+    long long total = rows * cols;
+    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (long long)gridDim.x * blockDim.x) {
+        long long r = idx / cols, c = idx - r * cols;
+        T acc = beta ? D[r * ldd + c] : (T)0;
+        if (beta < 0) acc = ring_mac<T>((T)0, -1, acc);
+        if (ax) acc = ring_mac<T>(acc, ax, X[r * ldx + c]);
+        if (ay) acc = ring_mac<T>(acc, ay, Y[r * ldy + c]);
+        D[r * ldd + c] = acc;
+    }
+}
+
+}  // namespace starmm

@@ -114,6 +114,8 @@ struct starmm_plan {
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
+    long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
+    long long str_issued = 0;                   // Strassen temporaries currently issued
     // peer destinations of the fused k-split combine (starmm_plan_set_peers)
     int remote_parts = 0;
     long long remote_rows = 0, remote_ld = 0;
@@ -346,9 +348,13 @@ int starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mod
     if (!plan) return STARMM_CONTRACT_VIOLATION;
     *plan = nullptr;
     if (semiring < 0 || semiring > STARMM_SR_TROPICAL_I32) return STARMM_CONTRACT_VIOLATION;
-    if (algo < STARMM_CO2 || algo > STARMM_STAR) return STARMM_CONTRACT_VIOLATION;
+    if (algo < STARMM_CO2 || algo > STARMM_STAR_STRASSEN_2) return STARMM_CONTRACT_VIOLATION;
     if (alloc_mode != STARMM_POOLED && alloc_mode != STARMM_RAW) return STARMM_CONTRACT_VIOLATION;
-    if (alloc_mode == STARMM_RAW && algo != STARMM_CO3) return STARMM_CONTRACT_VIOLATION;  // registry.py:34-35
+    if (alloc_mode == STARMM_RAW && algo != STARMM_CO3 && algo != STARMM_STRASSEN)
+        return STARMM_CONTRACT_VIOLATION;                                     // registry.py:34-35
+    // the fast family subtracts: rings only (registry.py:41-42)
+    if (algo >= STARMM_STRASSEN && semiring != STARMM_SR_INT64 && semiring != STARMM_SR_FP64)
+        return STARMM_NO_ADDITIVE_INVERSE;
     if (m < 1 || n < 1 || k < 1) return STARMM_DIM_MISMATCH;
     if (!is_pow2(base_dim) || workers < 1) return STARMM_CONTRACT_VIOLATION;          // matrix.py:44-47
     if (ksplit_log2 > 16) return STARMM_CONTRACT_VIOLATION;
@@ -753,9 +759,247 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     return STARMM_OK;
 }
 
+// ============================================================================
+// The Strassen family (strassen.py:1-235): C <- A (x) B over a ring, overwriting C.
+// One building block, mm(C, A, B, mode) with mode = store / add / sub, recursed on the
+// host; leaves are the tile kernels (CO2 plan on the sub-problem), operand sums and
+// the signed assembly are ring_combine kernels.  The variants differ in temporaries
+// exactly as the reference: the straightforward step materialises every operand sum
+// and all seven products (<= 17 half-size blocks per level); the sar step owns three
+// LIFO-reused blocks (S, T, P) and merges each product into the quadrants it feeds;
+// star-strassen-1 runs classical 8-way levels above switch_depth(workers), -2 runs
+// straightforward levels there; both use the sar step below.
+namespace {
+
+struct Combo { int r1, c1, op, r2, c2; };   // op: 0 bare quadrant, +1 add, -1 sub
+// strassen.py:30-47
+const Combo S_DEFS[8] = {{0, 0, 0, 0, 0}, {0, 0, 1, 1, 1}, {1, 0, 1, 1, 1}, {0, 0, 0, 0, 0},
+                         {1, 1, 0, 0, 0}, {0, 0, 1, 0, 1}, {1, 0, -1, 0, 0}, {0, 1, -1, 1, 1}};
+const Combo T_DEFS[8] = {{0, 0, 0, 0, 0}, {0, 0, 1, 1, 1}, {0, 0, 0, 0, 0}, {0, 1, -1, 1, 1},
+                         {1, 0, -1, 0, 0}, {1, 1, 0, 0, 0}, {0, 0, 1, 0, 1}, {1, 0, 1, 1, 1}};
+struct Term { int r, sign; };
+// strassen.py:49-54 (C_FORMULAS), indexed [qi][qj]
+const Term C_FORM[2][2][4] = {{{{1, 1}, {4, 1}, {5, -1}, {7, 1}}, {{3, 1}, {5, 1}, {0, 0}, {0, 0}}},
+                              {{{2, 1}, {4, 1}, {0, 0}, {0, 0}}, {{1, 1}, {3, 1}, {2, -1}, {6, 1}}}};
+enum MmMode { MM_STORE = 0, MM_ADD = 1, MM_SUB = 2 };
+
+struct StrCtx {
+    starmm_plan* P;
+    cudaStream_t s;
+    size_t eb;
+    long long leaf;
+    int k_switch;
+    int launches;
+};
+
+char* quad(const void* base, long long ld, int i, int j, long long h, size_t eb) {
+    return (char*)base + (size_t)((i * h) * ld + j * h) * eb;
+}
+
+int ring_combine(StrCtx& x, void* D, long long ldd, const void* X, long long ldx, const void* Y,
+                 long long ldy, long long n, int beta, int ax, int ay) {
+    int blocks = grid_blocks(n * n);
+    if (x.P->sr == STARMM_SR_INT64)
+        ring_combine_kernel<long long><<<blocks, 256, 0, x.s>>>((long long*)D, ldd, (const long long*)X,
+                                                               ldx, (const long long*)Y, ldy, n, n,
+                                                               beta, ax, ay);
+    else
+        ring_combine_kernel<double><<<blocks, 256, 0, x.s>>>((double*)D, ldd, (const double*)X, ldx,
+                                                            (const double*)Y, ldy, n, n, beta, ax, ay);
+    ++x.launches;
+    return cuda_status(cudaGetLastError());
+}
+
+int str_acquire(StrCtx& x, long long n, void** out) {
+    size_t bytes = (size_t)(n * n) * x.eb;
+    if (x.P->alloc == STARMM_RAW) {
+        CK(cudaMallocAsync(out, bytes, x.s));
+        ++x.P->raw_count;
+        x.P->raw_bytes += (long long)bytes;
+    } else {
+        TRY(x.P->arena.acquire(bytes, out, true, &x.P->ws_fresh, &x.P->ws_reuse));
+    }
+    x.P->str_issued += (long long)bytes;
+    x.P->ws_high_water = std::max(x.P->ws_high_water, x.P->str_issued);
+    return STARMM_OK;
+}
+
+void str_release(StrCtx& x, void* p, long long n) {
+    size_t bytes = (size_t)(n * n) * x.eb;
+    if (x.P->alloc == STARMM_RAW) cudaFreeAsync(p, x.s);
+    else x.P->arena.release(p, bytes);   // LIFO: the next same-size acquire gets it back
+    x.P->str_issued -= (long long)bytes;
+}
+
+// leaf: the classical tile kernel on an n x n sub-problem (CO2 protocol)
+int str_leaf(StrCtx& x, int mode, void* C, long long ldc, const void* A, long long lda,
+             const void* B, long long ldb, long long n) {
+    starmm_plan* P = x.P;
+    const int sv_algo = P->algo, sv_flags = P->flags, sv_alloc = P->alloc;
+    const long long sv_m = P->m, sv_n = P->n, sv_k = P->k;
+    void* tmp = nullptr;
+    int rc = STARMM_OK;
+    if (mode == MM_SUB && (rc = str_acquire(x, n, &tmp))) return rc;
+    P->algo = STARMM_CO2; P->alloc = STARMM_POOLED;
+    P->m = P->n = P->k = n;
+    P->flags = (sv_flags | STARMM_F_ALLOW_NONPOW2) & ~STARMM_F_INIT_IDENTITY;
+    if (mode != MM_ADD) P->flags |= STARMM_F_INIT_IDENTITY;
+    if (mode == MM_SUB) rc = execute_impl(P, tmp, n, A, lda, B, ldb, x.s, true);
+    else rc = execute_impl(P, C, ldc, A, lda, B, ldb, x.s, true);
+    P->algo = sv_algo; P->flags = sv_flags; P->alloc = sv_alloc;
+    P->m = sv_m; P->n = sv_n; P->k = sv_k;
+    ++x.launches;
+    if (!rc && mode == MM_SUB) rc = ring_combine(x, C, ldc, tmp, n, nullptr, 0, n, 1, -1, 0);
+    if (tmp) str_release(x, tmp, n);
+    return rc;
+}
+
+int str_mm(StrCtx& x, int depth, int mode, void* C, long long ldc, const void* A, long long lda,
+           const void* B, long long ldb, long long n);
+
+// materialise operand r of `defs` from quadrants of X (bare quadrants are used in place)
+int str_operand(StrCtx& x, const Combo& d, const void* X, long long ldx, long long h, void** tmp,
+                const void** op, long long* ld) {
+    if (d.op == 0) {
+        *op = quad(X, ldx, d.r1, d.c1, h, x.eb);
+        *ld = ldx;
+        *tmp = nullptr;
+        return STARMM_OK;
+    }
+    TRY(str_acquire(x, h, tmp));
+    TRY(ring_combine(x, *tmp, h, quad(X, ldx, d.r1, d.c1, h, x.eb), ldx,
+                     quad(X, ldx, d.r2, d.c2, h, x.eb), ldx, h, 0, 1, d.op));
+    *op = *tmp;
+    *ld = h;
+    return STARMM_OK;
+}
+
+// straightforward step (strassen.py:77-93)
+int str_straightforward(StrCtx& x, int depth, int mode, void* C, long long ldc, const void* A,
+                        long long lda, const void* B, long long ldb, long long n) {
+    const long long h = n / 2;
+    void* tS[8] = {}; void* tT[8] = {}; void* tP[8] = {};
+    const void* S[8]; const void* T[8]; long long lS[8], lT[8];
+    int rc = STARMM_OK;
+    for (int r = 1; r <= 7 && !rc; ++r) rc = str_operand(x, S_DEFS[r], A, lda, h, &tS[r], &S[r], &lS[r]);
+    for (int r = 1; r <= 7 && !rc; ++r) rc = str_operand(x, T_DEFS[r], B, ldb, h, &tT[r], &T[r], &lT[r]);
+    for (int r = 1; r <= 7 && !rc; ++r) rc = str_acquire(x, h, &tP[r]);
+    for (int r = 1; r <= 7 && !rc; ++r) rc = str_mm(x, depth + 1, MM_STORE, tP[r], h, S[r], lS[r], T[r], lT[r], h);
+    // assemble each output quadrant from its signed products (ops.py:170-185)
+    for (int qi = 0; qi < 2 && !rc; ++qi)
+        for (int qj = 0; qj < 2 && !rc; ++qj) {
+            char* Cq = quad(C, ldc, qi, qj, h, x.eb);
+            const Term* t = C_FORM[qi][qj];
+            const int flip = (mode == MM_SUB) ? -1 : 1;
+            int beta = (mode == MM_STORE) ? 0 : 1;
+            for (int u = 0; u < 4 && t[u].r && !rc; u += 2) {
+                const bool pair = (u + 1 < 4) && t[u + 1].r;
+                rc = ring_combine(x, Cq, ldc, tP[t[u].r], h, pair ? tP[t[u + 1].r] : nullptr, h, h, beta,
+                                  flip * t[u].sign, pair ? flip * t[u + 1].sign : 0);
+                beta = 1;
+            }
+        }
+    for (int r = 7; r >= 1; --r) if (tP[r]) str_release(x, tP[r], h);
+    for (int r = 7; r >= 1; --r) if (tT[r]) str_release(x, tT[r], h);
+    for (int r = 7; r >= 1; --r) if (tS[r]) str_release(x, tS[r], h);
+    return rc;
+}
+
+// sar step (strassen.py:120-145): per product S, T, P blocks, LIFO-reused across products
+int str_sar(StrCtx& x, int depth, int mode, void* C, long long ldc, const void* A, long long lda,
+            const void* B, long long ldb, long long n) {
+    const long long h = n / 2;
+    bool virgin[2][2] = {{mode == MM_STORE, mode == MM_STORE}, {mode == MM_STORE, mode == MM_STORE}};
+    int rc = STARMM_OK;
+    for (int r = 1; r <= 7 && !rc; ++r) {
+        void *tS = nullptr, *tT = nullptr, *tP = nullptr;
+        const void *Sop, *Top;
+        long long lS, lT;
+        rc = str_operand(x, S_DEFS[r], A, lda, h, &tS, &Sop, &lS);
+        if (!rc) rc = str_operand(x, T_DEFS[r], B, ldb, h, &tT, &Top, &lT);
+        if (!rc) rc = str_acquire(x, h, &tP);
+        if (!rc) rc = str_mm(x, depth + 1, MM_STORE, tP, h, Sop, lS, Top, lT, h);
+        // merge into every quadrant the product feeds (C_USES, strassen.py:56-59)
+        for (int qi = 0; qi < 2 && !rc; ++qi)
+            for (int qj = 0; qj < 2 && !rc; ++qj)
+                for (int u = 0; u < 4; ++u) {
+                    const Term& t = C_FORM[qi][qj][u];
+                    if (t.r != r) continue;
+                    const int sign = (mode == MM_SUB ? -1 : 1) * t.sign;
+                    char* Cq = quad(C, ldc, qi, qj, h, x.eb);
+                    rc = ring_combine(x, Cq, ldc, tP, h, nullptr, 0, h, virgin[qi][qj] ? 0 : 1, sign, 0);
+                    virgin[qi][qj] = false;   // first touch stores (virgin tiles, ops.py:57-65)
+                    break;
+                }
+        if (tP) str_release(x, tP, h);
+        if (tT) str_release(x, tT, h);
+        if (tS) str_release(x, tS, h);
+    }
+    return rc;
+}
+
+// classical 8-way level (star-strassen-1 above the switch, classic.py:86-93)
+int str_classical(StrCtx& x, int depth, int mode, void* C, long long ldc, const void* A,
+                  long long lda, const void* B, long long ldb, long long n) {
+    const long long h = n / 2;
+    int rc = STARMM_OK;
+    for (int k = 0; k < 2 && !rc; ++k)
+        for (int i = 0; i < 2 && !rc; ++i)
+            for (int j = 0; j < 2 && !rc; ++j) {
+                int m = (k == 0) ? mode : (mode == MM_SUB ? MM_SUB : MM_ADD);
+                rc = str_mm(x, depth + 1, m, quad(C, ldc, i, j, h, x.eb), ldc, quad(A, lda, i, k, h, x.eb),
+                            lda, quad(B, ldb, k, j, h, x.eb), ldb, h);
+            }
+    return rc;
+}
+
+int str_mm(StrCtx& x, int depth, int mode, void* C, long long ldc, const void* A, long long lda,
+           const void* B, long long ldb, long long n) {
+    const long long h = n / 2;
+    if ((n & 1) || h < x.leaf) return str_leaf(x, mode, C, ldc, A, lda, B, ldb, n);
+    switch (x.P->algo) {
+    case STARMM_STRASSEN: return str_straightforward(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+    case STARMM_SAR_STRASSEN: return str_sar(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+    case STARMM_STAR_STRASSEN_1:
+        if (depth < x.k_switch) return str_classical(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+        return str_sar(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+    default:   // STARMM_STAR_STRASSEN_2
+        if (depth < x.k_switch) return str_straightforward(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+        return str_sar(x, depth, mode, C, ldc, A, lda, B, ldb, n);
+    }
+}
+
+int strassen_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
+                     int64_t ldb, void* stream) {
+    if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
+    if (P->m != P->n || P->n != P->k) return STARMM_DIM_MISMATCH;
+    if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
+    int prev_dev = 0;
+    CK(cudaGetDevice(&prev_dev));
+    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
+    TRY(ensure_bookkeeping(P));
+    StrCtx x{P, (cudaStream_t)stream, (size_t)elem_bytes(P->sr),
+             std::max<long long>(P->base_dim, P->strassen_leaf), switch_depth(P->workers), 0};
+    int rc = str_mm(x, 0, MM_STORE, C, ldc, A, lda, B, ldb, P->n);
+    if (!rc && !(P->flags & STARMM_F_ASYNC)) rc = cuda_status(cudaStreamSynchronize(x.s));
+    P->st.kernel_launches = x.launches;
+    P->st.executes += 1;
+    if (prev_dev != P->device) cudaSetDevice(prev_dev);
+    return rc;
+}
+
+}  // namespace
+
 int starmm_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda, const void* B,
                    int64_t ldb, void* stream) {
+    if (P && P->algo >= STARMM_STRASSEN) return strassen_execute(P, C, ldc, A, lda, B, ldb, stream);
     return execute_impl(P, C, ldc, A, lda, B, ldb, stream, false);
+}
+
+int starmm_plan_set_strassen_leaf(starmm_plan* P, int64_t leaf) {
+    if (!P || leaf < 1) return STARMM_CONTRACT_VIOLATION;
+    P->strassen_leaf = leaf;
+    return STARMM_OK;
 }
 
 int starmm_plan_set_peers(starmm_plan* P, int nparts, void* const* bases, int64_t ld,

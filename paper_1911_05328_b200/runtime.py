@@ -96,6 +96,8 @@ class Executor:
         if p is None:
             p = _lib.Plan(s.sr_id, algo, mode, m, n, k, cfg.base_dim, cfg.workers, ks,
                           self.device, flags)
+            if cfg.strassen_leaf is not None:
+                p.set_strassen_leaf(cfg.strassen_leaf)
             self._plans[key] = p
         return p
 

@@ -49,7 +49,7 @@ def test_plan_create_validates_before_touching_a_device():
     h = ctypes.c_void_p()
     # unknown semiring / algo / mode -> ContractViolation (5)
     assert L.starmm_plan_create(ctypes.byref(h), 9, 0, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 5
-    assert L.starmm_plan_create(ctypes.byref(h), 0, 7, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 5
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 9, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 5
     # raw mode only for co3 (registry.py:34-35)
     assert L.starmm_plan_create(ctypes.byref(h), 0, 2, 1, 64, 64, 64, 32, 1, -1, 0, 0) == 5
     # base_dim must be a power of two (matrix.py:44-45)
@@ -57,6 +57,11 @@ def test_plan_create_validates_before_touching_a_device():
     # check_problem: non-pow2 n -> InvalidSplit (2); n < b -> InvalidSplit
     assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 48, 48, 48, 16, 1, -1, 0, 0) == 2
     assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 16, 16, 16, 32, 1, -1, 0, 0) == 2
+    # the fast family needs a ring -> NoAdditiveInverse (7)
+    assert L.starmm_plan_create(ctypes.byref(h), 2, 5, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 7
+    assert L.starmm_plan_create(ctypes.byref(h), 4, 8, 0, 64, 64, 64, 32, 1, -1, 0, 0) == 7
+    # raw mode is accepted by strassen only among the fast family
+    assert L.starmm_plan_create(ctypes.byref(h), 0, 6, 1, 64, 64, 64, 32, 1, -1, 0, 0) == 5
     # non-square without ALLOW_NONPOW2 -> DimMismatch (1)
     assert L.starmm_plan_create(ctypes.byref(h), 0, 0, 0, 64, 32, 64, 16, 1, -1, 0, 0) == 1
     # NULL plan pointer
@@ -117,8 +122,6 @@ def test_registry_validation_order_without_gpu():
         with pytest.raises(sm.NoAdditiveInverse):
             t = _cpu(np.zeros((4, 4)), sm.TROPICAL)
             sm.run_algorithm(ex, "strassen", t, t, t, sm.TROPICAL)
-        with pytest.raises(sm.ContractViolation):   # Strassen family is out of scope
-            sm.run_algorithm(ex, "strassen", z, z, z, s)
     with sm.Executor(sm.Config(base_dim=8)) as ex:
         with pytest.raises(sm.InvalidSplit):
             sm.run_algorithm(ex, "co2", z, z, z, s)

@@ -440,3 +440,49 @@ def test_cli_run_verify_bench(tmp_path, capsys):
     rows = out.read_text().strip().split("\n")
     assert rows[0] == "algo,n,b,p,median_ns,speedup_vs_co2_pct,speedup_vs_co3_pct"
     assert len(rows) == 1 + 4
+
+
+# ---- the Strassen family (strassen.py): rings only, C <- A (x) B ------------
+STRASSEN = {"strassen": sm.strassen_parallel, "sar-strassen": sm.sar_strassen,
+            "star-strassen-1": sm.star_strassen_1, "star-strassen-2": sm.star_strassen_2}
+
+
+@pytest.mark.parametrize("algo", list(STRASSEN))
+@pytest.mark.parametrize("sid", ["int", "float"])
+@pytest.mark.parametrize("n,leaf,workers", [(256, 32, 1), (512, 64, 16), (1024, 128, 4)])
+def test_strassen_family_overwrites_with_product(algo, sid, n, leaf, workers):
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(n + len(algo))
+    if sid == "int":
+        A = rng.integers(-2 ** 40, 2 ** 40, (n, n), dtype=np.int64)   # products wrap mod 2^64
+        B = rng.integers(-2 ** 40, 2 ** 40, (n, n), dtype=np.int64)
+    else:
+        A, B = rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    want = O.naive_mm(SR_OF[sid], A, B)
+    C = sm.Matrix(np.full((n, n), 7, dtype=s.dtype), s)          # overwritten, not folded
+    cfg = sm.Config(base_dim=16, workers=workers, strassen_leaf=leaf)
+    STRASSEN[algo](C, sm.Matrix(A, s), sm.Matrix(B, s), s, cfg)
+    if sid == "int":
+        assert np.array_equal(C.numpy(), want)
+    else:
+        assert sm.matrices_equal(C.numpy(), want, tol=1e-9 * n)
+
+
+def test_strassen_space_straightforward_vs_sar():
+    """straightforward keeps up to 17 half-size blocks live per level; sar three."""
+    n, leaf = 512, 128
+    s = sm.INT_RING
+    A = sm.Matrix(np.ones((n, n), np.int64), s)
+    hw = {}
+    for algo in ("strassen", "sar-strassen"):
+        with sm.Executor(sm.Config(base_dim=16, strassen_leaf=leaf)) as ex:
+            C = sm.Matrix(np.zeros((n, n), np.int64), s)
+            sm.run_algorithm(ex, algo, C, A, A, s)
+            assert np.all(C.numpy() == n)
+            hw[algo] = ex.last_stats["pool_high_water_bytes"]
+    half = (n // 2) ** 2 * 8
+    assert hw["sar-strassen"] < hw["strassen"]
+    assert hw["strassen"] <= 17 * half + 17 * (n // 4) ** 2 * 8
+    with pytest.raises(sm.NoAdditiveInverse):
+        T = sm.Matrix(np.zeros((8, 8)), sm.TROPICAL)
+        sm.sar_strassen(T, T, T, sm.TROPICAL, sm.Config(base_dim=2))
