@@ -1,5 +1,5 @@
 // aux_kernels.cuh -- HBM-bound helpers around the tile products:
-//   range_*      range guards for the exact narrow fast paths (one pass, O(n^2))
+//   RangeAcc     range guard of the exact narrow paths, fused into the packers
 //   pack_*       panel packing into the k-group-major layout of simt_kernel.cuh
 //   pad_copy     zero-padded copy for the DMMA path when n is not tile aligned
 //   fill         C <- identity (INIT_IDENTITY with split-k protocols)
@@ -10,69 +10,6 @@
 #include "common.cuh"
 
 namespace starmm {
-
-// ---- range guard -----------------------------------------------------------
-// out[0] = max |x| over the operand (finite entries only for tropical_i32),
-// as an unsigned 64-bit magnitude; reduced with atomicMax.
-template <class T>
-__global__ void range_absmax_kernel(const T* X, long long rows, long long cols, long long ld,
-                                    unsigned long long* out, int skip_i32_inf) {
-    unsigned long long m = 0;
-    long long total = rows * cols;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cols, c = idx - r * cols;
-        T v = X[r * ld + c];
-        if (skip_i32_inf && (long long)v == 0x7fffffffLL) continue;
-        long long sv = (long long)v;
-        unsigned long long a = sv < 0 ? (unsigned long long)(-(sv + 1)) + 1ull : (unsigned long long)sv;
-        m = a > m ? a : m;
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
-        m = v > m ? v : m;
-    }
-    if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
-}
-
-// Range + integrality guard for the 16-bit (min,+) path: out[0] = max |x| over
-// finite entries (rounded up), out[1] = 1 if any entry is non-integral, NaN,
-// -inf, or (for int32) would not be exact.  +inf / INT32_MAX are skipped.
-template <class T>
-__global__ void range_minplus_kernel(const T* X, long long rows, long long cols, long long ld,
-                                     unsigned long long* out) {
-    unsigned long long m = 0;
-    unsigned bad = 0;
-    long long total = rows * cols;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cols, c = idx - r * cols;
-        T v = X[r * ld + c];
-        if constexpr (sizeof(T) == 4 && ((T)0.5 != 0)) {          // float
-            float f = (float)v;
-            if (f == __int_as_float(0x7f800000)) continue;
-            if (!(f == rintf(f)) || fabsf(f) > 1e9f) { bad = 1; continue; }
-            unsigned long long a = (unsigned long long)fabsf(f);
-            m = a > m ? a : m;
-        } else {                                                    // int32
-            if ((long long)v == 0x7fffffffLL) continue;
-            long long sv = (long long)v;
-            unsigned long long a = (unsigned long long)(sv < 0 ? -sv : sv);
-            m = a > m ? a : m;
-        }
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long v = __shfl_xor_sync(0xffffffffu, m, o);
-        m = v > m ? v : m;
-        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
-    }
-    if ((threadIdx.x & 31) == 0) {
-        if (m) atomicMax(&out[0], m);
-        if (bad) atomicOr(&out[1], 1ull);
-    }
-}
 
 // Running range guard fused into the packers (one read of A and B instead of two):
 // out[0] = max |x| over the real (non-padding) elements read, +inf / INT32_MAX

@@ -44,6 +44,7 @@ struct PolF32Pair {        // packed element float, G = 2, accumulator float
     using Tp = float; using Acc = float;
     static constexpr int G = 2;
     static constexpr int KSTEP = 2, OUTS = 1, BK = 16;
+    static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     // a = (A[i][k], A[i][k+1]), b = (B[k][j], B[k+1][j])
     static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
@@ -55,6 +56,7 @@ struct PolF32Single {      // fp32 (min,+) one k at a time: FADD + FMNMX (ptxas 
     using Tp = float; using Acc = float;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fminf(c, a + b); }
 };
@@ -62,6 +64,7 @@ struct PolF32PairMin2 {    // FADD2 + two 2-input FMNMX
     using Tp = float; using Acc = float;
     static constexpr int G = 2;
     static constexpr int KSTEP = 2, OUTS = 1, BK = 16;
+    static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return __int_as_float(0x7f800000); }
     static STARMM_DEV void term2(Acc& c, float2 a, float2 b) {
         float2 v = __fadd2_rn(a, b);
@@ -73,6 +76,7 @@ struct PolF64Min {
     using Tp = double; using Acc = double;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return __longlong_as_double(0x7ff0000000000000ULL); }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fmin(c, a + b); }
 };
@@ -80,6 +84,7 @@ struct PolI32Vmin {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0x7fffffff; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s32(a, b, c); }
 };
@@ -87,6 +92,7 @@ struct PolI32Sat {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0x7fffffff; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
         long long s = (long long)a + (long long)b;
@@ -99,6 +105,7 @@ struct PolI64 {
     using Tp = long long; using Acc = unsigned long long;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0ull; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
         c += (unsigned long long)a * (unsigned long long)b;
@@ -108,6 +115,7 @@ struct PolI64Narrow {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
+    static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c += a * b; }
 };
@@ -118,6 +126,7 @@ struct PolI64Narrow {
 struct PolI8Dp4a {
     using Tp = int; using Acc = int;            // Tp packs A[i][4q..4q+3] / B[4q..4q+3][j] as s8x4
     static constexpr int G = 1, KSTEP = 4, OUTS = 1, BK = 64;
+    static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __dp4a(a, b, c); }
 };
@@ -128,6 +137,7 @@ struct PolI8Dp4a {
 struct PolS16x2Min {
     using Tp = unsigned; using Acc = unsigned;
     static constexpr int G = 1, KSTEP = 1, OUTS = 2, BK = 32;
+    static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return 0x7fff7fffu; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s16x2(a, b, c); }
 };

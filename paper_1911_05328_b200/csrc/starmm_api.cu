@@ -141,7 +141,7 @@ struct PathShape {
 template <class Pol>
 PathShape simt_shape() {
     PathShape sh;
-    sh.bm = simt::BM; sh.bn = simt::bn<Pol>(); sh.bk = Pol::BK; sh.per_sm = 1;
+    sh.bm = simt::BM; sh.bn = simt::bn<Pol>(); sh.bk = Pol::BK; sh.per_sm = Pol::OCC;
     // bytes of packed operand per original (k, x) element
     sh.a_bytes_per_km = (long long)Pol::G * sizeof(typename Pol::Tp) * 1000 / Pol::KSTEP;
     sh.b_bytes_per_kn = (long long)Pol::G * sizeof(typename Pol::Tp) * 1000 / (Pol::KSTEP * Pol::OUTS);
@@ -171,7 +171,7 @@ PathShape path_shape(int path) {
 
 template <class Pol, class Sr>
 int launch_simt(const SimtParams& p, int grid, cudaStream_t s) {
-    auto kern = simt_mm_kernel<Pol, Sr>;
+    auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
     constexpr int smem = simt::smem_bytes<Pol>();
     static bool attr_done = false;
     if (!attr_done) {
@@ -258,44 +258,6 @@ int launch_pack(const void* A, long long lda, const void* B, long long ldb, long
 int occupancy_grid(starmm_plan* P, int per_sm, long long tasks) {
     long long g = (long long)P->sms * per_sm;
     return (int)std::max<long long>(1, std::min<long long>(g, tasks));
-}
-
-// (max finite |x|, non-integral flag) of A and B for the 16-bit (min,+) path.
-template <class T>
-int range_minplus_pair(starmm_plan* P, const void* A, long long lda, const void* B, long long ldb,
-                       cudaStream_t s, unsigned long long* mx, bool* bad) {
-    CK(cudaMemsetAsync(P->d_range, 0, 2 * sizeof(unsigned long long), s));
-    range_minplus_kernel<T><<<grid_blocks(P->m * P->k), 256, 0, s>>>((const T*)A, P->m, P->k, lda,
-                                                                    P->d_range);
-    CK(cudaGetLastError());
-    range_minplus_kernel<T><<<grid_blocks(P->k * P->n), 256, 0, s>>>((const T*)B, P->k, P->n, ldb,
-                                                                    P->d_range);
-    CK(cudaGetLastError());
-    unsigned long long h[2];
-    CK(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    *mx = h[0];
-    *bad = h[1] != 0;
-    return STARMM_OK;
-}
-
-// max |x| of A and B via the range kernels; returns host values.
-template <class T>
-int range_pair(starmm_plan* P, const void* A, long long lda, const void* B, long long ldb,
-               int skip_inf, cudaStream_t s, unsigned long long* ma, unsigned long long* mb) {
-    CK(cudaMemsetAsync(P->d_range, 0, 2 * sizeof(unsigned long long), s));
-    range_absmax_kernel<T><<<grid_blocks(P->m * P->k), 256, 0, s>>>((const T*)A, P->m, P->k, lda,
-                                                                   P->d_range, skip_inf);
-    CK(cudaGetLastError());
-    range_absmax_kernel<T><<<grid_blocks(P->k * P->n), 256, 0, s>>>((const T*)B, P->k, P->n, ldb,
-                                                                   P->d_range + 1, skip_inf);
-    CK(cudaGetLastError());
-    unsigned long long h[2];
-    CK(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
-    *ma = h[0];
-    *mb = h[1];
-    return STARMM_OK;
 }
 
 int ensure_bookkeeping(starmm_plan* P) {

@@ -39,12 +39,11 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
-    run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_sync", n, A, B, C, cnt, sms);
-    run<PolI8Dp4a, SrInt64, 1, true>("i64_dp4a_mbar", n, A, B, C, cnt, sms);
-    run<PolS16x2Min, SrTropF32, 1, false>("minplus_s16x2_sync", n, A, B, C, cnt, sms);
-    run<PolS16x2Min, SrTropF32, 1, true>("minplus_s16x2_mbar", n, A, B, C, cnt, sms);
-    run<PolF32Pair, SrTropF32, 1, false>("f32_fadd2_fmnmx3_sync", n, A, B, C, cnt, sms);
-    run<PolF32Pair, SrTropF32, 1, true>("f32_fadd2_fmnmx3_mbar", n, A, B, C, cnt, sms);
-    run<PolI64Narrow, SrInt64, 1, true>("i64narrow_imad_mbar", n, A, B, C, cnt, sms);
+    run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1", n, A, B, C, cnt, sms);
+    run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_occ2", n, A, B, C, cnt, sms);
+    run<PolS16x2Min, SrTropF32, 1, false>("minplus_s16x2_occ1", n, A, B, C, cnt, sms);
+    run<PolS16x2Min, SrTropF32, 2, false>("minplus_s16x2_occ2", n, A, B, C, cnt, sms);
+    run<PolF32Pair, SrTropI32, 1, false>("i32_carrier_occ1", n, A, B, C, cnt, sms);
+    run<PolF32Pair, SrTropI32, 2, false>("i32_carrier_occ2", n, A, B, C, cnt, sms);
     return 0;
 }
