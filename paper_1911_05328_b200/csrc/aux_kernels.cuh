@@ -88,25 +88,32 @@ struct ConvS16Dup {
     template <class T> static STARMM_DEV unsigned cvt(T x) { unsigned e = s16_enc<T>(x); return e | (e << 16); }
 };
 
-// int64 ring -> s8x4 words along k: A (rows x kdim) -> P[kp/4][rowsp]
+// int64 ring -> s8x4 words along k: A (rows x kdim) -> P[kp/4][rowsp].  A 32-row x
+// 128-k tile goes through shared memory so that both the int64 reads (32 B per
+// thread, consecutive along a row) and the packed int32 writes are coalesced.
 __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long kdim, long long lda,
                                    int* P, long long rowsp, long long kp, unsigned long long* range) {
+    __shared__ int tile[32][33];
     RangeAcc acc;
-    long long total = (kp / 4) * rowsp;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long kw = idx / rowsp, r = idx - kw * rowsp;
+    const long long r0 = (long long)blockIdx.y * 32, w0 = (long long)blockIdx.x * 32;   // words
+    const int tx = threadIdx.x, ty = threadIdx.y;                                       // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        const long long r = r0 + i, k = (w0 + tx) * 4;
         unsigned w = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            long long k = kw * 4 + i;
-            long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
+        for (int q = 0; q < 4; ++q) {
+            long long v = (r < rows && k + q < kdim) ? A[r * lda + k + q] : 0;
             acc.add(v);
-            w |= ((unsigned)(v & 0xff)) << (8 * i);
+            w |= ((unsigned)(v & 0xff)) << (8 * q);
         }
-        P[idx] = (int)w;
+        tile[i][tx] = (int)w;
     }
     if (range) acc.flush(range);
+    __syncthreads();
+    for (int i = ty; i < 32; i += 8) {
+        const long long kw = w0 + i, r = r0 + tx;
+        if (kw < kp / 4 && r < rowsp) P[kw * rowsp + r] = tile[tx][i];
+    }
 }
 // B (kdim x cols) -> P[kp/4][colsp]
 __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
@@ -180,7 +187,9 @@ __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long
 // B (kdim x cols, ld) -> P[kp/G][colsp][G]
 template <class Tin, class Tp, int G, class Conv>
 __global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long long ldb,
-                              Tp* P, long long colsp, long long kp, Tp pad) {
+                              Tp* P, long long colsp, long long kp, Tp pad,
+                              unsigned long long* range = nullptr) {
+    RangeAcc acc;
     long long total = (kp / G) * colsp;
     for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (long long)gridDim.x * blockDim.x) {
@@ -188,9 +197,16 @@ __global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long
 #pragma unroll
         for (int g = 0; g < G; ++g) {
             long long k = kg * G + g;
-            P[idx * G + g] = (k < kdim && c < cols) ? (Tp)Conv::cvt(B[k * ldb + c]) : pad;
+            Tp v = pad;
+            if (k < kdim && c < cols) {
+                Tin x = B[k * ldb + c];
+                acc.add(x);
+                v = (Tp)Conv::cvt(x);
+            }
+            P[idx * G + g] = v;
         }
     }
+    if (range) acc.flush(range);
 }
 
 // Zero-padded copy (DMMA path): dst[rp x cp] from src[rows x cols, ld].

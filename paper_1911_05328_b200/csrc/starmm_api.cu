@@ -114,6 +114,7 @@ struct starmm_plan {
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
+    int last_guarded_path = 0;                  // optimistic first guess for the next execute
     long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
     long long str_issued = 0;                   // Strassen temporaries currently issued
     // peer destinations of the fused k-split combine (starmm_plan_set_peers)
@@ -244,13 +245,13 @@ int fill_dispatch(int sr, void* C, long long rows, long long cols, long long ld,
 template <class Tin, class Tp, int G, class Conv>
 int launch_pack(const void* A, long long lda, const void* B, long long ldb, long long m,
                 long long n, long long k, void* Ap, void* Bp, long long Mp, long long Np,
-                long long Kp, Tp pad, cudaStream_t s) {
+                long long Kp, Tp pad, cudaStream_t s, unsigned long long* range = nullptr) {
     dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
     pack_a_kernel<Tin, Tp, G, Conv><<<ga, dim3(32, 8), 0, s>>>((const Tin*)A, m, k, lda, (Tp*)Ap, Mp,
-                                                              Kp, pad);
+                                                              Kp, pad, range);
     CK(cudaGetLastError());
     pack_b_kernel<Tin, Tp, G, Conv><<<grid_blocks((Kp / G) * Np), 256, 0, s>>>(
-        (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad);
+        (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad, range);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -409,6 +410,9 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_INT64) { path = fast_ok ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64; guard_pending = fast_ok; }
     else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
+    // the previous execute's guard outcome is the better first guess (data ranges are
+    // usually stable across calls); the guard itself still runs on every call
+    if (guard_pending && P->last_guarded_path) path = P->last_guarded_path;
 
     // geometry of the chosen path (re-derived if the guard changes the path)
     bool is_dmma = false;
@@ -497,29 +501,29 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             switch (path) {
             case PATH_SIMT_F32_PAIR:
                 rc = launch_pack<float, float, 2, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                 Mp, Np, Kp, finf, s); break;
+                                                                 Mp, Np, Kp, finf, s, rng); break;
             case PATH_SIMT_I32_CARRIER:
                 rc = launch_pack<int, float, 2, ConvI32ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                               Mp, Np, Kp, finf, s); break;
+                                                               Mp, Np, Kp, finf, s, rng); break;
             case PATH_SIMT_I32_VMIN:
                 rc = launch_pack<int, int, 1, ConvI32Vmin>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
-                                                            Np, Kp, (1 << 30) - 1, s); break;
+                                                            Np, Kp, (1 << 30) - 1, s, rng); break;
             case PATH_SIMT_I32_SAT:
                 rc = launch_pack<int, int, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
-                                                             Np, Kp, 0x7fffffff, s); break;
+                                                             Np, Kp, 0x7fffffff, s, rng); break;
             case PATH_SIMT_I64:
                 rc = launch_pack<long long, long long, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k,
-                                                                         pa, pb, Mp, Np, Kp, 0LL, s); break;
+                                                                         pa, pb, Mp, Np, Kp, 0LL, s, rng); break;
             case PATH_SIMT_I64_NARROW:
                 rc = launch_pack<long long, int, 1, ConvI64ToI32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                   Mp, Np, Kp, 0, s); break;
+                                                                   Mp, Np, Kp, 0, s, rng); break;
             case PATH_SIMT_F64_MIN: {
                 const double dinf = std::numeric_limits<double>::infinity();
                 rc = launch_pack<double, double, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa,
-                                                                   pb, Mp, Np, Kp, dinf, s); break;
+                                                                   pb, Mp, Np, Kp, dinf, s, rng); break;
             }
             case PATH_SIMT_I64_DP4A:
-                pack_a_s8x4_kernel<<<grid_blocks((Kp / 4) * Mp), 256, 0, s>>>(
+                pack_a_s8x4_kernel<<<dim3((unsigned)((Kp / 4 + 31) / 32), (unsigned)(Mp / 32)), dim3(32, 8), 0, s>>>(
                     (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
                 pack_b_s8x4_kernel<<<grid_blocks((Kp / 4) * Np), 256, 0, s>>>(
                     (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
@@ -527,7 +531,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                 break;
             case PATH_SIMT_F64T_CARRIER:
                 rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                  Mp, Np, Kp, finf, s); break;
+                                                                  Mp, Np, Kp, finf, s, rng); break;
             case PATH_SIMT_F32_S16X2:
             case PATH_SIMT_I32_S16X2:
             case PATH_SIMT_F64T_S16X2: {
@@ -587,6 +591,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             else if (mx < (1ull << 28)) actual = PATH_SIMT_I32_VMIN;                     // no overflow
             else actual = PATH_SIMT_I32_SAT;
         }
+        P->last_guarded_path = actual;
         if (actual == path) break;
         path = actual;                  // re-pack for the path the range allows
       }

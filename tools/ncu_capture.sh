@@ -2,17 +2,21 @@
 # ncu evidence for the bench workloads (run under gpurun; one GPU).
 # Each profiled command first runs plain and must exit 0 (B200_PROFILING.md).
 # usage: bash tools/ncu_capture.sh <tag> [configs...]
+#   launch list : the bench command itself (e2e + cpu baseline legs included)
+#   full capture: the tile kernel, from the same command without the e2e / cpu legs
 set -x
 TAG=${1:-r01}; shift
 CFGS=${@:-4 3 5 2}
-B="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline"
 for c in $CFGS; do
   X=""; [ "$c" = "5" ] && X="--n 16384"
   K=simt_mm; [ "$c" = "4" ] && K=dmma
-  $B --config $c $X > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
+  B="python bench.py --steps 2 --warmup 1 --config $c $X"
+  $B > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
-      --log-file gpurun_out/${TAG}_launches_c$c.csv $B --config $c $X > /dev/null 2>&1 || exit 2
+      --log-file gpurun_out/${TAG}_launches_c$c.csv $B > /dev/null 2>&1 || exit 2
+  B2="$B --no-e2e --no-cpu-baseline"
+  $B2 > /dev/null 2>&1 || exit 3
   ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
-      -o gpurun_out/${TAG}_prof_c$c $B --config $c $X > gpurun_out/${TAG}_ncu_c$c.log 2>&1 || exit 3
+      -o gpurun_out/${TAG}_prof_c$c $B2 > gpurun_out/${TAG}_ncu_c$c.log 2>&1 || exit 4
 done
 echo done
