@@ -486,3 +486,61 @@ def test_strassen_space_straightforward_vs_sar():
     with pytest.raises(sm.NoAdditiveInverse):
         T = sm.Matrix(np.zeros((8, 8)), sm.TROPICAL)
         sm.sar_strassen(T, T, T, sm.TROPICAL, sm.Config(base_dim=2))
+
+
+def _fused_two_process_worker(rank, world, port, sid, n, q):
+    import os
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        import torch
+        import paper_1911_05328_b200 as sm
+        from oracle import oracle as O
+        from paper_1911_05328_b200.distributed import DistributedMM, choose_grid, ks_groups
+        torch.cuda.set_device(0)
+        s = sm.get_semiring(sid)
+        rng = np.random.default_rng(3)
+        A = rng.integers(-40, 40, (n, n)).astype(s.dtype)
+        B = rng.integers(-40, 40, (n, n)).astype(s.dtype)
+        C0 = rng.integers(-40, 40, (n, n)).astype(s.dtype)
+        grid = choose_grid(world, ks=2)                    # 1 x 1 x 2: pure k-split
+        dmm = DistributedMM(n, s, grid, rank, algo="star", base_dim=32, workers=148,
+                            group_ks=ks_groups(grid), device=0, combine="fused")
+        assert dmm.combine_mode == "fused"
+        Cb = torch.from_numpy(np.ascontiguousarray(dmm.c_block(C0))).cuda()
+        Ap = torch.from_numpy(np.ascontiguousarray(dmm.a_panel(A))).cuda()
+        Bp = torch.from_numpy(np.ascontiguousarray(dmm.b_panel(B))).cuda()
+        out = dmm.step(Cb, Ap, Bp).cpu().numpy()
+        want = C0.copy()
+        O.gemm_fold(O.SR_BY_NAME[sid], want, A, B)
+        lo, hi = dmm.owned_rows()
+        q.put((rank, bool(np.array_equal(out, want[lo:hi])), lo, hi))
+        dmm.close()
+    except Exception as e:  # pragma: no cover - reported to the parent
+        q.put((rank, repr(e), -1, -1))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("sid", ["int", "tropical_i32", "tropical_f32"])
+def test_fused_combine_two_processes_cuda_ipc(sid):
+    """The real DistributedMM(combine='fused') path -- owner rows shared through CUDA IPC
+    (torch reduce_tensor / rebuild), tile epilogues folding into the peer's buffer -- run
+    as two processes on ONE GPU.  Host collectives go over gloo; no kernel waits on any
+    other, so sharing the device is safe (B200_PROFILING.md)."""
+    import torch.multiprocessing as mp
+    n, world = 512, 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 31000 + hash(sid) % 1000
+    procs = [ctx.Process(target=_fused_two_process_worker, args=(r, world, port, sid, n, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=60)
+    assert all(r[1] is True for r in res), res
+    assert sorted((r[2], r[3]) for r in res) == [(0, n // 2), (n // 2, n)]
