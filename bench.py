@@ -212,13 +212,15 @@ def main():
     ap.add_argument("--config", type=int, default=4, choices=[2, 3, 4, 5])
     ap.add_argument("--algo", default="star", choices=["co2", "co3", "tar", "sar", "star"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=None, help="override n (smoke runs only)")
+    ap.add_argument("--size", type=int, default=None, help="override n (smoke runs only)")
     ap.add_argument("--ksplit-gpus", type=int, default=None)
     ap.add_argument("--combine", default="fused", choices=["fused", "nccl"],
                     help="k-split combine across GPUs (only when the grid has ks > 1)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo: plumbing check with several ranks on fewer GPUs (timings invalid)")
     args = ap.parse_args()
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -227,10 +229,14 @@ def main():
     if args.impl == "reference":
         return reference_arm(args, world, rank)
 
+    local_rank = local_rank % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local_rank)
     device = torch.device("cuda", local_rank)
     if world > 1:
-        dist.init_process_group("nccl", device_id=device)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group("gloo")
 
     import paper_1911_05328_b200 as sm
     from paper_1911_05328_b200 import _lib
@@ -238,7 +244,7 @@ def main():
 
     cid = args.config
     cfg = CONFIGS[cid]
-    n = args.n or cfg["n"]
+    n = args.size or cfg["n"]
     s = sm.get_semiring(cfg["semiring"])
     ks = args.ksplit_gpus or (2 if (cid == 5 and world >= 8) else 1)
     grid = choose_grid(world, ks)
@@ -415,7 +421,7 @@ def reference_arm(args, world, rank):
     from oracle import oracle as O
     cid = args.config
     cfg = CONFIGS[cid]
-    n = args.n or cfg["n"]
+    n = args.size or cfg["n"]
     rng = np.random.default_rng(cfg["seed"])
     dt = cfg["dtype"]
     # same distributions as bench_configs.make_inputs, generated only as far as needed

@@ -8,7 +8,7 @@ set -x
 TAG=${1:-r01}; shift
 CFGS=${@:-4 3 5 2}
 for c in $CFGS; do
-  X=""; [ "$c" = "5" ] && X="--n 16384"
+  X=""; [ "$c" = "5" ] && X="--size 16384"
   K=simt_mm; [ "$c" = "4" ] && K=dmma
   B="python bench.py --steps 2 --warmup 1 --config $c $X"
   $B > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
