@@ -78,7 +78,13 @@ struct PolF64Min {
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
     static STARMM_DEV Acc init() { return __longlong_as_double(0x7ff0000000000000ULL); }
-    static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = fmin(c, a + b); }
+    // the reference's own rule (semiring.py:56-58): v = a + b; if v < out: out = v --
+    // a NaN candidate never wins, and -0.0 does not replace +0.0 (fmin would, and costs
+    // a DSETP+FSEL+SEL sequence on sm_100a: there is no DMNMX)
+    static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
+        const double v = a + b;
+        c = v < c ? v : c;
+    }
 };
 struct PolI32Vmin {
     using Tp = int; using Acc = int;

@@ -544,3 +544,77 @@ def test_fused_combine_two_processes_cuda_ipc(sid):
         p.join(timeout=60)
     assert all(r[1] is True for r in res), res
     assert sorted((r[2], r[3]) for r in res) == [(0, n // 2), (n // 2, n)]
+
+
+# ---- raw C-ABI edge cases ------------------------------------------------------
+@pytest.mark.parametrize("sid", ["int", "float", "tropical", "tropical_f32", "tropical_i32"])
+def test_abi_strided_leading_dimensions(sid):
+    """C, A, B as column windows of wider buffers (ld > cols) through starmm_execute."""
+    from paper_1911_05328_b200 import _lib
+    s = sm.get_semiring(sid)
+    n, pad = 200, 37
+    rng = np.random.default_rng(8)
+    big = lambda: rng.integers(0, 60, (n, n + pad)).astype(s.dtype)   # noqa: E731
+    Ab, Bb, Cb = big(), big(), big()
+    A, B, C0 = Ab[:, 5:5 + n], Bb[:, 11:11 + n], Cb[:, 3:3 + n]
+    want = np.ascontiguousarray(C0).copy()
+    O.gemm_fold(SR_OF[sid], want, np.ascontiguousarray(A), np.ascontiguousarray(B))
+    Ad, Bd, Cd = (torch.from_numpy(x).cuda() for x in (Ab, Bb, Cb))
+    es = Ad.element_size()
+    plan = _lib.Plan(s.sr_id, "star", "pooled", n, n, n, 8, 16, -1, 0, _lib.F_ALLOW_NONPOW2)
+    plan.execute(Cd.data_ptr() + 3 * es, n + pad, Ad.data_ptr() + 5 * es, n + pad,
+                 Bd.data_ptr() + 11 * es, n + pad, torch.cuda.current_stream().cuda_stream)
+    plan.close()
+    got = Cd.cpu().numpy()
+    assert_match(sid, got[:, 3:3 + n], want)
+    assert np.array_equal(got[:, :3], Cb[:, :3]) and np.array_equal(got[:, 3 + n:], Cb[:, 3 + n:])
+
+
+def test_abi_error_paths():
+    from paper_1911_05328_b200 import _lib
+    s = sm.FLOAT_RING
+    plan = _lib.Plan(s.sr_id, "co2", "pooled", 64, 64, 64, 8, 1, -1, 0, 0)
+    t = torch.zeros(64 * 64 + 1, dtype=torch.float64, device="cuda")
+    stream = torch.cuda.current_stream().cuda_stream
+    with pytest.raises(sm.AlignmentError):        # 4-byte offset into a float64 buffer
+        plan.execute(t.data_ptr() + 4, 64, t.data_ptr(), 64, t.data_ptr(), 64, stream)
+    with pytest.raises(sm.DimMismatch):           # ld < cols
+        plan.execute(t.data_ptr(), 32, t.data_ptr(), 64, t.data_ptr(), 64, stream)
+    with pytest.raises(sm.ContractViolation):     # NULL operand
+        plan.execute(0, 64, t.data_ptr(), 64, t.data_ptr(), 64, stream)
+    plan.close()
+
+
+def test_int64_extreme_values_wrap():
+    n = 128
+    lo, hi = np.iinfo(np.int64).min, np.iinfo(np.int64).max
+    rng = np.random.default_rng(2)
+    A = rng.choice(np.array([lo, hi, -1, 1, 0, 2 ** 62], dtype=np.int64), (n, n))
+    B = rng.choice(np.array([lo, hi, -1, 3, 2 ** 33], dtype=np.int64), (n, n))
+    C0 = rng.choice(np.array([lo, hi, 0], dtype=np.int64), (n, n))
+    want = C0.copy()
+    O.gemm_fold(O.SR_INT64, want, A, B)
+    for algo in ("co2", "tar", "star"):
+        got = run(algo, sm.INT_RING, C0, A, B, sm.Config(base_dim=16, workers=16, ksplit=1))
+        assert np.array_equal(got, want), algo
+
+
+@pytest.mark.parametrize("sid", ["tropical", "tropical_f32"])
+def test_tropical_nan_and_neg_inf_operands(sid):
+    """NaN candidates are ignored by the reference product ("if v < out"), -inf wins, and
+    +inf + -inf (NaN) is ignored too (semiring.py:48-60)."""
+    s = sm.get_semiring(sid)
+    n = 96
+    rng = np.random.default_rng(5)
+    A = rng.integers(0, 50, (n, n)).astype(s.dtype)
+    B = rng.integers(0, 50, (n, n)).astype(s.dtype)
+    A[rng.random(A.shape) < 0.05] = np.nan
+    B[rng.random(B.shape) < 0.05] = np.inf
+    A[rng.random(A.shape) < 0.02] = -np.inf
+    A[0, :] = np.nan                       # a row of only NaN candidates -> stays +inf/C0
+    C0 = rng.integers(0, 90, (n, n)).astype(s.dtype)
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B)
+    for fast in (True, False):
+        got = run("co2", s, C0, A, B, sm.Config(base_dim=8, allow_nonpow2=True, fastpath=fast))
+        assert np.array_equal(got, want, equal_nan=True)
