@@ -73,7 +73,8 @@ def peaks(sm_max_mhz: float):
     return {"fp64_tensor": max(dmma, cublas), "fp64_dmma_ubench": dmma, "cublas_dgemm": cublas,
             "issue": issue, "viaddmnmx_ubench": vmin,
             "idp4a_ubench": 2 * _packed("dp4a", 7.4066e13),
-            "viaddmnmx_s16x2_ubench": 2 * _packed("viaddmnmx_s16x2", 3.6974e13)}
+            "viaddmnmx_s16x2_ubench": 2 * _packed("viaddmnmx_s16x2", 3.6974e13),
+            "int8_tensor_nominal": 4.5e15}
 
 
 # path -> (roofline key, instruction mix) for the dominant kernel
@@ -82,6 +83,7 @@ PATH_PEAK = {
     "simt_i64_dp4a": ("idp4a_ubench", "IDP.4A: 4 int8 terms per lane-op"),
     "simt_f32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
     "simt_i32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
+    "tcgen05_i8_umma": ("int8_tensor_nominal", "tcgen05.mma kind::i8 (UTCIMMA), s32 in TMEM"),
 }
 
 
@@ -219,6 +221,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--int-tensor", action="store_true",
+                    help="opt-in: small-range int64 on tcgen05 kind::i8 (config 2; DESIGN.md §5c)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: plumbing check with several ranks on fewer GPUs (timings invalid)")
     args = ap.parse_args()
@@ -252,7 +256,7 @@ def main():
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
                         group_ks=group_ks, device=local_rank, time_kernel=True,
-                        combine=args.combine)
+                        combine=args.combine, int_tensor=args.int_tensor)
 
     A = gen_panel(cid, "A", dmm.m, dmm.k, dmm.r0, dmm.k0, device)
     B = A if (cid in (3, 5) and dmm.r0 == dmm.k0 and dmm.m == dmm.k and dmm.c0 == dmm.k0
@@ -303,7 +307,11 @@ def main():
     achieved = local_ops / kern_s
     key, mix = PATH_PEAK.get(st["path_name"], ("issue", "1 lane-op per term (FADD2+FMNMX3 / "
                                                  "VIADDMNMX / IMAD), 64 terms/clk/SM"))
-    if key == "fp64_tensor":
+    if key == "int8_tensor_nominal":
+        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
+                "unit": "Tops/s", "peak_source": "NOMINAL dense int8 4.5 POPS (B200 datasheet; "
+                "not measured on this pool)"}
+    elif key == "fp64_tensor":
         roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
                 "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
                 "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json "
@@ -372,7 +380,7 @@ def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
     Ch0 = C.cpu().pin_memory()
     Ch = Ch0.clone().pin_memory()
     cfg = sm.Config(base_dim=CONFIGS[cid]["b"], workers=torch.cuda.get_device_properties(device)
-                    .multi_processor_count, allow_nonpow2=True)
+                    .multi_processor_count, allow_nonpow2=True, int_tensor_cores=args.int_tensor)
     ex = sm.Executor(cfg) if world == 1 else None
     out = None
     if world > 1:

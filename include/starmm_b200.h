@@ -92,6 +92,7 @@ enum starmm_alloc { STARMM_POOLED = 0, STARMM_RAW = 1 };
 #define STARMM_F_INIT_IDENTITY  0x4  /* ignore incoming C: C <- A (x) B (k-split partials) */
 #define STARMM_F_ALLOW_NONPOW2  0x8  /* accept any n >= 1 (divergence from matrix.py:57-61) */
 #define STARMM_F_TIME_MAIN      0x10 /* CUDA-event time the tile kernel (stats.main_kernel_ns) */
+#define STARMM_F_INT_TENSOR     0x20 /* opt-in: exact small-range int64 on tcgen05 kind::i8 */
 
 typedef struct starmm_plan starmm_plan;
 

@@ -25,6 +25,7 @@
 #include "dmma_kernel.cuh"
 #include "simt_kernel.cuh"
 #include "aux_kernels.cuh"
+#include "tc_i8_kernel.cuh"
 
 using namespace starmm;
 
@@ -130,7 +131,7 @@ enum PathId : int {
     PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
     PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
     PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11,
-    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13
+    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13, PATH_TC_I8 = 14
 };
 
 // Tile / packing geometry of one kernel path (mirrors the device-side constants).
@@ -166,6 +167,10 @@ PathShape path_shape(int path) {
     case PATH_SIMT_I32_S16X2: return simt_shape<PolS16x2Min>();
     case PATH_SIMT_F64T_S16X2: return simt_shape<PolS16x2Min>();
     case PATH_SIMT_F64T_CARRIER: return simt_shape<PolF32Pair>();
+    case PATH_TC_I8: {
+        PathShape sh{tci8::BM, tci8::BN, tci8::BK, 1, 1000, 1000};
+        return sh;
+    }
     }
     return simt_shape<PolI64>();
 }
@@ -252,6 +257,50 @@ int launch_pack(const void* A, long long lda, const void* B, long long ldb, long
     CK(cudaGetLastError());
     pack_b_kernel<Tin, Tp, G, Conv><<<grid_blocks((Kp / G) * Np), 256, 0, s>>>(
         (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad, range);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda needed)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int box_rows) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q));
+        if (!fn || q != cudaDriverEntryPointSuccess) return STARMM_INTERNAL_ERROR;
+    }
+    cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)kp};
+    cuuint32_t box[2] = {(cuuint32_t)tci8::BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? STARMM_OK : STARMM_INTERNAL_ERROR;
+}
+
+int launch_tc_i8(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp,
+                 long long tiles_m, long long tiles_n, int sms, int init_identity, void* C, long long ldc,
+                 long long M, long long N, cudaStream_t s) {
+    CUtensorMap ta, tb;
+    TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp, Kp, tci8::BM));
+    TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np, Kp, tci8::BN));
+    static bool attr_done = false;
+    if (!attr_done) {
+        CK(cudaFuncSetAttribute(tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                tci8::SMEM_BYTES));
+        attr_done = true;
+    }
+    TcI8Params p;
+    p.tiles_m = tiles_m; p.tiles_n = tiles_n; p.num_tiles = tiles_m * tiles_n;
+    p.nk = (int)(Kp / tci8::BK); p.init_identity = init_identity;
+    p.C = (long long*)C; p.ldc = ldc; p.M = M; p.N = N;
+    int grid = (int)std::min<long long>(p.num_tiles, sms);
+    tc_i8_kernel<<<grid, tci8::THREADS, tci8::SMEM_BYTES, s>>>(ta, tb, p);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -408,7 +457,10 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
     else if (P->sr == STARMM_SR_TROPICAL_F64) { path = fast_ok ? PATH_SIMT_F64T_S16X2 : PATH_SIMT_F64_MIN; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
-    else if (P->sr == STARMM_SR_INT64) { path = fast_ok ? PATH_SIMT_I64_DP4A : PATH_SIMT_I64; guard_pending = fast_ok; }
+    else if (P->sr == STARMM_SR_INT64) {
+        path = fast_ok ? ((P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A) : PATH_SIMT_I64;
+        guard_pending = fast_ok;
+    }
     else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
     // the previous execute's guard outcome is the better first guess (data ranges are
     // usually stable across calls); the guard itself still runs on every call
@@ -427,8 +479,9 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
         tiles = tiles_m * tiles_n;
         gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
-        if (P->algo == STARMM_CO2) {
+        if (P->algo == STARMM_CO2 || path == PATH_TC_I8) {
             s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
+                                   // (the opt-in tensor path keeps whole-K tiles too)
         } else if (P->ksplit_req >= 0) {
             s_log2 = P->ksplit_req;
         } else {
@@ -529,6 +582,13 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
+            case PATH_TC_I8:
+                pack_i8_rows_kernel<<<grid_blocks(Mp * Kp), 256, 0, s>>>(
+                    (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, Kp, rng);
+                pack_i8_transpose_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 32)), dim3(32, 8), 0, s>>>(
+                    (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, Kp, rng);
+                rc = cuda_status(cudaGetLastError());
+                break;
             case PATH_SIMT_F64T_CARRIER:
                 rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
                                                                   Mp, Np, Kp, finf, s, rng); break;
@@ -572,7 +632,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if (P->sr == STARMM_SR_INT64) {
             // exact iff every int32 partial sum fits: K * max|a| * max|b| < 2^31
             long double bound = (long double)P->k * (long double)mx * (long double)mx;
-            if (mx <= 127 && bound < 2147483648.0L) actual = PATH_SIMT_I64_DP4A;
+            if (mx <= 127 && bound < 2147483648.0L)
+                actual = (P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A;
             else if (mx < (1ull << 31) && bound < 2147483648.0L) actual = PATH_SIMT_I64_NARROW;
             else actual = PATH_SIMT_I64;
         } else if (P->sr == STARMM_SR_TROPICAL_F64) {
@@ -651,7 +712,10 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             }
             if ((rc = cuda_status(cudaEventRecord(P->ev0, s)))) break;
         }
-        if (is_dmma) {
+        if (path == PATH_TC_I8) {
+            rc = launch_tc_i8(opA, opB, Mp, Np, Kp, tiles_m, tiles_n, P->sms, init_identity ? 1 : 0, C, ldc,
+                              P->m, P->n, s);
+        } else if (is_dmma) {
             DmmaParams dp;
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
             dp.g = g; dp.w = w;

@@ -91,6 +91,8 @@ class Executor:
             flags |= _lib.F_NO_FASTPATH
         if cfg.allow_nonpow2:
             flags |= _lib.F_ALLOW_NONPOW2
+        if cfg.int_tensor_cores:
+            flags |= _lib.F_INT_TENSOR
         key = (s.sr_id, algo, mode, m, n, k, flags, ks)
         p = self._plans.get(key)
         if p is None:

@@ -618,3 +618,37 @@ def test_tropical_nan_and_neg_inf_operands(sid):
     for fast in (True, False):
         got = run("co2", s, C0, A, B, sm.Config(base_dim=8, allow_nonpow2=True, fastpath=fast))
         assert np.array_equal(got, want, equal_nan=True)
+
+
+# ---- opt-in tcgen05 kind::i8 path (exact small-range int64) -----------------------
+@pytest.mark.parametrize("n", [128, 300, 1024, 2048])
+@pytest.mark.parametrize("algo", ["co2", "star", "tar"])
+def test_tcgen05_int8_path_bitexact(n, algo):
+    rng = np.random.default_rng(n)
+    A = rng.integers(-127, 128, (n, n), dtype=np.int64)
+    B = rng.integers(-127, 128, (n, n), dtype=np.int64)
+    C0 = rng.integers(-2 ** 62, 2 ** 62, (n, n), dtype=np.int64)
+    want = C0.copy()
+    O.gemm_fold(O.SR_INT64, want, A, B, par=True)
+    cfg = sm.Config(base_dim=16, workers=16, int_tensor_cores=True, allow_nonpow2=True)
+    with sm.Executor(cfg) as ex:
+        C = sm.Matrix(C0, sm.INT_RING)
+        sm.run_algorithm(ex, algo, C, sm.Matrix(A, sm.INT_RING), sm.Matrix(B, sm.INT_RING), sm.INT_RING)
+        assert ex.last_stats["path_name"] == "tcgen05_i8_umma"
+    assert np.array_equal(C.numpy(), want)
+
+
+def test_tcgen05_guard_falls_back_exactly():
+    """Values beyond int8 (or K*max^2 >= 2^31) must leave the tensor path."""
+    n = 256
+    rng = np.random.default_rng(0)
+    A = rng.integers(-127, 128, (n, n), dtype=np.int64)
+    B = rng.integers(-127, 128, (n, n), dtype=np.int64)
+    A[7, 9] = 128                                    # one value out of int8 range
+    want = O.naive_mm(O.SR_INT64, A, B)
+    cfg = sm.Config(base_dim=16, int_tensor_cores=True)
+    with sm.Executor(cfg) as ex:
+        C = sm.Matrix(np.zeros((n, n), np.int64), sm.INT_RING)
+        sm.run_algorithm(ex, "co2", C, sm.Matrix(A, sm.INT_RING), sm.Matrix(B, sm.INT_RING), sm.INT_RING)
+        assert ex.last_stats["path_name"] == "simt_i64_narrow_i32"
+    assert np.array_equal(C.numpy(), want)
