@@ -93,6 +93,8 @@ enum starmm_alloc { STARMM_POOLED = 0, STARMM_RAW = 1 };
 #define STARMM_F_ALLOW_NONPOW2  0x8  /* accept any n >= 1 (divergence from matrix.py:57-61) */
 #define STARMM_F_TIME_MAIN      0x10 /* CUDA-event time the tile kernel (stats.main_kernel_ns) */
 #define STARMM_F_INT_TENSOR     0x20 /* opt-in: exact small-range int64 on tcgen05 kind::i8 */
+#define STARMM_F_FP64_EMU       0x40 /* opt-in: fp64 (+,x) as Ozaki-II CRT over 16 int8 tcgen05 GEMMs
+                                        (DESIGN.md §5d); non-finite inputs and k >= 2^17 stay on DMMA */
 
 typedef struct starmm_plan starmm_plan;
 

@@ -23,12 +23,14 @@ ALGO_IDS = {"co2": 0, "co3": 1, "tar": 2, "sar": 3, "star": 4, "strassen": 5, "s
 ALLOC_IDS = {"pooled": 0, "raw": 1}
 F_ASYNC, F_NO_FASTPATH, F_INIT_IDENTITY, F_ALLOW_NONPOW2, F_TIME_MAIN = 0x1, 0x2, 0x4, 0x8, 0x10
 F_INT_TENSOR = 0x20
+F_FP64_EMU = 0x40
 
 PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f32_fadd2_fmnmx3",
               5: "simt_i32_via_f32_carrier", 6: "simt_i32_viaddmnmx", 7: "simt_i32_saturating",
               8: "simt_f64_min", 9: "simt_i64_dp4a", 10: "simt_f32_s16x2_viaddmnmx",
               11: "simt_i32_s16x2_viaddmnmx", 12: "simt_f64trop_s16x2_viaddmnmx",
-              13: "simt_f64trop_via_f32_carrier", 14: "tcgen05_i8_umma"}
+              13: "simt_f64trop_via_f32_carrier", 14: "tcgen05_i8_umma",
+              15: "ozaki2_fp64_tcgen05_i8x16"}
 
 
 class StarmmStats(ctypes.Structure):

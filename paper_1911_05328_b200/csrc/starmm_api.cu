@@ -25,7 +25,8 @@
 #include "dmma_kernel.cuh"
 #include "simt_kernel.cuh"
 #include "aux_kernels.cuh"
-#include "tc_i8_kernel.cuh"
+#include "tc_gemm.cuh"
+#include "ozaki.cuh"
 
 using namespace starmm;
 
@@ -131,7 +132,7 @@ enum PathId : int {
     PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
     PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
     PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11,
-    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13, PATH_TC_I8 = 14
+    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13, PATH_TC_I8 = 14, PATH_OZAKI_F64 = 15
 };
 
 // Tile / packing geometry of one kernel path (mirrors the device-side constants).
@@ -168,7 +169,11 @@ PathShape path_shape(int path) {
     case PATH_SIMT_F64T_S16X2: return simt_shape<PolS16x2Min>();
     case PATH_SIMT_F64T_CARRIER: return simt_shape<PolF32Pair>();
     case PATH_TC_I8: {
-        PathShape sh{tci8::BM, tci8::BN, tci8::BK, 1, 1000, 1000};
+        PathShape sh{2 * tcg::BM, tcg::BN, tcg::BK, 1, 1000, 1000};
+        return sh;
+    }
+    case PATH_OZAKI_F64: {   // P residue planes of int8 per operand
+        PathShape sh{2 * tcg::BM, tcg::BN, tcg::BK, 1, 1000LL * oz::P, 1000LL * oz::P};
         return sh;
     }
     }
@@ -275,7 +280,7 @@ int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int
     }
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)kp};
-    cuuint32_t box[2] = {(cuuint32_t)tci8::BK, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)tcg::BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -283,26 +288,71 @@ int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int
     return r == CUDA_SUCCESS ? STARMM_OK : STARMM_INTERNAL_ERROR;
 }
 
-int launch_tc_i8(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp,
-                 long long tiles_m, long long tiles_n, int sms, int init_identity, void* C, long long ldc,
-                 long long M, long long N, cudaStream_t s) {
+// The CTA-pair tensor-core GEMM over `passes` stacked int8 operand planes
+// (A: passes x [Mp][Kp], B^T: passes x [Np][Kp]); Mp, Np multiples of 256.
+template <class Epi>
+int launch_tcg(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp, int passes,
+               const Epi& epi, int sms, cudaStream_t s, int* grid_out) {
+    if ((long long)passes * Mp >= (1LL << 31) || (long long)passes * Np >= (1LL << 31)) return STARMM_TOO_LARGE;
     CUtensorMap ta, tb;
-    TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp, Kp, tci8::BM));
-    TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np, Kp, tci8::BN));
+    TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp * passes, Kp, tcg::BM));
+    TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np * passes, Kp, tcg::BNH));
+    auto kern = tcg_kernel<Epi>;
     static bool attr_done = false;
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(tc_i8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                tci8::SMEM_BYTES));
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
         attr_done = true;
     }
-    TcI8Params p;
-    p.tiles_m = tiles_m; p.tiles_n = tiles_n; p.num_tiles = tiles_m * tiles_n;
-    p.nk = (int)(Kp / tci8::BK); p.init_identity = init_identity;
-    p.C = (long long*)C; p.ldc = ldc; p.M = M; p.N = N;
-    int grid = (int)std::min<long long>(p.num_tiles, sms);
-    tc_i8_kernel<<<grid, tci8::THREADS, tci8::SMEM_BYTES, s>>>(ta, tb, p);
+    TcgShape sh;
+    sh.tiles_m = (int)(Mp / 256); sh.tiles_n = (int)(Np / 256); sh.num_tiles = sh.tiles_m * sh.tiles_n;
+    sh.group_m = 8;
+    sh.nk = (int)(Kp / tcg::BK); sh.passes = passes;
+    sh.a_pass_rows = (int)Mp; sh.b_pass_rows = (int)Np;
+    const int grid = 2 * std::max(1, std::min(sms / 2, sh.num_tiles));
+    if (grid_out) *grid_out = grid;
+    kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES, s>>>(ta, tb, sh, epi);
     CK(cudaGetLastError());
     return STARMM_OK;
+}
+
+TcgOut tcg_out(const starmm_plan* P, void* C, long long ldc, bool init_identity) {
+    TcgOut o;
+    o.C = C; o.ldc = ldc; o.M = P->m; o.N = P->n; o.init_identity = init_identity ? 1 : 0;
+    o.remote_parts = P->remote_parts; o.remote_rows = P->remote_rows; o.remote_ld = P->remote_ld;
+    for (int i = 0; i < 8; ++i) o.remote_base[i] = P->remote_base[i];
+    return o;
+}
+
+// CRT constants of the Ozaki-II moduli (exact, host side, 128-bit)
+const OzCrt& ozaki_crt() {
+    static OzCrt c;
+    static bool done = false;
+    if (done) return c;
+    typedef unsigned __int128 u128;
+    u128 M = 1;
+    for (int p = 0; p < oz::P; ++p) M *= (u128)oz::MOD[p];
+    for (int p = 0; p < oz::P; ++p) {
+        const int m = oz::MOD[p];
+        const u128 Mp = M / (u128)m;
+        const int r = (int)(Mp % (u128)m);
+        int inv = 1;
+        while ((r * inv) % m != 1) ++inv;               // m <= 256: brute force is exact
+        const u128 W = (Mp * (u128)inv) % M;
+        for (int l = 0; l < 4; ++l) c.W[p][l] = (uint32_t)(W >> (32 * l));
+    }
+    const u128 H = M / 2;
+    for (int l = 0; l < 4; ++l) { c.Ml[l] = (uint32_t)(M >> (32 * l)); c.Mh[l] = (uint32_t)(H >> (32 * l)); }
+    c.invM = 1.0 / (double)M;
+    done = true;
+    return c;
+}
+
+// bits kept per scaled operand: M > 2 k 2^(2t) with a one-bit margin
+int ozaki_bits(long long k) {
+    double lm = 0;
+    for (int p = 0; p < oz::P; ++p) lm += std::log2((double)oz::MOD[p]);
+    int t = (int)std::floor((lm - std::log2((double)std::max(1LL, k)) - 2.0) / 2.0);
+    return std::min(t, 62);
 }
 
 int occupancy_grid(starmm_plan* P, int per_sm, long long tasks) {
@@ -454,7 +504,16 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     // path the observed range allows.
     int path = 0;
     bool guard_pending = false;
-    if (P->sr == STARMM_SR_FP64) path = PATH_DMMA_F64;
+    if (P->sr == STARMM_SR_FP64) {
+        // opt-in Ozaki-II emulation on the int8 tensor cores; the guard
+        // (finite inputs) runs in the same pass that finds the per-row/column scales
+        if (fast_ok && (P->flags & STARMM_F_FP64_EMU) && P->k < (1LL << 17)) {
+            path = PATH_OZAKI_F64;
+            guard_pending = true;
+        } else {
+            path = PATH_DMMA_F64;
+        }
+    }
     else if (P->sr == STARMM_SR_TROPICAL_F64) { path = fast_ok ? PATH_SIMT_F64T_S16X2 : PATH_SIMT_F64_MIN; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
     else if (P->sr == STARMM_SR_INT64) {
@@ -464,7 +523,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
     // the previous execute's guard outcome is the better first guess (data ranges are
     // usually stable across calls); the guard itself still runs on every call
-    if (guard_pending && P->last_guarded_path) path = P->last_guarded_path;
+    if (guard_pending && P->last_guarded_path && P->sr != STARMM_SR_FP64) path = P->last_guarded_path;
 
     // geometry of the chosen path (re-derived if the guard changes the path)
     bool is_dmma = false;
@@ -479,7 +538,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
         tiles = tiles_m * tiles_n;
         gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
-        if (P->algo == STARMM_CO2 || path == PATH_TC_I8) {
+        if (P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64) {
             s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
                                    // (the opt-in tensor path keeps whole-K tiles too)
         } else if (P->ksplit_req >= 0) {
@@ -523,11 +582,13 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         return STARMM_OK;
     };
     int rc = STARMM_OK;
+    unsigned long long *oz_rowmax = nullptr, *oz_colmax = nullptr;
     const void* opA = A; const void* opB = B;
     long long olda = lda, oldb = ldb;
     do {
       for (;;) {
         if ((rc = plan_geometry())) break;
+        opA = A; opB = B; olda = lda; oldb = ldb;     // a re-plan starts from the caller's operands
         unsigned long long* rng = guard_pending ? P->d_range : nullptr;
         if (rng && (rc = cuda_status(cudaMemsetAsync(rng, 0, 2 * sizeof(unsigned long long), s)))) break;
         if (is_dmma) {
@@ -589,6 +650,19 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
+            case PATH_OZAKI_F64: {
+                // scale pass (and the finiteness guard); residues are packed after it
+                if ((rc = stage_acquire((size_t)Mp * 8, (void**)&oz_rowmax))) break;
+                if ((rc = stage_acquire((size_t)Np * 8, (void**)&oz_colmax))) break;
+                if ((rc = cuda_status(cudaMemsetAsync(oz_colmax, 0, (size_t)Np * 8, s)))) break;
+                const int wpb = 8;
+                oz_amax_rows_kernel<<<(unsigned)std::min<long long>((P->m + wpb - 1) / wpb, 148LL * 16), 32 * wpb, 0, s>>>(
+                    (const double*)A, P->m, P->k, lda, oz_rowmax, rng + 1);
+                oz_amax_cols_kernel<<<dim3((unsigned)((P->n + 31) / 32), (unsigned)((P->k + 255) / 256)), dim3(32, 8), 0, s>>>(
+                    (const double*)B, P->k, P->n, ldb, oz_colmax, rng + 1);
+                rc = cuda_status(cudaGetLastError());
+                break;
+            }
             case PATH_SIMT_F64T_CARRIER:
                 rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
                                                                   Mp, Np, Kp, finf, s, rng); break;
@@ -629,7 +703,9 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         const unsigned long long mx = h[0];
         const bool bad = h[1] != 0;
         int actual = path;
-        if (P->sr == STARMM_SR_INT64) {
+        if (P->sr == STARMM_SR_FP64) {
+            actual = bad ? PATH_DMMA_F64 : PATH_OZAKI_F64;   // NaN / inf: IEEE semantics via DMMA
+        } else if (P->sr == STARMM_SR_INT64) {
             // exact iff every int32 partial sum fits: K * max|a| * max|b| < 2^31
             long double bound = (long double)P->k * (long double)mx * (long double)mx;
             if (mx <= 127 && bound < 2147483648.0L)
@@ -657,6 +733,15 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         path = actual;                  // re-pack for the path the range allows
       }
       if (rc) break;
+        if (path == PATH_OZAKI_F64) {   // residue planes for the scales the guard pass found
+            const int t = ozaki_bits(P->k);
+            oz_pack_rows_kernel<<<grid_blocks(Mp * Kp / 4), 256, 0, s>>>(
+                (const double*)A, P->m, P->k, lda, oz_rowmax, t, (signed char*)opA, Mp, Kp);
+            oz_pack_cols_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 64)), dim3(32, 8), 0, s>>>(
+                (const double*)B, P->k, P->n, ldb, oz_colmax, t, (signed char*)opB, Np, Kp);
+            if ((rc = cuda_status(cudaGetLastError()))) break;
+            launches += 2;
+        }
 
         // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
         const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
@@ -713,8 +798,19 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             if ((rc = cuda_status(cudaEventRecord(P->ev0, s)))) break;
         }
         if (path == PATH_TC_I8) {
-            rc = launch_tc_i8(opA, opB, Mp, Np, Kp, tiles_m, tiles_n, P->sms, init_identity ? 1 : 0, C, ldc,
-                              P->m, P->n, s);
+            EpiFoldI64 e;
+            e.o = tcg_out(P, C, ldc, init_identity);
+            rc = launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s, nullptr);
+        } else if (path == PATH_OZAKI_F64) {
+            EpiOzakiF64 e;
+            e.o = tcg_out(P, C, ldc, init_identity);
+            e.rowmax = oz_rowmax; e.colmax = oz_colmax; e.t = ozaki_bits(P->k);
+            e.crt = ozaki_crt();
+            const long long ctas = 2LL * std::max(1LL, std::min<long long>(P->sms / 2, (Mp / 256) * (Np / 256)));
+            void* scratch = nullptr;
+            if ((rc = stage_acquire((size_t)ctas * 2 * EpiOzakiF64::BUF_BYTES, &scratch))) break;
+            e.scratch = (unsigned char*)scratch;
+            rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, nullptr);
         } else if (is_dmma) {
             DmmaParams dp;
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;

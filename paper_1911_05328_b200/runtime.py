@@ -93,6 +93,8 @@ class Executor:
             flags |= _lib.F_ALLOW_NONPOW2
         if cfg.int_tensor_cores:
             flags |= _lib.F_INT_TENSOR
+        if cfg.fp64_emulation:
+            flags |= _lib.F_FP64_EMU
         key = (s.sr_id, algo, mode, m, n, k, flags, ks)
         p = self._plans.get(key)
         if p is None:

@@ -390,9 +390,10 @@ def test_host_path_aliased_operands_and_public_api():
 
 
 # ---- fused k-split combine (starmm_plan_set_peers), emulated on one GPU -----
-@pytest.mark.parametrize("sid", ["int", "float", "tropical_f32", "tropical_i32"])
+@pytest.mark.parametrize("sid,extra", [("int", 0), ("float", 0), ("tropical_f32", 0), ("tropical_i32", 0),
+                                       ("int", 0x20), ("float", 0x40)])
 @pytest.mark.parametrize("ks", [2, 4])
-def test_fused_ksplit_combine_single_gpu_emulation(sid, ks):
+def test_fused_ksplit_combine_single_gpu_emulation(sid, extra, ks):
     """Exactly the kernel path of DistributedMM(combine="fused"): ks 'virtual ranks',
     each with its own k-slice plan, fold their partial tiles with the atomic-madd into
     the owners' row chunks (here local buffers instead of NVLink-mapped peers).  The
@@ -415,12 +416,14 @@ def test_fused_ksplit_combine_single_gpu_emulation(sid, ks):
     for K in range(ks):
         k0, k1 = block_bounds(n, ks, K)
         plan = _lib.Plan(s.sr_id, "star", "pooled", n, n, k1 - k0, 32, 148, -1, 0,
-                         _lib.F_ALLOW_NONPOW2)
+                         _lib.F_ALLOW_NONPOW2 | extra)
         plan.set_peers([t.data_ptr() for t in owned], n, chunk)
         Ap = Ad[:, k0:k1]
         Bp = Bd[k0:k1]
         plan.execute(scratch.data_ptr(), n, Ap.data_ptr(), Ap.stride(0), Bp.data_ptr(),
                      Bp.stride(0), torch.cuda.current_stream().cuda_stream)
+        if extra:   # the opt-in tensor-core paths fold through the same remote epilogue
+            assert _lib.PATH_NAMES[plan.stats()["path"]] in ("tcgen05_i8_umma", "ozaki2_fp64_tcgen05_i8x16")
         plan.close()
     got = torch.cat(owned, 0).cpu().numpy()
     assert_match(sid, got, want)
