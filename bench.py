@@ -74,7 +74,10 @@ def peaks(sm_max_mhz: float):
             "issue": issue, "viaddmnmx_ubench": vmin,
             "idp4a_ubench": 2 * _packed("dp4a", 7.4066e13),
             "viaddmnmx_s16x2_ubench": 2 * _packed("viaddmnmx_s16x2", 3.6974e13),
-            "int8_tensor_nominal": 4.5e15}
+            # library int8 GEMM on this pool (tools/int8_peak.py -> profiles/r01_int8_peak.json)
+            "int8_tensor_burst": 1e12 * _measured("r01_int8_peak.json", "int_mm_n8192_burst_tops", 3053.9),
+            "int8_tensor_sustained": 1e12 * _measured("r01_int8_peak.json", "int_mm_n16384_sustained_tops",
+                                                      2061.5)}
 
 
 # path -> (roofline key, instruction mix) for the dominant kernel
@@ -83,8 +86,11 @@ PATH_PEAK = {
     "simt_i64_dp4a": ("idp4a_ubench", "IDP.4A: 4 int8 terms per lane-op"),
     "simt_f32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
     "simt_i32_s16x2_viaddmnmx": ("viaddmnmx_s16x2_ubench", "VIADDMNMX.S16x2: 2 terms per lane-op"),
-    "tcgen05_i8_umma": ("int8_tensor_nominal", "tcgen05.mma kind::i8 (UTCIMMA), s32 in TMEM"),
+    "tcgen05_i8_umma": ("int8_tensor", "tcgen05.mma.cta_group::2 kind::i8 (UTCIMMA.2CTA), s32 in TMEM"),
+    "ozaki2_fp64_tcgen05_i8x16": ("int8_tensor", "16 x tcgen05.mma.cta_group::2 kind::i8 residue passes + "
+                                  "exact CRT epilogue (Ozaki scheme II)"),
 }
+INT8_PASSES = {"tcgen05_i8_umma": 1, "ozaki2_fp64_tcgen05_i8x16": 16}
 
 
 # ---- clocks during the timed region ----------------------------------------
@@ -223,6 +229,10 @@ def main():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--int-tensor", action="store_true",
                     help="opt-in: small-range int64 on tcgen05 kind::i8 (config 2; DESIGN.md §5c)")
+    ap.add_argument("--fp64-emu", action="store_true",
+                    help="opt-in: fp64 (+,x) as Ozaki-II over 16 int8 tcgen05 GEMMs (config 4; DESIGN.md §5d)")
+    ap.add_argument("--no-opt-in", action="store_true",
+                    help="skip the secondary measurement of the opt-in tensor-core path")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: plumbing check with several ranks on fewer GPUs (timings invalid)")
     args = ap.parse_args()
@@ -256,7 +266,7 @@ def main():
     sms = torch.cuda.get_device_properties(device).multi_processor_count
     dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
                         group_ks=group_ks, device=local_rank, time_kernel=True,
-                        combine=args.combine, int_tensor=args.int_tensor)
+                        combine=args.combine, int_tensor=args.int_tensor, fp64_emu=args.fp64_emu)
 
     A = gen_panel(cid, "A", dmm.m, dmm.k, dmm.r0, dmm.k0, device)
     B = A if (cid in (3, 5) and dmm.r0 == dmm.k0 and dmm.m == dmm.k and dmm.c0 == dmm.k0
@@ -303,31 +313,14 @@ def main():
     # ---- roofline of the dominant kernel ----
     clocks = clk.summary()
     pk = peaks(clocks["sm_max_mhz"] or 1965.0)
-    local_ops = 2.0 * dmm.m * dmm.nn * dmm.k
-    achieved = local_ops / kern_s
-    key, mix = PATH_PEAK.get(st["path_name"], ("issue", "1 lane-op per term (FADD2+FMNMX3 / "
-                                                 "VIADDMNMX / IMAD), 64 terms/clk/SM"))
-    if key == "int8_tensor_nominal":
-        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
-                "unit": "Tops/s", "peak_source": "NOMINAL dense int8 4.5 POPS (B200 datasheet; "
-                "not measured on this pool)"}
-    elif key == "fp64_tensor":
-        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
-                "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
-                "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json "
-                "has no fp64 entry)"}
-    else:
-        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
-                "unit": "Tops/s", "peak_source": ("measured instruction-mix peak, "
-                "profiles/r01_packed_ops_microbench.jsonl / r01_peaks_microbench.json"
-                if key != "issue" else "BASELINE issue roofline: 148 SMs x 128 lanes x sm_max_mhz")}
-        roof["baseline_issue_roofline"] = pk["issue"] / 1e12
-        roof["frac_of_baseline_issue_roofline"] = achieved / pk["issue"]
-    roof["instruction_mix"] = mix
-    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof, mix = roofline(pk, st["path_name"], 2.0 * dmm.m * dmm.nn * dmm.k, kern_s)
     roof["traffic"] = _ncu_traffic(cid, st["path_name"])
-    roof["kernel_ms"] = kern_s * 1e3
     roof["kernel_share_of_step"] = kern_s / t_step
+
+    # ---- the opt-in tensor-core path of this config, measured as a secondary line ----
+    opt_in = None
+    if world == 1 and not args.no_opt_in and not (args.fp64_emu or args.int_tensor) and cid in (2, 4):
+        opt_in = opt_in_run(args, s, cid, n, grid, rank, sms, local_rank, A, B, C, pk)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
@@ -351,6 +344,7 @@ def main():
                        "combine": dmm.combine_mode if grid.ks > 1 else "none",
                        "ksplit_per_tile": st["ksplit"], "l2": "inputs larger than L2 (no flush)"},
             "roofline": roof,
+            "opt_in_tensor_path": opt_in,
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": int(st["kernel_launches"]) * args.steps,
@@ -360,6 +354,72 @@ def main():
     dmm.close()
     if world > 1:
         dist.destroy_process_group()
+
+
+def roofline(pk, path, local_ops, kern_s):
+    achieved = local_ops / kern_s
+    key, mix = PATH_PEAK.get(path, ("issue", "1 lane-op per term (FADD2+FMNMX3 / "
+                                          "VIADDMNMX / IMAD), 64 terms/clk/SM"))
+    if key == "int8_tensor":
+        passes = INT8_PASSES[path]
+        sustained = kern_s > 0.010          # long kernels run into the power cap
+        peak = pk["int8_tensor_sustained" if sustained else "int8_tensor_burst"]
+        roof = {"bound": "tensor", "achieved": passes * achieved / 1e12, "peak": peak / 1e12,
+                "unit": "int8 Tops/s", "peak_source": "measured cuBLASLt int8 GEMM (torch._int_mm), "
+                + ("sustained n=16384" if sustained else "burst n=8192") + ", profiles/r01_int8_peak.json",
+                "int8_ops_per_semiring_op": passes}
+        if passes > 1:
+            roof["emulated_fp64_tflops"] = achieved / 1e12
+            roof["vs_fp64_tensor_peak"] = achieved / pk["fp64_tensor"]
+    elif key == "fp64_tensor":
+        roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
+                "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
+                "profiles/r01_peaks_microbench.json, r01_cublas_dgemm.json (MEASURED_PEAKS.json "
+                "has no fp64 entry)"}
+    else:
+        roof = {"bound": "issue", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
+                "unit": "Tops/s", "peak_source": ("measured instruction-mix peak, "
+                "profiles/r01_packed_ops_microbench.jsonl / r01_peaks_microbench.json"
+                if key != "issue" else "BASELINE issue roofline: 148 SMs x 128 lanes x sm_max_mhz")}
+        roof["baseline_issue_roofline"] = pk["issue"] / 1e12
+        roof["frac_of_baseline_issue_roofline"] = achieved / pk["issue"]
+    roof["instruction_mix"] = mix
+    roof["frac"] = roof["achieved"] / roof["peak"]
+    roof["kernel_ms"] = kern_s * 1e3
+    return roof, mix
+
+
+def opt_in_run(args, s, cid, n, grid, rank, sms, local_rank, A, B, C, pk):
+    """Secondary measurement (N=1) of the config's OPT-IN tensor-core path: int64 on
+    tcgen05 kind::i8 (config 2) or fp64 via Ozaki-II (config 4).  Same inputs, own
+    copy of C, same timing rules; the headline line above stays the default path."""
+    from paper_1911_05328_b200.distributed import DistributedMM
+    cfg = CONFIGS[cid]
+    dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
+                        device=local_rank, time_kernel=True, combine=args.combine,
+                        int_tensor=(cid == 2), fp64_emu=(cid == 4))
+    C2 = C.clone()
+    steps, warm = max(1, min(args.steps, 3)), max(1, min(args.warmup, 2))
+    for _ in range(warm):
+        dmm.step(C2, A, B)
+    torch.cuda.synchronize()
+    dmm.plan.reset_stats()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(steps):
+        dmm.step(C2, A, B)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / steps
+    st = dmm.plan.stats()
+    kern_s = st["main_kernel_ns"] / 1e9 / max(1, st["main_kernel_launches"])
+    roof, _ = roofline(pk, st["path_name"], 2.0 * n ** 3, kern_s)
+    dmm.close()
+    del C2
+    return {"flag": "--fp64-emu" if cid == 4 else "--int-tensor", "path": st["path_name"],
+            "value": 2.0 * n ** 3 / t / 1e12, "unit": "Tops/s", "ms_per_step": t * 1e3, "steps": steps,
+            "roofline": roof, "note": "opt-in (DESIGN.md §5c/§5d); exactness / error bound in "
+            "tests/test_gpu_fp64_emulation.py and test_gpu_parity.py"}
 
 
 def _ncu_traffic(cid, path):
@@ -380,7 +440,8 @@ def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
     Ch0 = C.cpu().pin_memory()
     Ch = Ch0.clone().pin_memory()
     cfg = sm.Config(base_dim=CONFIGS[cid]["b"], workers=torch.cuda.get_device_properties(device)
-                    .multi_processor_count, allow_nonpow2=True, int_tensor_cores=args.int_tensor)
+                    .multi_processor_count, allow_nonpow2=True, int_tensor_cores=args.int_tensor,
+                    fp64_emulation=args.fp64_emu)
     ex = sm.Executor(cfg) if world == 1 else None
     out = None
     if world > 1:

@@ -88,7 +88,8 @@ class DistributedMM:
     def __init__(self, n: int, semiring, grid: Grid, rank: int, algo: str = "star",
                  base_dim: int = 64, workers: int = 1, group_ks=None,
                  local_mm: Optional[Callable] = None, device: Optional[int] = None,
-                 time_kernel: bool = False, combine: str = "nccl", int_tensor: bool = False):
+                 time_kernel: bool = False, combine: str = "nccl", int_tensor: bool = False,
+                 fp64_emu: bool = False):
         self.n, self.s, self.grid, self.rank = n, semiring, grid, rank
         self.I, self.J, self.K = grid.coords(rank)
         self.r0, self.r1 = block_bounds(n, grid.pr, self.I)
@@ -109,6 +110,8 @@ class DistributedMM:
                 flags |= _lib.F_TIME_MAIN
             if int_tensor:
                 flags |= _lib.F_INT_TENSOR
+            if fp64_emu:
+                flags |= _lib.F_FP64_EMU
             self.plan = _lib.Plan(semiring.sr_id, algo, "pooled", self.m, self.nn, self.k,
                                   base_dim, workers, -1,
                                   device if device is not None else torch.cuda.current_device(),
