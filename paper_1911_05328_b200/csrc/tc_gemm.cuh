@@ -19,8 +19,11 @@
 //   warps 2..5    : epilogue -- TMEM lanes 32 (w % 4) .. + 31 are output rows
 // Pipelines: STAGES-deep smem ring (full: TMA -> MMA, empty: MMA -> TMA) and a
 // 2-deep TMEM accumulator ring (acc_full: MMA -> epilogue of both CTAs, acc_empty:
-// 8 epilogue warps of the pair -> MMA), so the epilogue of pass j overlaps the
-// mainloop of pass j + 1.
+// 8 epilogue warps of the pair -> MMA), so the epilogue of one work unit overlaps
+// the mainloop of the next.  Work units are (pass, tile) in PASS-MAJOR order: all
+// of a CTA pair's tiles for pass p, then pass p + 1, so each pass streams its own
+// operand planes like one ordinary GEMM (tile-major order let the pairs drift
+// across passes and thrashed L2: 218 GB of DRAM reads per 16-pass launch).
 #pragma once
 #include <cuda.h>
 #include <cstdint>
@@ -50,7 +53,7 @@ constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >
 struct TcgShape {
     int tiles_m, tiles_n, num_tiles, group_m;   // 256 x 256 pair tiles, grouped raster
     int nk;                                     // k-stages per pass
-    int passes;                                 // stacked operand passes (1 or #moduli)
+    int passes;                                 // stacked operand passes (1 or #moduli), pass-major
     int a_pass_rows, b_pass_rows;               // row offset of pass p in the stacked maps
 };
 
@@ -148,25 +151,8 @@ struct TcgChunk {
     int last;        // last pass of the tile
     int lane;
     uint32_t* stage; // this warp's 32 x EPI_PITCH transpose buffer (8-byte capable)
-    int tile_slot;   // persistent unit ordinal of this CTA (for per-CTA scratch)
     int warp_q;      // TMEM lane quarter (w % 4)
     int chunk;       // 0 .. BN/32-1
-};
-
-// Deferred epilogue work of the PREVIOUS tile of this CTA, run in `passes` slices,
-// one after each pass epilogue of the current tile (and drained after the last
-// tile), so that a heavy reconstruction never holds a TMEM buffer (EpiOzakiF64).
-struct TcgDeferred {
-    int row0;        // first global output row of this warp's 32 rows (previous tile)
-    int colbase;     // first global output column of the previous tile
-    int slice;       // 0 .. passes-1
-    int buf;         // scratch buffer the previous tile used (tile_slot & 1)
-    int lane, warp_q;
-    uint32_t* stage;
-};
-struct TcgNoDeferred {
-    static constexpr bool kDeferred = false;
-    STARMM_DEV void deferred(const TcgDeferred&) const {}
 };
 
 // Transpose helper: lane L holds row (row0 + L), columns col0 .. col0+31 in v[];
@@ -218,10 +204,10 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
     if (warp == 0) {
         if (lane == 0) {   // ---- TMA producer (both CTAs) ----
             uint32_t it = 0;
-            for (int t = cluster_id; t < sh.num_tiles; t += num_clusters) {
-                int tm, tn;
-                tcg_tile_coords(sh, t, tm, tn);
-                for (int p = 0; p < sh.passes; ++p) {
+            for (int p = 0; p < sh.passes; ++p) {
+                for (int t = cluster_id; t < sh.num_tiles; t += num_clusters) {
+                    int tm, tn;
+                    tcg_tile_coords(sh, t, tm, tn);
                     const int ay = p * sh.a_pass_rows + tm * 256 + (int)rank * BM;
                     const int by = p * sh.b_pass_rows + tn * BN + (int)rank * BNH;
                     for (int kt = 0; kt < sh.nk; ++kt, ++it) {
@@ -238,8 +224,8 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
     } else if (warp == 1) {
         if (leader && lane == 0) {   // ---- MMA issuer (leader CTA only) ----
             uint32_t it = 0, u = 0;
-            for (int t = cluster_id; t < sh.num_tiles; t += num_clusters) {
-                for (int p = 0; p < sh.passes; ++p, ++u) {
+            for (int p = 0; p < sh.passes; ++p) {
+                for (int t = cluster_id; t < sh.num_tiles; t += num_clusters, ++u) {
                     const uint32_t b = u & 1;
                     if (u >= 2) mb_wait(&acc_empty[b], ((u >> 1) - 1) & 1);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -263,21 +249,17 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
         const int q = warp & 3;
         uint32_t* stage = epi_stage + (warp - 2) * 32 * EPI_PITCH * 2;
         uint32_t u = 0;
-        int slot = 0;
-        int prev_tm = -1, prev_tn = -1;
-        TcgDeferred dfr;
-        dfr.lane = lane; dfr.warp_q = q; dfr.stage = stage;
-        for (int t = cluster_id; t < sh.num_tiles; t += num_clusters, ++slot) {
-            int tm, tn;
-            tcg_tile_coords(sh, t, tm, tn);
-            for (int p = 0; p < sh.passes; ++p, ++u) {
+        for (int p = 0; p < sh.passes; ++p) {
+            for (int t = cluster_id; t < sh.num_tiles; t += num_clusters, ++u) {
+                int tm, tn;
+                tcg_tile_coords(sh, t, tm, tn);
                 const uint32_t b = u & 1;
                 mb_wait(&acc_full[b], (u >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
                 TcgChunk c;
                 c.row0 = tm * 256 + (int)rank * BM + q * 32;
                 c.pass = p; c.last = p == sh.passes - 1; c.lane = lane; c.stage = stage;
-                c.tile_slot = slot; c.warp_q = q;
+                c.warp_q = q;
 #pragma unroll 1
                 for (int ch = 0; ch < BN / 32; ++ch) {
                     uint32_t v[32];
@@ -289,20 +271,6 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                 asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
                 __syncwarp();
                 if (lane == 0) mb_arrive_cluster(&acc_empty[b], 0);
-                if (Epi::kDeferred && prev_tm >= 0) {
-                    dfr.row0 = prev_tm * 256 + (int)rank * BM + q * 32;
-                    dfr.colbase = prev_tn * BN; dfr.slice = p; dfr.buf = (slot - 1) & 1;
-                    epi.deferred(dfr);
-                }
-            }
-            prev_tm = tm; prev_tn = tn;
-        }
-        if (Epi::kDeferred && prev_tm >= 0) {          // drain the last tile
-            dfr.row0 = prev_tm * 256 + (int)rank * BM + q * 32;
-            dfr.colbase = prev_tn * BN; dfr.buf = (slot - 1) & 1;
-            for (int p = 0; p < sh.passes; ++p) {
-                dfr.slice = p;
-                epi.deferred(dfr);
             }
         }
     }
@@ -319,7 +287,7 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
 // Epilogues
 // ---------------------------------------------------------------------------
 // int32 results straight to an int32 matrix (dev harness / tests of the core).
-struct EpiStoreI32 : TcgNoDeferred {
+struct EpiStoreI32 {
     int* C; long long ldc; int M, N;
     STARMM_DEV void operator()(const TcgChunk& c, const uint32_t (&v)[32]) const {
         tcg_stage_rows(c, v);
@@ -345,7 +313,10 @@ STARMM_DEV void tcg_fold(const TcgOut& o, long long row, long long col, typename
     using T = typename Sr::T;
     if (o.remote_parts > 0) {
         const int part = (int)(row / o.remote_rows);
-        T* q = (T*)o.remote_base[part] + (row - part * o.remote_rows) * o.remote_ld + col;
+        void* base = o.remote_base[0];   // constant indices: no local-memory copy of the params
+#pragma unroll
+        for (int i = 1; i < 8; ++i) base = part == i ? o.remote_base[i] : base;
+        T* q = (T*)base + (row - part * o.remote_rows) * o.remote_ld + col;
         Sr::atomic_fold(q, d);
         return;
     }
@@ -355,7 +326,7 @@ STARMM_DEV void tcg_fold(const TcgOut& o, long long row, long long col, typename
 
 // small-range int64 ring: widen (exact) and fold into / store to int64 C.  The C
 // loads of a chunk are issued as one batch (16 rows in flight) before any store.
-struct EpiFoldI64 : TcgNoDeferred {
+struct EpiFoldI64 {
     TcgOut o;
     STARMM_DEV void operator()(const TcgChunk& c, const uint32_t (&v)[32]) const {
         tcg_stage_rows(c, v);

@@ -2,15 +2,18 @@
 # ncu evidence for the bench workloads (run under gpurun; one GPU).
 # Each profiled command first runs plain and must exit 0 (B200_PROFILING.md).
 # usage: bash tools/ncu_capture.sh <tag> [configs...]
+#   configs: 2 3 4 5 (default paths), 2t (config 2 --int-tensor), 4e (config 4 --fp64-emu)
 #   launch list : the bench command itself (e2e + cpu baseline legs included)
 #   full capture: the tile kernel, from the same command without the e2e / cpu legs
 set -x
 TAG=${1:-r01}; shift
 CFGS=${@:-4 3 5 2}
 for c in $CFGS; do
-  X=""; [ "$c" = "5" ] && X="--size 16384"
-  K=simt_mm; [ "$c" = "4" ] && K=dmma
-  B="python bench.py --steps 2 --warmup 1 --config $c $X"
+  base=${c:0:1}; X=""; F=""
+  [ "$base" = "5" ] && X="--size 16384"
+  K=simt_mm; [ "$base" = "4" ] && K=dmma
+  case $c in 2t) F="--int-tensor"; K=tcg_kernel;; 4e) F="--fp64-emu"; K=tcg_kernel;; esac
+  B="python bench.py --steps 2 --warmup 1 --config $base $X $F --no-opt-in"
   $B > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/${TAG}_launches_c$c.csv $B > /dev/null 2>&1 || exit 2

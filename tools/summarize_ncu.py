@@ -26,6 +26,9 @@ METRICS = [
     ("lts__t_sector_hit_rate.pct", "L2 hit %"),
     ("sm__throughput.avg.pct_of_peak_sustained_elapsed", "SM throughput %"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
+    ("TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+     "tensor pipe active % of elapsed (tcgen05)"),
+    ("TPC.TriageCompute.sm__pipe_tensor_subpipe_imma_cycles_active_realtime.avg", "IMMA subpipe active cycles"),
     ("sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active", "ALU pipe active %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe active %"),
     ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "ALU inst %"),
@@ -78,7 +81,8 @@ def main():
     cfgs = sys.argv[2:] or ["4", "2", "3", "5"]
     md = [f"# ncu summary `{tag}` (B200, `--clock-control none`)\n",
           "Launch lists: `ncu --metrics gpu__time_duration.sum` over `python bench.py --steps 2 "
-          "--warmup 1 --no-e2e --no-cpu-baseline --config C` (config 5 at `--n 16384`); times are "
+          "--warmup 1 --no-e2e --no-cpu-baseline --no-opt-in --config C` (config 5 at `--size 16384`; "
+          "`2t` = config 2 `--int-tensor`, `4e` = config 4 `--fp64-emu`); times are "
           "cold-cache and serialised, so compare SHARES. Full captures: `ncu --set full -k "
           "regex:<tile kernel> -s 1 -c 1` of the same command (tools/ncu_capture.sh).\n"]
     traffic_path = os.path.join(PROF, "ncu_traffic.json")
@@ -105,8 +109,8 @@ def main():
             wb = float(d["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1,
                                                          "Kbyte": 1e3}[d["dram__bytes_write.sum"][1]]
             n = plain["config"]["n"]
-            key = f"{c}:{path}"
-            if plain["config"]["n"] == {"2": 4096, "3": 8192, "4": 16384, "5": 49152}[c]:
+            key = f"{c[0]}:{path}"
+            if plain["config"]["n"] == {"2": 4096, "3": 8192, "4": 16384, "5": 49152}[c[0]]:
                 traffic[key] = rb + wb
             md.append(f"\nDRAM traffic per launch {(rb + wb) / 1e9:.2f} GB (n={n}).")
         except (KeyError, ValueError):

@@ -11,25 +11,6 @@
 #include "../paper_1911_05328_b200/csrc/ozaki.cuh"
 
 using namespace starmm;
-struct EpiOzNoCrt : EpiOzakiF64 {      // residue stores only (timing split)
-    STARMM_DEV void deferred(const TcgDeferred&) const {}
-};
-struct EpiOzNoStore : EpiOzakiF64 {    // CRT slices only (timing split)
-    STARMM_DEV void operator()(const TcgChunk&, const uint32_t (&)[32]) const {}
-};
-template <class E> float time_oz(const CUtensorMap& ta, const CUtensorMap& tb, const TcgShape& sh, const EpiOzakiF64& base,
-                                 int grid, int reps) {
-    E e; static_cast<EpiOzakiF64&>(e) = base;
-    auto k = tcg_kernel<E>;
-    cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES);
-    k<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, e);
-    cudaDeviceSynchronize();
-    cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-    cudaEventRecord(a);
-    for (int r = 0; r < reps; ++r) k<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, e);
-    cudaEventRecord(b); cudaEventSynchronize(b);
-    float ms; cudaEventElapsedTime(&ms, a, b); return ms / reps;
-}
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { \
     printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); exit(1); } } while (0)
 
@@ -117,19 +98,12 @@ int main(int argc, char** argv) {
         for (int j = 0; j < N; ++j) if (hc[j] != hr[(size_t)i * N + j]) { if (bad < 5) printf("mismatch r%d c%d %d vs %d\n", rows[i], j, hc[j], hr[(size_t)i*N+j]); ++bad; }
     }
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
-    if (epi_kind[0] == 'o') {
-        if (passes != oz::P) { printf("oz epilogue needs passes=%d\n", oz::P); return 1; }
-        EpiOzakiF64 eo;
-        double* Cd; unsigned long long* mx; unsigned char* scr;
-        CK(cudaMalloc(&Cd, (size_t)M * N * 8)); CK(cudaMemset(Cd, 0, (size_t)M * N * 8));
-        CK(cudaMalloc(&mx, (size_t)(M + N) * 8)); CK(cudaMemset(mx, 0, (size_t)(M + N) * 8));
-        CK(cudaMalloc(&scr, (size_t)grid * 2 * EpiOzakiF64::BUF_BYTES));
-        eo.o.C = Cd; eo.o.ldc = N; eo.o.M = M; eo.o.N = N; eo.o.init_identity = 0; eo.o.remote_parts = 0;
-        eo.rowmax = mx; eo.colmax = mx + M; eo.t = 54; eo.scratch = scr;
-        memset(&eo.crt, 0, sizeof(eo.crt)); eo.crt.invM = 1e-38;
-        printf("{\"split_ms\": {\"store_only\": %.3f, \"crt_only\": %.3f}}\n",
-               time_oz<EpiOzNoCrt>(ta, tb, sh, eo, grid, reps), time_oz<EpiOzNoStore>(ta, tb, sh, eo, grid, reps));
-        auto ko = tcg_kernel<EpiOzakiF64>;
+    if (epi_kind[0] == 'o') {   // Ozaki residue epilogue (timing only)
+        unsigned char* Rb;
+        CK(cudaMalloc(&Rb, (size_t)passes * M * N));
+        EpiOzakiResidues eo;
+        eo.R = Rb; eo.Mp = M; eo.Np = N;
+        auto ko = tcg_kernel<EpiOzakiResidues>;
         CK(cudaFuncSetAttribute(ko, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
         ko<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, eo);
         CK(cudaDeviceSynchronize());
