@@ -290,26 +290,60 @@ int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int
 
 // The CTA-pair tensor-core GEMM over `passes` stacked int8 operand planes
 // (A: passes x [Mp][Kp], B^T: passes x [Np][Kp]); Mp, Np multiples of 256.
+// CTA pairs that can be co-resident (cluster 2x1x1, 1 CTA/SM): the persistent grid,
+// which the drift gate requires to be fully resident
 template <class Epi>
+int tcg_max_clusters(int sms) {
+    static int cached = -1;
+    if (cached < 0) {
+        auto kern = tcg_kernel<Epi>;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3((unsigned)sms); lc.blockDim = dim3(tcg::THREADS); lc.dynamicSmemBytes = tcg::SMEM_BYTES;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.attrs = at; lc.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, kern, &lc) != cudaSuccess || c < 1) {
+            cudaGetLastError();
+            c = std::max(1, sms / 2);
+        }
+        cached = c;
+    }
+    return cached;
+}
+
+// `acquire(bytes, &ptr)` hands out stream-ordered scratch (the plan's arena) for the
+// drift-gate counters: one per (pass, tile round), zeroed before the launch.
+template <class Epi, class Acquire>
 int launch_tcg(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp, int passes,
-               const Epi& epi, int sms, cudaStream_t s, int* grid_out) {
+               const Epi& epi, int sms, cudaStream_t s, Acquire&& acquire) {
     if ((long long)passes * Mp >= (1LL << 31) || (long long)passes * Np >= (1LL << 31)) return STARMM_TOO_LARGE;
     CUtensorMap ta, tb;
     TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp * passes, Kp, tcg::BM));
     TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np * passes, Kp, tcg::BNH));
     auto kern = tcg_kernel<Epi>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
-        attr_done = true;
-    }
+    const int clusters = tcg_max_clusters<Epi>(sms);
     TcgShape sh;
     sh.tiles_m = (int)(Mp / 256); sh.tiles_n = (int)(Np / 256); sh.num_tiles = sh.tiles_m * sh.tiles_n;
     sh.group_m = 8;
     sh.nk = (int)(Kp / tcg::BK); sh.passes = passes;
     sh.a_pass_rows = (int)Mp; sh.b_pass_rows = (int)Np;
-    const int grid = 2 * std::max(1, std::min(sms / 2, sh.num_tiles));
-    if (grid_out) *grid_out = grid;
+    const int pairs = std::max(1, std::min(clusters, sh.num_tiles));
+    const int grid = 2 * pairs;
+    // bounded drift, one wave: 16-pass n=16384 DRAM reads 274 -> 69 GB, GEMM -17%
+    // (tools/tc_gemm_dev.cu)
+    sh.rounds = (sh.num_tiles + pairs - 1) / pairs;
+    sh.gate_depth = 1;
+    sh.gate = nullptr;
+    if ((long long)passes * sh.rounds > 1) {
+        void* g = nullptr;
+        const size_t gb = (size_t)passes * sh.rounds * sizeof(unsigned);
+        TRY(acquire(gb, &g));
+        CK(cudaMemsetAsync(g, 0, gb, s));
+        sh.gate = (unsigned*)g;
+    }
     kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES, s>>>(ta, tb, sh, epi);
     CK(cudaGetLastError());
     return STARMM_OK;
@@ -800,13 +834,13 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if (path == PATH_TC_I8) {
             EpiFoldI64 e;
             e.o = tcg_out(P, C, ldc, init_identity);
-            rc = launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s, nullptr);
+            rc = launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s, stage_acquire);
         } else if (path == PATH_OZAKI_F64) {
             void* planes = nullptr;
             if ((rc = stage_acquire((size_t)oz::P * Mp * Np, &planes))) break;
             EpiOzakiResidues e;
             e.R = (unsigned char*)planes; e.Mp = Mp; e.Np = Np;
-            if ((rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, nullptr))) break;
+            if ((rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, stage_acquire))) break;
             if (timed && (rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
             const long long groups = (P->n + OZ_CRT_W - 1) / OZ_CRT_W;
             oz_crt_kernel<<<grid_blocks(P->m * groups), 256, 0, s>>>(

@@ -55,6 +55,12 @@ struct TcgShape {
     int nk;                                     // k-stages per pass
     int passes;                                 // stacked operand passes (1 or #moduli), pass-major
     int a_pass_rows, b_pass_rows;               // row offset of pass p in the stacked maps
+    // bounded drift (optional): the producer of every CTA may start wave w + gate_depth
+    // only after all CTAs issued every load of wave w (waves = pass x tile round), so
+    // the pairs stay close enough in time to share each wave's panels in L2.  Needs
+    // every cluster co-resident (the grid comes from cudaOccupancyMaxActiveClusters).
+    unsigned* gate;                             // passes * rounds counters, zeroed; or null
+    int gate_depth, rounds;
 };
 
 // ---------------------------------------------------------------------------
@@ -67,6 +73,9 @@ STARMM_DEV uint32_t cta_rank() {
 }
 STARMM_DEV void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+STARMM_DEV unsigned ld_acquire(const unsigned* p) {
+    unsigned v; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
 }
 STARMM_DEV void mb_init(uint64_t* b, uint32_t n) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su32(b)), "r"(n));
@@ -208,6 +217,12 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                 for (int t = cluster_id; t < sh.num_tiles; t += num_clusters) {
                     int tm, tn;
                     tcg_tile_coords(sh, t, tm, tn);
+                    const int w = p * sh.rounds + (t - cluster_id) / num_clusters;
+                    if (sh.gate && w >= sh.gate_depth) {
+                        const int wd = w - sh.gate_depth, rd = wd % sh.rounds;
+                        const unsigned need = 2u * (unsigned)min(num_clusters, sh.num_tiles - rd * num_clusters);
+                        while (ld_acquire(sh.gate + wd) < need) __nanosleep(128);
+                    }
                     const int ay = p * sh.a_pass_rows + tm * 256 + (int)rank * BM;
                     const int by = p * sh.b_pass_rows + tn * BN + (int)rank * BNH;
                     for (int kt = 0; kt < sh.nk; ++kt, ++it) {
@@ -217,6 +232,10 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                         if (leader) mb_expect_tx(&full[s], 2 * STAGE_BYTES);
                         tma_load_2sm(a, &tmap_a, &full[s], kt * BK, ay);
                         tma_load_2sm(a + A_BYTES, &tmap_b, &full[s], kt * BK, by);
+                    }
+                    if (sh.gate) {
+                        __threadfence();
+                        atomicAdd(sh.gate + w, 1u);
                     }
                 }
             }

@@ -58,6 +58,7 @@ int main(int argc, char** argv) {
     int passes = argc > 5 ? atoi(argv[5]) : 1;
     int group_m = argc > 6 ? atoi(argv[6]) : 8;
     const char* epi_kind = argc > 7 ? argv[7] : "i32";   // i32 | oz (Ozaki CRT epilogue, timing only)
+    int gate_depth = argc > 8 ? atoi(argv[8]) : 0;     // 0: no drift gating
     // M, N multiples of 256, K multiple of 128 (dev harness)
     signed char *A, *B; int* C;
     CK(cudaMalloc(&A, (size_t)M * K * passes)); CK(cudaMalloc(&B, (size_t)N * K * passes));
@@ -70,12 +71,32 @@ int main(int argc, char** argv) {
     TcgShape sh;
     sh.tiles_m = M / 256; sh.tiles_n = N / 256; sh.num_tiles = sh.tiles_m * sh.tiles_n; sh.group_m = group_m;
     sh.nk = K / tcg::BK; sh.passes = passes; sh.a_pass_rows = M; sh.b_pass_rows = N;
+    sh.gate = nullptr; sh.gate_depth = gate_depth; sh.rounds = 1;
     EpiStoreI32 epi;
     epi.C = C; epi.ldc = N; epi.M = M; epi.N = N;
     auto kern = tcg_kernel<EpiStoreI32>;
     CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
     int sms; CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-    int grid = 2 * std::min(sms / 2, sh.num_tiles);
+    int clusters = 0;
+    {
+        cudaLaunchConfig_t lc = {};
+        lc.gridDim = dim3(sms); lc.blockDim = dim3(tcg::THREADS); lc.dynamicSmemBytes = tcg::SMEM_BYTES;
+        cudaLaunchAttribute at[1]; at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = 2; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+        lc.attrs = at; lc.numAttrs = 1;
+        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
+        CK(cudaOccupancyMaxActiveClusters(&clusters, kern, &lc));
+    }
+    int grid = 2 * std::min(clusters, sh.num_tiles);
+    sh.rounds = (sh.num_tiles + grid / 2 - 1) / (grid / 2);
+    unsigned* gate = nullptr;
+    if (gate_depth > 0) {
+        CK(cudaMalloc(&gate, (size_t)sh.rounds * passes * 4 * 64));
+        sh.gate = gate;
+    }
+    auto reset_gate = [&]() { if (gate) cudaMemsetAsync(gate, 0, (size_t)sh.rounds * passes * 4); };
+    printf("{\"max_active_clusters\": %d}\n", clusters);
+    reset_gate();
     kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, epi);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
@@ -105,14 +126,15 @@ int main(int argc, char** argv) {
         eo.R = Rb; eo.Mp = M; eo.Np = N;
         auto ko = tcg_kernel<EpiOzakiResidues>;
         CK(cudaFuncSetAttribute(ko, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
+        reset_gate();
         ko<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, eo);
         CK(cudaDeviceSynchronize());
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) ko<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, eo);
+        for (int r = 0; r < reps; ++r) { reset_gate(); ko<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, eo); }
         cudaEventRecord(e1);
     } else {
         cudaEventRecord(e0);
-        for (int r = 0; r < reps; ++r) kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, epi);
+        for (int r = 0; r < reps; ++r) { reset_gate(); kern<<<grid, tcg::THREADS, tcg::SMEM_BYTES>>>(ta, tb, sh, epi); }
         cudaEventRecord(e1);
     }
     CK(cudaEventSynchronize(e1));
