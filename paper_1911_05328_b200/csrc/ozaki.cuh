@@ -65,12 +65,32 @@ STARMM_DEV uint32_t oz_res_limbs(int x2, int x1, int x0) {
     return (uint32_t)r & 0xff;
 }
 
+// The same residue on the FP64 pipe: q = rint(x / m) can be off by one (x/m rounds),
+// the remainder fma(-m, q, x) is exact, and the symmetric fold is integer.
+template <int m>
+STARMM_DEV uint32_t oz_res_f64(double x) {
+    const double q = rint(x * (1.0 / m));
+    int r = (int)fma(-(double)m, q, x);
+    r += (r < -((m - 1) / 2)) ? m : 0;
+    r -= (r > (m - 1) / 2) ? m : 0;
+    return (uint32_t)r & 0xff;
+}
+
+// All P residues of one scaled element, ORed into byte `shift` of each plane's word.
+// Odd moduli go through the FP64 pipe, even ones through IMAD: the packers are
+// math-pipe bound, and the two pipes issue in parallel.
 template <int I = 0>
-STARMM_DEV void oz_pack_element(long long x, int shift, uint32_t (&packed)[oz::P]) {
+STARMM_DEV void oz_pack_element(double xd, long long x, int shift, uint32_t (&packed)[oz::P]) {
     if constexpr (I < oz::P) {
-        const int x0 = (int)(x & 0x1FFFFF), x1 = (int)((x >> 21) & 0x1FFFFF), x2 = (int)(x >> 42);
-        packed[I] |= oz_res_limbs<oz::MOD[I]>(x2, x1, x0) << shift;
-        oz_pack_element<I + 1>(x, shift, packed);
+        uint32_t r;
+        if constexpr (I % 2 == 1) {
+            r = oz_res_f64<oz::MOD[I]>(xd);
+        } else {
+            const int x0 = (int)(x & 0x1FFFFF), x1 = (int)((x >> 21) & 0x1FFFFF), x2 = (int)(x >> 42);
+            r = oz_res_limbs<oz::MOD[I]>(x2, x1, x0);
+        }
+        packed[I] |= r << shift;
+        oz_pack_element<I + 1>(xd, x, shift, packed);
     }
 }
 
@@ -124,14 +144,14 @@ __global__ void oz_amax_cols_kernel(const double* B, long long k, long long n, l
 // ---- residue packing -----------------------------------------------------------
 // A [m][k] (row-major = K-major already) -> P planes [Mp][Kp] int8; each thread
 // converts 4 consecutive k of one row and stores one 32-bit word per plane.
+// Grid: x over the k-words of a row, y strides over rows (no divisions).
 __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, long long lda,
                                     const unsigned long long* rowmax, int t, signed char* out,
                                     long long Mp, long long Kp) {
-    const long long words = Mp * (Kp / 4);
     const long long plane = Mp * Kp;
-    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < words;
-         w += (long long)gridDim.x * blockDim.x) {
-        const long long r = w / (Kp / 4), k0 = (w - r * (Kp / 4)) * 4;
+    const long long k0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
+    if (k0 >= Kp) return;
+    for (long long r = blockIdx.y; r < Mp; r += gridDim.y) {
         uint32_t packed[oz::P];
 #pragma unroll
         for (int p = 0; p < oz::P; ++p) packed[p] = 0;
@@ -140,7 +160,10 @@ __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, l
 #pragma unroll
             for (int e = 0; e < 4; ++e) {
                 const long long kk = k0 + e;
-                if (kk < k) oz_pack_element(__double2ll_rn(oz_ldexp(A[r * lda + kk], sig)), 8 * e, packed);
+                if (kk < k) {
+                    const double xd = rint(oz_ldexp(A[r * lda + kk], sig));
+                    oz_pack_element(xd, (long long)xd, 8 * e, packed);
+                }
             }
         }
 #pragma unroll
@@ -171,7 +194,10 @@ oz_pack_cols_kernel(const double* B, long long k, long long n, long long ldb,
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
             const long long kk = k0 + kw * 4 + e;
-            if (c < n && kk < k) oz_pack_element(__double2ll_rn(oz_ldexp(B[kk * ldb + c], tau)), 8 * e, packed);
+            if (c < n && kk < k) {
+                const double xd = rint(oz_ldexp(B[kk * ldb + c], tau));
+                oz_pack_element(xd, (long long)xd, 8 * e, packed);
+            }
         }
 #pragma unroll
         for (int p = 0; p < oz::P; ++p) tile[p][tx][kw] = packed[p];
@@ -325,11 +351,10 @@ __global__ void __launch_bounds__(256)
 oz_crt_kernel(const unsigned char* __restrict__ R, long long Mp, long long Np,
               const unsigned long long* __restrict__ rowmax, const unsigned long long* __restrict__ colmax,
               int t, const OzCrt crt, const TcgOut o) {
-    const long long groups = (o.N + OZ_CRT_W - 1) / OZ_CRT_W;
-    const long long total = o.M * groups;
-    for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < total;
-         w += (long long)gridDim.x * blockDim.x) {
-        const long long row = w / groups, c0 = (w - row * groups) * OZ_CRT_W;
+    // grid: x over 16-column groups of a row, y strides over rows (no divisions)
+    const long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * OZ_CRT_W;
+    if (c0 >= o.N) return;
+    for (long long row = blockIdx.y; row < o.M; row += gridDim.y) {
         const unsigned char* rbase = R + (size_t)row * Np + c0;
         const bool local = o.remote_parts == 0;
         const int ncol = (int)min((long long)OZ_CRT_W, o.N - c0);

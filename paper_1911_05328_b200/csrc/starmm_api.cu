@@ -769,7 +769,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
       if (rc) break;
         if (path == PATH_OZAKI_F64) {   // residue planes for the scales the guard pass found
             const int t = ozaki_bits(P->k);
-            oz_pack_rows_kernel<<<grid_blocks(Mp * Kp / 4), 256, 0, s>>>(
+            oz_pack_rows_kernel<<<dim3((unsigned)((Kp / 4 + 255) / 256), (unsigned)std::min<long long>(Mp, 65535)), 256, 0, s>>>(
                 (const double*)A, P->m, P->k, lda, oz_rowmax, t, (signed char*)opA, Mp, Kp);
             oz_pack_cols_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 64)), dim3(32, 8), 0, s>>>(
                 (const double*)B, P->k, P->n, ldb, oz_colmax, t, (signed char*)opB, Np, Kp);
@@ -843,7 +843,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             if ((rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, stage_acquire))) break;
             if (timed && (rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
             const long long groups = (P->n + OZ_CRT_W - 1) / OZ_CRT_W;
-            oz_crt_kernel<<<grid_blocks(P->m * groups), 256, 0, s>>>(
+            oz_crt_kernel<<<dim3((unsigned)((groups + 127) / 128), (unsigned)std::min<long long>(P->m, 65535)), 128, 0, s>>>(
                 (const unsigned char*)planes, Mp, Np, oz_rowmax, oz_colmax, ozaki_bits(P->k), ozaki_crt(),
                 tcg_out(P, C, ldc, init_identity));
             rc = cuda_status(cudaGetLastError());
