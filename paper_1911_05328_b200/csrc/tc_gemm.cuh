@@ -12,14 +12,15 @@
 // those 128 rows of A and 128 of the 256 B^T rows (columns of C) per k-stage, and
 // holds its 128 x 256 s32 accumulator half in its own TMEM.
 //
-// Roles per CTA (192 threads):
+// Roles per CTA (320 threads):
 //   warp 0 lane 0 : TMA producer (both CTAs; bytes land on the leader's full barrier)
 //   warp 1        : TMEM owner (alloc/dealloc, cta_group::2); lane 0 of the LEADER
 //                   issues the MMAs and commits (multicast) to both CTAs' barriers
-//   warps 2..5    : epilogue -- TMEM lanes 32 (w % 4) .. + 31 are output rows
+//   warps 2..9    : epilogue -- TMEM lanes 32 (w % 4) .. + 31 are output rows; the
+//                   two warps of a lane quarter take 128 columns each
 // Pipelines: STAGES-deep smem ring (full: TMA -> MMA, empty: MMA -> TMA) and a
 // 2-deep TMEM accumulator ring (acc_full: MMA -> epilogue of both CTAs, acc_empty:
-// 8 epilogue warps of the pair -> MMA), so the epilogue of one work unit overlaps
+// 16 epilogue warps of the pair -> MMA), so the epilogue of one work unit overlaps
 // the mainloop of the next.  Work units are (pass, tile) in PASS-MAJOR order: all
 // of a CTA pair's tiles for pass p, then pass p + 1, so each pass streams its own
 // operand planes like one ordinary GEMM (tile-major order let the pairs drift
@@ -37,10 +38,11 @@ constexpr int BN = 256;                 // output columns per pair tile (UMMA N)
 constexpr int BNH = BN / 2;             // B^T rows loaded per CTA
 constexpr int BK = 128;                 // int8 elements (= bytes) per k-stage: one 128B swizzle atom
 constexpr int STAGES = 6;
-constexpr int THREADS = 192;
+constexpr int EPI_WARPS = 8;           // 2 per TMEM lane quarter, each half the columns
+constexpr int THREADS = 64 + 32 * EPI_WARPS;
 constexpr int A_BYTES = BM * BK, B_BYTES = BNH * BK, STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int EPI_PITCH = 33;           // elements; per-warp 32 x 32 transpose buffer
-constexpr int EPI_BYTES = 4 * 32 * EPI_PITCH * 8;   // sized for 8-byte elements
+constexpr int EPI_PITCH = 33;           // 4-byte words; per-warp 32 x 32 transpose buffer
+constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_PITCH * 4;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + EPI_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int ACC_COLS = BN;            // one s32 accumulator = 256 TMEM columns
 constexpr int TMEM_COLS = 2 * ACC_COLS; // double-buffered: all 512 columns
@@ -159,7 +161,7 @@ struct TcgChunk {
     int pass;        // pass index (CRT modulus)
     int last;        // last pass of the tile
     int lane;
-    uint32_t* stage; // this warp's 32 x EPI_PITCH transpose buffer (8-byte capable)
+    uint32_t* stage; // this warp's 32 x EPI_PITCH word transpose buffer
     int warp_q;      // TMEM lane quarter (w % 4)
     int chunk;       // 0 .. BN/32-1
 };
@@ -195,7 +197,7 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) { mb_init(&full[s], 1); mb_init(&empty[s], 1); }
-        for (int b = 0; b < 2; ++b) { mb_init(&acc_full[b], 1); mb_init(&acc_empty[b], 8); }
+        for (int b = 0; b < 2; ++b) { mb_init(&acc_full[b], 1); mb_init(&acc_empty[b], 2 * EPI_WARPS); }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_a) : "memory");
         asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&tmap_b) : "memory");
@@ -264,9 +266,9 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                 }
             }
         }
-    } else {   // ---- epilogue warps 2..5 (both CTAs) ----
-        const int q = warp & 3;
-        uint32_t* stage = epi_stage + (warp - 2) * 32 * EPI_PITCH * 2;
+    } else {   // ---- epilogue warps 2..9 (both CTAs) ----
+        const int q = warp & 3, half = (warp - 2) >> 2;
+        uint32_t* stage = epi_stage + (warp - 2) * 32 * EPI_PITCH;
         uint32_t u = 0;
         for (int p = 0; p < sh.passes; ++p) {
             for (int t = cluster_id; t < sh.num_tiles; t += num_clusters, ++u) {
@@ -280,7 +282,7 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                 c.pass = p; c.last = p == sh.passes - 1; c.lane = lane; c.stage = stage;
                 c.warp_q = q;
 #pragma unroll 1
-                for (int ch = 0; ch < BN / 32; ++ch) {
+                for (int ch = half * (BN / 64); ch < (half + 1) * (BN / 64); ++ch) {
                     uint32_t v[32];
                     tmem_ld32(tmem + b * ACC_COLS + ((uint32_t)(q * 32) << 16) + ch * 32, v);
                     c.col0 = tn * BN + ch * 32;
@@ -382,17 +384,24 @@ struct EpiFoldI64 {
 // int64 (|x| <= 127 once the guard passes) -> int8, K-major [rows][kp], zero padded.
 // A is already [m][k]; B ([k][n]) is transposed through a 32x32 shared-memory tile.
 // Both fold the range guard into the same pass (RangeAcc, aux_kernels.cuh).
+// grid: x over 8-element k-words of a row, y strides over rows (no divisions)
 __global__ void pack_i8_rows_kernel(const long long* A, long long rows, long long kdim, long long lda,
                                     signed char* P, long long rowsp, long long kp,
                                     unsigned long long* range) {
     RangeAcc acc;
-    long long total = rowsp * kp;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / kp, k = idx - r * kp;
-        long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
-        acc.add(v);
-        P[idx] = (signed char)v;
+    const long long k0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
+    if (k0 < kp) {
+        for (long long r = blockIdx.y; r < rowsp; r += gridDim.y) {
+            uint32_t w[2] = {0u, 0u};
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                const long long k = k0 + e;
+                const long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
+                acc.add(v);
+                w[e >> 2] |= (uint32_t)(unsigned char)(signed char)v << (8 * (e & 3));
+            }
+            *reinterpret_cast<uint2*>(P + r * kp + k0) = make_uint2(w[0], w[1]);
+        }
     }
     if (range) acc.flush(range);
 }
