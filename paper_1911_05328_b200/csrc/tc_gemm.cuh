@@ -59,8 +59,9 @@ struct TcgShape {
     int a_pass_rows, b_pass_rows;               // row offset of pass p in the stacked maps
     // bounded drift (optional): the producer of every CTA may start wave w + gate_depth
     // only after all CTAs issued every load of wave w (waves = pass x tile round), so
-    // the pairs stay close enough in time to share each wave's panels in L2.  Needs
-    // every cluster co-resident (the grid comes from cudaOccupancyMaxActiveClusters).
+    // the pairs stay close enough in time to share each wave's panels in L2.  Meant
+    // for a fully co-resident grid (cudaOccupancyMaxActiveClusters); a wait gives up
+    // after 2 ms, so a partly resident grid is slower but cannot deadlock.
     unsigned* gate;                             // passes * rounds counters, zeroed; or null
     int gate_depth, rounds;
 };
@@ -75,6 +76,9 @@ STARMM_DEV uint32_t cta_rank() {
 }
 STARMM_DEV void cluster_sync() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+STARMM_DEV unsigned long long globaltimer_ns() {
+    unsigned long long t; asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t)); return t;
 }
 STARMM_DEV unsigned ld_acquire(const unsigned* p) {
     unsigned v; asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory"); return v;
@@ -223,7 +227,11 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
                     if (sh.gate && w >= sh.gate_depth) {
                         const int wd = w - sh.gate_depth, rd = wd % sh.rounds;
                         const unsigned need = 2u * (unsigned)min(num_clusters, sh.num_tiles - rd * num_clusters);
-                        while (ld_acquire(sh.gate + wd) < need) __nanosleep(128);
+                        // bounded wait: if the grid is not fully co-resident (another
+                        // kernel holding SMs), give up after 2 ms instead of hanging
+                        const unsigned long long t0 = globaltimer_ns();
+                        while (ld_acquire(sh.gate + wd) < need && globaltimer_ns() - t0 < 2000000ull)
+                            __nanosleep(128);
                     }
                     const int ay = p * sh.a_pass_rows + tm * 256 + (int)rank * BM;
                     const int by = p * sh.b_pass_rows + tn * BN + (int)rank * BNH;
