@@ -26,7 +26,7 @@ pytestmark = pytest.mark.gpu
 TILES = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "ref_tiles.json")))
 
 
-def _run(cid, algo="star", C0=None, A=None, B=None, workers=148):
+def _run(cid, algo="star", C0=None, A=None, B=None, workers=148, **opt):
     cfg = CONFIGS[cid]
     s = sm.get_semiring(cfg["semiring"])
     if A is None:
@@ -34,7 +34,7 @@ def _run(cid, algo="star", C0=None, A=None, B=None, workers=148):
     Am = sm.Matrix(A, s)
     Bm = Am if B is A else sm.Matrix(B, s)
     C = sm.Matrix(C0, s)
-    conf = sm.Config(base_dim=cfg["b"], workers=workers, allow_nonpow2=(cid == 5))
+    conf = sm.Config(base_dim=cfg["b"], workers=workers, allow_nonpow2=(cid == 5), **opt)
     with sm.Executor(conf) as ex:
         sm.run_algorithm(ex, algo, C, Am, Bm, s)
         st = ex.last_stats
@@ -113,6 +113,31 @@ def test_config4_fp64_n16384():
     lhs = (C.data.sum() - torch.from_numpy(C0).cuda().sum()).item()
     rhs = (Am.data.sum(0) * Bm.data.sum(1)).sum().item()
     assert abs(lhs - rhs) <= 1e-9 * max(1.0, abs(rhs)) * n
+
+
+def test_config2_opt_in_tensor_cores_full_size():
+    """Opt-in tcgen05 kind::i8 path at config 2's full size: the 64 sampled tiles and
+    the reference's tile hashes bit-exact, and bit-identical to the default dp4a path."""
+    A, B, C0 = make_inputs(2)
+    ref = _run(2, A=A, B=B, C0=C0)[3].data
+    _, _, _, C, Am, Bm, st = _run(2, A=A, B=B, C0=C0, int_tensor_cores=True)
+    assert st["path_name"] == "tcgen05_i8_umma"
+    _check_tiles(2, A, B, C0, C.data, count=64)
+    assert torch.equal(C.data, ref)
+
+
+def test_config4_opt_in_fp64_emulation_full_size():
+    """Opt-in Ozaki-II at config 4's full size: sampled tiles within the config-4
+    tolerance, the checksum of checksums, and bitwise determinism across runs."""
+    A, B, C0, C, Am, Bm, st = _run(4, fp64_emulation=True)
+    assert st["path_name"] == "ozaki2_fp64_tcgen05_i8x16"
+    _check_tiles(4, A, B, C0, C.data, count=16)
+    n = A.shape[0]
+    lhs = (C.data.sum() - torch.from_numpy(C0).cuda().sum()).item()
+    rhs = (Am.data.sum(0) * Bm.data.sum(1)).sum().item()
+    assert abs(lhs - rhs) <= 1e-9 * max(1.0, abs(rhs)) * n
+    again = _run(4, A=A, B=B, C0=C0, fp64_emulation=True)[3].data
+    assert torch.equal(again, C.data)
 
 
 def test_config5_tropical_i32_n49152():
