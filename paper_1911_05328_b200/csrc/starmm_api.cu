@@ -1220,8 +1220,10 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const size_t eb = (size_t)elem_bytes(P->sr);
     const long long m = P->m, n = P->n, k = P->k;
     // auto: ~one block per 1e12 semiring ops (>= ~15 ms of B200 work, so per-block
-    // guards / packing stay negligible), at most 16 blocks
-    long long auto_blocks = std::max<long long>(1, std::min<long long>(
+    // guards / packing stay negligible), at most 16 blocks, and at least 4 once m >= 512
+    // so that small, PCIe-bound problems still overlap uploads, compute and downloads
+    // (config 2: one block left 384 MB up, compute and 128 MB down fully serial)
+    long long auto_blocks = std::max<long long>(m >= 512 ? 4 : 1, std::min<long long>(
         16, (long long)(2.0 * (double)m * (double)n * (double)k / 1e12)));
     long long R = block_rows > 0 ? block_rows
                                  : std::max<long long>(128, round_up((m + auto_blocks - 1) / auto_blocks, 128));
