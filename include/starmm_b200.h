@@ -135,8 +135,11 @@ int  starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mo
 int  starmm_execute(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,
                     const void* B, int64_t ldb, void* stream);
 /* Same computation with C, A and B in HOST memory (pinned for full overlap):
- * B is uploaded once, A/C stream through in blocks of `block_rows` rows (0 = auto)
- * overlapping the tile kernels, finished C blocks stream back.  Blocking.
+ * compute-bound problems first run k-outer chunks over all rows as A's column
+ * chunks and B's row chunks arrive, then the rest of k in row blocks of
+ * `block_rows` rows (0 = auto) whose results (C0 folded in) stream back while the
+ * next block computes; PCIe-bound ones upload B, then stream A/C row blocks.
+ * Blocking.  DESIGN.md §7b.
  * The reference's entry points take host (numpy) matrices (classic.py:294-316);
  * this is their host-buffer form. */
 int  starmm_execute_host(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,

@@ -213,6 +213,12 @@ __global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long
 }
 
 // Zero-padded copy (DMMA path): dst[rp x cp] from src[rows x cols, ld].
+// the range guard's two words -> mapped pinned host memory (zero-copy stores)
+__global__ void publish_range_kernel(const unsigned long long* d_range, unsigned long long* h_range) {
+    if (threadIdx.x < 2) h_range[threadIdx.x] = d_range[threadIdx.x];
+    __threadfence_system();
+}
+
 template <class T>
 __global__ void pad_copy_kernel(const T* src, long long rows, long long cols, long long ld,
                                 T* dst, long long rp, long long cp) {

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <vector>
+#include <string>
 #include <algorithm>
 #include <cmath>
 #include <limits>
@@ -110,6 +111,11 @@ struct starmm_plan {
     // persistent device bookkeeping (from the arena, kept for the plan's life)
     unsigned long long* d_counters = nullptr;   // CNT__N
     unsigned long long* d_range = nullptr;      // 2 words
+    // the guard's verdict is published to mapped pinned host memory by a 1-thread kernel
+    // (zero-copy stores, no copy engine: a D2H memcpy here would queue behind the host
+    // path's block downloads on the D2H engine)
+    volatile unsigned long long* h_range = nullptr;
+    unsigned long long* h_range_dev = nullptr;
     unsigned* d_worker_used = nullptr;          // per persistent worker
     int max_workers = 0;
     starmm_stats st;
@@ -117,6 +123,7 @@ struct starmm_plan {
     long long raw_count = 0, raw_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
     int last_guarded_path = 0;                  // optimistic first guess for the next execute
+    int split_half_waves = 8;                   // auto k-split: grow s until tasks >= this many half waves
     long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
     long long str_issued = 0;                   // Strassen temporaries currently issued
     // peer destinations of the fused k-split combine (starmm_plan_set_peers)
@@ -405,6 +412,10 @@ int ensure_bookkeeping(starmm_plan* P) {
     P->d_counters = (unsigned long long*)p;
     P->d_range = P->d_counters + CNT__N;
     P->d_worker_used = (unsigned*)(P->d_range + 2);
+    void* h = nullptr;
+    CK(cudaHostAlloc(&h, 16, cudaHostAllocMapped));
+    P->h_range = (volatile unsigned long long*)h;
+    CK(cudaHostGetDevicePointer((void**)&P->h_range_dev, h, 0));
     return STARMM_OK;
 }
 
@@ -481,6 +492,7 @@ void starmm_plan_destroy(starmm_plan* P) {
     cudaDeviceSynchronize();
     if (P->ev0) cudaEventDestroy(P->ev0);
     if (P->ev1) cudaEventDestroy(P->ev1);
+    if (P->h_range) cudaFreeHost((void*)P->h_range);
     P->arena.destroy();
     cudaSetDevice(prev);
     delete P;
@@ -583,7 +595,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             // busy for several waves; otherwise each worker runs its tile's k range serially
             // (the in-place, temporary-free order of serial TAR/SAR).
             s_log2 = 0;
-            while ((tiles << s_log2) < 4LL * gpu_workers) ++s_log2;
+            while (2 * (tiles << s_log2) < (long long)P->split_half_waves * gpu_workers) ++s_log2;
         }
         // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels
         // than the recursion has (log2(k / b))
@@ -731,8 +743,12 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if (!guard_pending) break;
         // ---- the fused guard: decide the exact path the observed range allows ----
         unsigned long long h[2];
-        if ((rc = cuda_status(cudaMemcpyAsync(h, P->d_range, sizeof(h), cudaMemcpyDeviceToHost, s)))) break;
+        publish_range_kernel<<<1, 32, 0, s>>>(P->d_range, P->h_range_dev);
+        if ((rc = cuda_status(cudaGetLastError()))) break;
         if ((rc = cuda_status(cudaStreamSynchronize(s)))) break;
+        h[0] = P->h_range[0];
+        h[1] = P->h_range[1];
+        ++launches;
         guard_pending = false;
         const unsigned long long mx = h[0];
         const bool bad = h[1] != 0;
@@ -1205,11 +1221,50 @@ int starmm_ipc_close(void* dptr) {
     return STARMM_OK;
 }
 
-// Host-buffer execution: B is uploaded once; A and C stream through the device in
-// row blocks on a copy stream while the previous block computes on `stream`, and
-// finished C blocks stream back on a second copy stream (H2D and D2H overlap each
-// other and the tile kernels).  Each block is an ordinary execute of an
-// (R x n x k) sub-problem, so paths, schedules and guards are unchanged.
+// Host-buffer execution.  Two phases, so that the GPU computes from
+// the first uploaded megabytes and the result streams back while it still computes:
+//  1. k-outer prologue: k-chunks [kb_c, kb_{c+1}) of geometrically growing width
+//     (k/32, k/16, ... while they cover at most half of k).  Chunk c needs only
+//     A[:, chunk] and B[chunk, :]; it runs as ONE execute over all m rows into the
+//     device C (the first chunk stores, C <- A(x)B, later ones fold).  Uploads of
+//     chunk c+1 overlap chunk c's compute; only chunk 0's transfer is exposed.
+//  2. row blocks: block i folds the remaining k range [kq, k) into its rows, then
+//     C0 (uploaded meanwhile into a staging buffer) is folded in with madd and the
+//     block streams back on its own copy stream while block i+1 computes.
+// (+) and min are associative and commutative, so integers and (min,+) stay
+// bit-exact; fp64 sums in a different order (tolerance, as every k-split).  When
+// A aliases B (square, same ld) every element is uploaded once: chunk c adds the
+// "cross" of row block c (columns >= kb_c) and column block c (rows >= kb_{c+1}),
+// and the bottom-right square [kq, m) x [kq, n) completes the matrix before phase 2.
+// STARMM_HOST_PHASE1=0 disables phase 1 (row blocks only, C0 uploaded in place).
+// Phase 1 pays only when the problem is compute-bound over PCIe: the estimated compute
+// time (a nominal per-semiring B200 rate) must exceed the H2D time (50 GB/s); PCIe-bound
+// problems (config 2) upload B first and run row blocks only.  STARMM_HOST_PHASE1=0/1
+// forces the choice.
+static double host_nominal_ops(int sr) {
+    switch (sr) {
+    case STARMM_SR_FP64: return 35e12;     // DMMA
+    case STARMM_SR_INT64: return 100e12;   // dp4a when the range guard passes
+    default: return 60e12;                 // (min,+): VIADDMNMX.S16x2 / fp32 carrier
+    }
+}
+
+static int host_phase1_chunks(long long m, long long n, long long k, int sr, double h2d_bytes,
+                              std::vector<long long>& kb) {
+    kb.assign(1, 0);
+    const char* env = getenv("STARMM_HOST_PHASE1");
+    if ((env && env[0] == '0') || m < 512 || k < 512) return 0;
+    const double t_mm = 2.0 * (double)m * (double)n * (double)k / host_nominal_ops(sr);
+    if (!(env && env[0] == '1') && t_mm < h2d_bytes / 50e9) return 0;
+    long long w = std::max<long long>(128, round_up((k + 31) / 32, 128)), sum = 0;
+    while (sum + w <= k / 2) {
+        sum += w;
+        kb.push_back(sum);
+        w *= 2;
+    }
+    return (int)kb.size() - 1;
+}
+
 int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* stream, int64_t block_rows) {
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
@@ -1219,110 +1274,167 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (prev_dev != P->device) CK(cudaSetDevice(P->device));
     const size_t eb = (size_t)elem_bytes(P->sr);
     const long long m = P->m, n = P->n, k = P->k;
-    // auto: ~one block per 1e12 semiring ops (>= ~15 ms of B200 work, so per-block
-    // guards / packing stay negligible), at most 16 blocks, and at least 4 once m >= 512
-    // so that small, PCIe-bound problems still overlap uploads, compute and downloads
-    // (config 2: one block left 384 MB up, compute and 128 MB down fully serial)
-    long long auto_blocks = std::max<long long>(m >= 512 ? 4 : 1, std::min<long long>(
-        16, (long long)(2.0 * (double)m * (double)n * (double)k / 1e12)));
+    const int saved_flags = P->flags;
+    const bool user_init = (saved_flags & STARMM_F_INIT_IDENTITY) != 0;   // C <- A(x)B: C0 unused
+    std::vector<long long> kb;
+    const bool same_ab = (A == B) && (m == k) && (n == k) && (lda == ldb);
+    const double h2d = (double)eb * ((double)m * k + (same_ab ? 0.0 : (double)k * n) +
+                                     ((saved_flags & STARMM_F_INIT_IDENTITY) ? 0.0 : (double)m * n));
+    const int nq = host_phase1_chunks(m, n, k, P->sr, h2d, kb);
+    const long long kq = kb.back();
+    // phase-2 row blocks: ~2.5e11 semiring ops each (>= ~7 ms of B200 work, so per-block
+    // guards / packing stay negligible), at most 16, and at least 8 (m >= 1024) or 4
+    // (m >= 512) so that small, PCIe-bound problems overlap uploads, compute and downloads
+    const double ops2 = 2.0 * (double)m * (double)n * (double)(k - kq);
+    const long long lo_blocks = m >= 1024 ? 8 : (m >= 512 ? 4 : 1);
+    const long long auto_blocks = std::max<long long>(lo_blocks, std::min<long long>(16, (long long)(ops2 / 2.5e11)));
     long long R = block_rows > 0 ? block_rows
                                  : std::max<long long>(128, round_up((m + auto_blocks - 1) / auto_blocks, 128));
     R = std::min(R, m);
     const long long nblk = (m + R - 1) / R;
-    const bool same_ab = (A == B) && (m == k) && (n == k) && (lda == ldb);
+    const bool staged_c0 = nq > 0 && !user_init;    // phase 1 owns dC, C0 goes to a staging buffer
     cudaStream_t cs = (cudaStream_t)stream;
     cudaStream_t up = nullptr, down = nullptr;
     CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
-    std::vector<cudaEvent_t> ev_in(nblk), ev_done(nblk);
-    for (auto& e : ev_in) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    for (auto& e : ev_done) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    void *dA = nullptr, *dB = nullptr, *dC = nullptr;
+    std::vector<cudaEvent_t> ev_q(nq), ev_a(nblk), ev_c(nblk), ev_done(nblk);
+    cudaEvent_t ev_rest = nullptr;
+    CK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
+    for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
+        for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // STARMM_HOST_TRACE=1: timing events on the three streams, printed as one JSON line
+    // per event to stderr (label, ms since the start) -- the schedule's timeline
+    const char* tenv = getenv("STARMM_HOST_TRACE");
+    const bool tracing = tenv && tenv[0] == '1';
+    std::vector<std::pair<std::string, cudaEvent_t>> trace;
+    auto mark = [&](const std::string& label, cudaStream_t st) {
+        if (!tracing) return;
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        cudaEventRecord(e, st);
+        trace.push_back({label, e});
+    };
+    mark("start", cs);
+    if (tracing) {
+        cudaStreamWaitEvent(up, trace[0].second, 0);
+        cudaStreamWaitEvent(down, trace[0].second, 0);
+    }
+    void *dA = nullptr, *dB = nullptr, *dC = nullptr, *dC0 = nullptr;
     long long fr = 0, ru = 0;
     const size_t a_bytes = (size_t)m * k * eb, b_bytes = (size_t)k * n * eb, c_bytes = (size_t)m * n * eb;
     int rc = STARMM_OK;
+    // host (src, ld_src) -> device (dst, ld_dst): the rows x cols block at (r0, c0)
+    auto up_block = [&](void* dst, long long ld_dst, const void* src, long long ld_src, long long r0,
+                        long long c0, long long rows, long long cols) {
+        if (rows <= 0 || cols <= 0) return (int)STARMM_OK;
+        return cuda_status(cudaMemcpy2DAsync((char*)dst + (r0 * ld_dst + c0) * eb, ld_dst * eb,
+                                             (const char*)src + (r0 * ld_src + c0) * eb, ld_src * eb,
+                                             cols * eb, rows, cudaMemcpyHostToDevice, up));
+    };
+    const char* k2env = getenv("STARMM_HOST_KSPLIT2");   // phase-2 k-split override (tuning)
+    const int ks2 = k2env ? atoi(k2env) : -2;
+    const int saved_ks = P->ksplit_req;
+    auto run = [&](void* Cd, const void* Ad, const void* Bd, long long rows, long long kk, bool store) {
+        P->m = rows; P->k = kk;
+        // phase-2 row blocks are slices of a larger problem: split k only while the
+        // tiles fill less than half a wave (k-split partials cost atomics -- CAS loops
+        // for float minima -- which cost more than an idle fraction of one wave)
+        if (kk == k - kq) {
+            P->split_half_waves = 1;
+            if (ks2 >= -1) P->ksplit_req = ks2;
+        }
+        P->flags = store ? (saved_flags | STARMM_F_INIT_IDENTITY) : (saved_flags & ~STARMM_F_INIT_IDENTITY);
+        int r = execute_impl(P, Cd, n, Ad, k, Bd, n, cs, true);
+        P->m = m; P->k = k; P->flags = saved_flags; P->ksplit_req = saved_ks; P->split_half_waves = 8;
+        return r;
+    };
     do {
         if ((rc = P->arena.acquire(a_bytes, &dA, false, &fr, &ru))) break;
         if (!same_ab && (rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
         if (same_ab) dB = dA;
         if ((rc = P->arena.acquire(c_bytes, &dC, false, &fr, &ru))) break;
-        // Upload order on `up`: block 0 of A and C, then B in k-chunks of R rows (when
-        // B aliases A those chunks ARE A's row blocks), then the remaining A/C blocks.
-        // Block 0 computes chunk by chunk as B arrives -- C0 (+)= sum_kc A0[:,kc] (x)
-        // B[kc,:] is exact by associativity -- so only the first chunk's transfer is
-        // exposed; later blocks need all of B and find it resident.
-        const long long KC = R;   // tools/e2e_ab.py: 299 ms vs 328 ms unchunked (config 4)
-        const long long nkc = (k + KC - 1) / KC;
-        std::vector<cudaEvent_t> ev_kc(nkc);
-        for (auto& e : ev_kc) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-        auto up_rows = [&](void* dst, const void* src, long long ld_src, long long cols, long long r0,
-                           long long rows) {
-            return cuda_status(cudaMemcpy2DAsync((char*)dst + r0 * cols * eb, cols * eb,
-                                                 (const char*)src + r0 * ld_src * eb, ld_src * eb,
-                                                 cols * eb, rows, cudaMemcpyHostToDevice, up));
-        };
-        const long long rows0 = std::min(R, m);
-        if ((rc = up_rows(dA, A, lda, k, 0, rows0))) break;    // (= B's chunk 0 when aliased)
-        if ((rc = up_rows(dC, C, ldc, n, 0, rows0))) break;
-        if ((rc = cuda_status(cudaEventRecord(ev_in[0], up)))) break;     // A0, C0 resident
-        for (long long c = 0; c < nkc && !rc; ++c) {
-            long long k0 = c * KC, kr = std::min(KC, k - k0);
+        if (staged_c0 && (rc = P->arena.acquire(c_bytes, &dC0, false, &fr, &ru))) break;
+        void* dCin = staged_c0 ? dC0 : dC;   // where C0's rows land
+        // ---- uploads, in consumption order, all on `up` ----
+        for (int c = 0; c < nq && !rc; ++c) {
+            const long long k0 = kb[c], k1 = kb[c + 1];
             if (same_ab) {
-                if (c > 0) rc = up_rows(dA, A, lda, k, k0, kr);               // A row block c
+                rc = up_block(dA, k, A, lda, k0, k0, k1 - k0, n - k0);             // row block c
+                if (!rc) rc = up_block(dA, k, A, lda, k1, k0, m - k1, k1 - k0);    // column block c
             } else {
-                rc = up_rows(dB, B, ldb, n, k0, kr);
+                rc = up_block(dB, n, B, ldb, k0, 0, k1 - k0, n);                   // B[chunk, :]
+                if (!rc) rc = up_block(dA, k, A, lda, 0, k0, m, k1 - k0);          // A[:, chunk]
             }
-            if (!rc) rc = cuda_status(cudaEventRecord(ev_kc[c], up));
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_q[c], up));
+            mark("up_chunk" + std::to_string(c), up);
         }
-        for (long long b = 1; b < nblk && !rc; ++b) {
-            long long r0 = b * R, rows = std::min(R, m - r0);
-            if (!same_ab) rc = up_rows(dA, A, lda, k, r0, rows);
-            if (!rc) rc = up_rows(dC, C, ldc, n, r0, rows);
-            if (!rc) rc = cuda_status(cudaEventRecord(ev_in[b], up));
-        }
-        if (rc) { for (auto& e : ev_kc) cudaEventDestroy(e); break; }
-        const long long saved_m = P->m, saved_k = P->k;
-        const int saved_flags = P->flags;
-        // block 0, chunk by chunk
-        if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[0], 0)))) { for (auto& e : ev_kc) cudaEventDestroy(e); break; }
-        for (long long c = 0; c < nkc && !rc; ++c) {
-            long long k0 = c * KC, kr = std::min(KC, k - k0);
-            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_kc[c], 0)))) break;
-            P->m = rows0;
-            P->k = kr;
-            if (c > 0) P->flags &= ~STARMM_F_INIT_IDENTITY;   // later chunks fold into C
-            rc = execute_impl(P, dC, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true);
-            P->m = saved_m; P->k = saved_k; P->flags = saved_flags;
-        }
-        for (auto& e : ev_kc) cudaEventDestroy(e);
         if (rc) break;
+        if (same_ab) rc = up_block(dA, k, A, lda, kq, kq, m - kq, n - kq);         // bottom-right
+        else rc = up_block(dB, n, B, ldb, kq, 0, k - kq, n);                       // B[kq:, :]
+        if (!rc) rc = cuda_status(cudaEventRecord(ev_rest, up));
+        mark("up_rest", up);
         for (long long b = 0; b < nblk && !rc; ++b) {
-            long long r0 = b * R, rows = std::min(R, m - r0);
-            if (b > 0) {
-                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_in[b], 0)))) break;
-                P->m = rows;
-                rc = execute_impl(P, (char*)dC + r0 * n * eb, n, (char*)dA + r0 * k * eb, k, dB, n, cs,
-                                  true);
-                P->m = saved_m;
+            const long long r0 = b * R, rows = std::min(R, m - r0);
+            if (!same_ab) rc = up_block(dA, k, A, lda, r0, kq, rows, k - kq);      // A[blk, kq:]
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_a[b], up));
+            mark("up_a" + std::to_string(b), up);
+            if (!rc && !user_init) rc = up_block(dCin, n, C, ldc, r0, 0, rows, n); // C0[blk, :]
+            if (!rc) rc = cuda_status(cudaEventRecord(ev_c[b], up));
+            mark("up_c" + std::to_string(b), up);
+        }
+        if (rc) break;
+        // ---- phase 1: k-outer chunks over all rows ----
+        for (int c = 0; c < nq && !rc; ++c) {
+            const long long k0 = kb[c], k1 = kb[c + 1];
+            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_q[c], 0)))) break;
+            rc = run(dC, (char*)dA + k0 * eb, (char*)dB + k0 * n * eb, m, k1 - k0, c == 0);
+            mark("mm_chunk" + std::to_string(c), cs);
+        }
+        if (rc) break;
+        // ---- phase 2: row blocks over [kq, k), C0 fold, download ----
+        if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_rest, 0)))) break;
+        for (long long b = 0; b < nblk && !rc; ++b) {
+            const long long r0 = b * R, rows = std::min(R, m - r0);
+            char* Cb = (char*)dC + r0 * n * eb;
+            if (kq < k) {
+                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_a[b], 0)))) break;
+                if (nq == 0 && (rc = cuda_status(cudaStreamWaitEvent(cs, ev_c[b], 0)))) break;
+                rc = run(Cb, (char*)dA + (r0 * k + kq) * eb, (char*)dB + kq * n * eb, rows, k - kq,
+                         nq == 0 && user_init);
                 if (rc) break;
+                mark("mm_blk" + std::to_string(b), cs);
+            }
+            if (staged_c0) {
+                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_c[b], 0)))) break;
+                if ((rc = madd_dispatch(P->sr, Cb, n, (char*)dC0 + r0 * n * eb, n, rows, n, 0, cs))) break;
             }
             if ((rc = cuda_status(cudaEventRecord(ev_done[b], cs)))) break;
             if ((rc = cuda_status(cudaStreamWaitEvent(down, ev_done[b], 0)))) break;
-            rc = cuda_status(cudaMemcpy2DAsync((char*)C + r0 * ldc * eb, ldc * eb, (char*)dC + r0 * n * eb,
-                                               n * eb, n * eb, rows, cudaMemcpyDeviceToHost, down));
+            rc = cuda_status(cudaMemcpy2DAsync((char*)C + r0 * ldc * eb, ldc * eb, Cb, n * eb, n * eb, rows,
+                                               cudaMemcpyDeviceToHost, down));
+            mark("down" + std::to_string(b), down);
         }
-        P->m = saved_m;
         if (rc) break;
         if ((rc = cuda_status(cudaStreamSynchronize(down)))) break;
         rc = cuda_status(cudaStreamSynchronize(cs));
     } while (0);
+    P->m = m; P->k = k; P->flags = saved_flags;
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(down);
+    cudaStreamSynchronize(cs);
+    for (auto& t : trace) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, trace[0].second, t.second);
+        fprintf(stderr, "{\"host_trace\": \"%s\", \"ms\": %.3f}\n", t.first.c_str(), ms);
+    }
+    for (auto& t : trace) cudaEventDestroy(t.second);
+    if (dC0) P->arena.release(dC0, c_bytes);
     if (dC) P->arena.release(dC, c_bytes);
     if (dB && !same_ab) P->arena.release(dB, b_bytes);
     if (dA) P->arena.release(dA, a_bytes);
-    for (auto& e : ev_in) cudaEventDestroy(e);
-    for (auto& e : ev_done) cudaEventDestroy(e);
+    cudaEventDestroy(ev_rest);
+    for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
+        for (auto& e : *v) cudaEventDestroy(e);
     cudaStreamDestroy(up);
     cudaStreamDestroy(down);
     if (prev_dev != P->device) cudaSetDevice(prev_dev);

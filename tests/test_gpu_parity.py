@@ -14,6 +14,7 @@ import torch
 
 import paper_1911_05328_b200 as sm
 from oracle import oracle as O
+from _host_schedule import host_phase1
 
 pytestmark = pytest.mark.gpu
 
@@ -368,10 +369,59 @@ def test_host_path_streams_row_blocks(sid, pinned, block_rows):
     with sm.Executor(sm.Config(base_dim=32, workers=148)) as ex:
         ex.execute_host("star", Ct, At, Bt, s, block_rows=block_rows)
         if block_rows:
-            # row blocks + the first block's k-chunks (computed as B streams in)
+            # phase-1 k-chunks over all rows + one execute per phase-2 row block
             nb = -(-n // block_rows)
-            assert ex.last_stats["executes"] == (nb - 1) + nb
+            assert ex.last_stats["executes"] == (len(host_phase1(n, n, n, sid)) - 1) + nb
     assert_match(sid, Ct.numpy(), want)
+
+
+@pytest.mark.parametrize("sid", ["int", "float", "tropical_f32", "tropical_i32"])
+@pytest.mark.parametrize("n", [512, 640, 1024, 1408])
+@pytest.mark.parametrize("aliased", [False, True])
+@pytest.mark.parametrize("phase1", ["1", "0"])
+def test_host_path_two_phase_schedule(sid, n, aliased, phase1, monkeypatch):
+    """Both phases of the host schedule: k-outer chunks (first one stores, C0 folded
+    from its staging buffer at the end) and row blocks; A aliasing B uploads each
+    element once through the cross / bottom-right regions."""
+    monkeypatch.setenv("STARMM_HOST_PHASE1", phase1)
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(n + aliased)
+    lo, hi = (1, 100) if sid.startswith("tropical") else (-30, 30)
+    A = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    B = A if aliased else rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    C0 = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    want = C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B, par=True)
+    At = torch.from_numpy(A.copy()).pin_memory()
+    Bt = At if aliased else torch.from_numpy(B.copy()).pin_memory()
+    Ct = torch.from_numpy(C0.copy()).pin_memory()
+    with sm.Executor(sm.Config(base_dim=64, workers=148, allow_nonpow2=True)) as ex:
+        ex.execute_host("star", Ct, At, Bt, s)
+        nq = len(host_phase1(n, n, n, sid, aliased)) - 1
+        assert nq == (0 if phase1 == "0" else (1 if n < 1024 else 2))
+        assert ex.last_stats["executes"] >= nq + 1
+    assert_match(sid, Ct.numpy(), want)
+
+
+def test_host_path_store_flag_ignores_c0():
+    """STARMM_F_INIT_IDENTITY through the host path: C <- A (x) B (C0 never uploaded)."""
+    n = 1024
+    s = sm.INT_RING
+    rng = np.random.default_rng(5)
+    A = rng.integers(-9, 9, (n, n))
+    B = rng.integers(-9, 9, (n, n))
+    want = np.zeros((n, n), np.int64)
+    O.gemm_fold(O.SR_INT64, want, A, B, par=True)
+    for ph in ("1", "0"):
+        os.environ["STARMM_HOST_PHASE1"] = ph
+        try:
+            Ct = torch.full((n, n), 7, dtype=torch.int64).pin_memory()
+            with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
+                ex.execute_host("star", Ct, torch.from_numpy(A).pin_memory(),
+                                torch.from_numpy(B).pin_memory(), s, flags=0x4)
+            assert np.array_equal(Ct.numpy(), want), ph
+        finally:
+            del os.environ["STARMM_HOST_PHASE1"]
 
 
 def test_host_path_aliased_operands_and_public_api():
