@@ -85,6 +85,47 @@ def test_split_protocols_vs_oracle(algo, ksplit, sid):
     assert_match(sid, got, want)
 
 
+# ---- SPEC oracle-equality property and determinism --
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("sid", ["int", "float", "tropical"])
+def test_spec_oracle_equality_property(algo, sid):
+    """Every algorithm, n in {b, 2b, 4b, 8b, 16b}, 10 seeds: int / tropical exact,
+    float within rel 1e-9 (matrices_equal), against the pinned oracle."""
+    b = 8
+    s = sm.get_semiring(sid)
+    for n in (b, 2 * b, 4 * b, 8 * b, 16 * b):
+        for seed in range(10):
+            rng = np.random.default_rng(1000 * n + seed)
+            if sid == "int":
+                A, B, C0 = (rng.integers(-100, 100, (n, n)).astype(np.int64) for _ in range(3))
+            elif sid == "float":
+                A, B, C0 = (rng.uniform(-1, 1, (n, n)) for _ in range(3))
+            else:
+                A, B, C0 = (rng.integers(0, 50, (n, n)).astype(np.float64) for _ in range(3))
+                A[rng.random(A.shape) < 0.1] = np.inf
+            want = C0.copy()
+            O.gemm_fold(SR_OF[sid], want, A, B)
+            got = run(algo, s, C0, A, B, sm.Config(base_dim=b, workers=1 + seed % 4 * 5))
+            assert_match(sid, got, want)
+
+
+@pytest.mark.parametrize("sid", ["int", "tropical", "tropical_f32", "tropical_i32"])
+@pytest.mark.parametrize("algo,ksplit", [("tar", 3), ("sar", 3), ("star", 3), ("co3", 2), ("star", None)])
+def test_integer_and_minplus_results_deterministic(sid, algo, ksplit):
+    """Integer and (min,+) values do not depend on the concurrent schedule: repeated
+    runs with concurrent k-slices (atomics, pair states) give identical bits."""
+    n = 384
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(7)
+    A = rng.integers(-60 if sid == "int" else 0, 60, (n, n)).astype(s.dtype)
+    B = rng.integers(-60 if sid == "int" else 0, 60, (n, n)).astype(s.dtype)
+    C0 = rng.integers(0, 200, (n, n)).astype(s.dtype)
+    cfg = sm.Config(base_dim=32, workers=148, ksplit=ksplit, allow_nonpow2=True)
+    outs = [run(algo, s, C0, A, B, cfg) for _ in range(4)]
+    for o in outs[1:]:
+        assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
+
+
 # ---- BASELINE config 1 (PR1) ----------------------------------------------
 def test_pr1_star_fp64_vs_reference():
     from bench_configs import make_inputs
