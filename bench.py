@@ -433,8 +433,9 @@ def _ncu_traffic(cid, path):
 def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
     """Public-API end to end with pinned HOST buffers, every step: N=1 goes through
     host_mm-style Executor.execute_host (starmm_execute_host streams row blocks, copies
-    overlapped with the tile kernels); N>1 copies each rank's panels in, runs
-    DistributedMM.step and copies the owned result rows out."""
+    overlapped with the tile kernels); N>1 runs DistributedMM.step_host on each rank's
+    pinned panels (the same overlapped host path without a k-split; with one, the
+    panels go up, the combine runs on the device and the owned rows come back)."""
     Ah = A.cpu().pin_memory()
     Bh = Ah if B is A else B.cpu().pin_memory()
     Ch0 = C.cpu().pin_memory()
@@ -452,11 +453,7 @@ def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
         if world == 1:
             ex.execute_host(args.algo, Ch, Ah, Bh, s)
         else:
-            Ad = Ah.to(device, non_blocking=True)
-            Bd = Ad if Bh is Ah else Bh.to(device, non_blocking=True)
-            Cd = Ch.to(device, non_blocking=True)
-            r = dmm.step(Cd, Ad, Bd)
-            out.copy_(r, non_blocking=True)
+            dmm.step_host(Ch, Ah, Bh, out)
 
     one()
     torch.cuda.synchronize()
@@ -479,7 +476,7 @@ def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
             "steps": steps, "timer": "host wall clock around the blocking API call",
             "api": "Executor.execute_host (starmm_execute_host: pinned host C, A, B)" if world == 1
-            else "DistributedMM.step with per-rank pinned panels"}
+            else "DistributedMM.step_host with per-rank pinned panels"}
 
 
 def reference_arm(args, world, rank):

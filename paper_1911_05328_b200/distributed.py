@@ -201,6 +201,35 @@ class DistributedMM:
         dist.barrier(group=self.group_ks)
         return self.owned[:r]
 
+    def step_host(self, C_h: torch.Tensor, A_h: torch.Tensor, B_h: torch.Tensor,
+                  out_h: Optional[torch.Tensor] = None) -> torch.Tensor:
+        """The step with this rank's panels in HOST memory (pinned CPU tensors or strided
+        views of pinned full matrices); returns this rank's reduced rows on the host.
+
+        Without a k-split the rank's sub-problem is independent, so it runs through
+        starmm_execute_host: uploads, tile kernels and downloads overlap,
+        and C_h is updated in place.  With a k-split the panels are uploaded, the
+        combine runs on the device, and the owned rows are copied into ``out_h``."""
+        if self.grid.ks == 1 and self.plan is not None:
+            for t in (C_h, A_h, B_h):
+                if t.device.type != "cpu" or (t.shape[1] > 1 and t.stride(1) != 1):
+                    raise ContractViolation("step_host needs row-major CPU panels")
+            stream = torch.cuda.current_stream().cuda_stream
+            self.plan.execute_host(C_h.data_ptr(), max(1, C_h.stride(0)), A_h.data_ptr(),
+                                   max(1, A_h.stride(0)), B_h.data_ptr(), max(1, B_h.stride(0)),
+                                   stream)
+            return C_h
+        dev = torch.device("cuda", torch.cuda.current_device())
+        Ad = A_h.to(dev, non_blocking=True)
+        Bd = Ad if B_h is A_h else B_h.to(dev, non_blocking=True)
+        Cd = C_h.to(dev, non_blocking=True)
+        r = self.step(Cd, Ad, Bd)
+        if out_h is None:
+            out_h = torch.empty(r.shape, dtype=r.dtype).pin_memory()
+        out_h.copy_(r, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out_h
+
     def close(self):
         if self.plan is not None:
             self.plan.close()

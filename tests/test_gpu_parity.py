@@ -480,6 +480,33 @@ def test_host_path_aliased_operands_and_public_api():
         sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64))
 
 
+@pytest.mark.parametrize("sid", ["int", "float", "tropical_i32"])
+@pytest.mark.parametrize("rank", [0, 3])
+def test_distributed_step_host_2d_block(sid, rank):
+    """DistributedMM.step_host without a k-split: rank (I, J) of a 2 x 2 grid runs its
+    block through the overlapped host path on strided views of pinned full matrices."""
+    from paper_1911_05328_b200.distributed import DistributedMM, Grid
+    n = 1536
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(40 + rank)
+    lo, hi = (1, 1000) if sid == "tropical_i32" else (-40, 40)
+    A = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    B = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    C0 = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    dmm = DistributedMM(n, s, Grid(2, 2, 1), rank, base_dim=64, workers=148, device=0)
+    Ah, Bh = torch.from_numpy(A).pin_memory(), torch.from_numpy(B).pin_memory()
+    Ch = torch.from_numpy(C0.copy()).pin_memory()
+    out = dmm.step_host(dmm.c_block(Ch), dmm.a_panel(Ah), dmm.b_panel(Bh))
+    dmm.close()
+    want = C0[dmm.r0:dmm.r1, dmm.c0:dmm.c1].copy()
+    O.gemm_fold(SR_OF[sid], want, np.ascontiguousarray(A[dmm.r0:dmm.r1]),
+                np.ascontiguousarray(B[:, dmm.c0:dmm.c1]), par=True)
+    assert_match(sid, out.numpy(), want)
+    rest = np.ones((n, n), bool)
+    rest[dmm.r0:dmm.r1, dmm.c0:dmm.c1] = False
+    assert np.array_equal(Ch.numpy()[rest], C0[rest])   # only the rank's block was written
+
+
 # ---- fused k-split combine (starmm_plan_set_peers), emulated on one GPU -----
 @pytest.mark.parametrize("sid,extra", [("int", 0), ("float", 0), ("tropical_f32", 0), ("tropical_i32", 0),
                                        ("int", 0x20), ("float", 0x40)])
