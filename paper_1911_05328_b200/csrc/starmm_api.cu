@@ -584,7 +584,39 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
         tiles = tiles_m * tiles_n;
         gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
-        if (P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64) {
+        const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
+        const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
+        if (simt_path && (P->ksplit_req < 0 || !may_split)) {
+            // CUDA-core paths: pick (CTAs per SM, split depth) by a wave cost model
+            //   time ~ ceil(tasks / CTAs) * (stages per task + overhead) / per-CTA rate
+            // overhead = 4.5 stages of prologue/epilogue per task, plus the split write-back
+            // (atomics: 2 stages; the CAS loop of the float minima: 20).  The kernels are
+            // compiled for two CTAs per SM; launched at one per SM they run at 0.89 of a
+            // full SM (tools/ksplit_ab.py, profiles/r01i_ksplit_c2.json).  Small problems
+            // such as config 2 (1024 tiles = 3.46 waves of 296 CTAs) then prefer one CTA
+            // per SM (co2: +5.5%) or a split to two.  co2 never splits (classic.py:125-128).
+            const bool cas_min = P->sr == STARMM_SR_TROPICAL_F32 || P->sr == STARMM_SR_TROPICAL_F64;
+            const double kst = (double)round_up(P->k, BK) / BK;
+            int smax = 0;
+            if (may_split)
+                while (smax < 6 && (P->k >> (smax + 1)) >= std::max(P->base_dim, BK) &&
+                       (tiles << smax) < 8LL * gpu_workers)
+                    ++smax;
+            double best = 0;
+            int best_occ = per_sm, best_s = 0;
+            for (int occ = per_sm; occ >= 1; --occ) {
+                const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : 0.89) : 1.0 / occ;
+                for (int sl = 0; sl <= smax; ++sl) {
+                    const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
+                    const double ovh = 4.5 + (sl == 0 ? 0.0 : (cas_min ? 20.0 : 2.0));
+                    const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
+                    if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
+                }
+            }
+            per_sm = best_occ;
+            gpu_workers = P->sms * per_sm;
+            s_log2 = best_s;
+        } else if (!may_split) {
             s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
                                    // (the opt-in tensor path keeps whole-K tiles too)
         } else if (P->ksplit_req >= 0) {
@@ -927,7 +959,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     }
 
     P->st.tasks = ntasks;
-    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * shape.per_sm);
+    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * per_sm);
     P->st.ksplit = S;
     P->st.tar_levels = tar_levels;
     P->st.kernel_launches = launches;
