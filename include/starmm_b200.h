@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define STARMM_ABI_VERSION 1
+#define STARMM_ABI_VERSION 2
 
 /* ---- status codes (errors.py:4-41) ------------------------------------- */
 enum starmm_status {
@@ -121,6 +121,8 @@ typedef struct {
     int64_t executes;
     int64_t main_kernel_ns;          /* sum of tile-kernel event times (STARMM_F_TIME_MAIN) */
     int64_t main_kernel_launches;    /* launches that contributed to main_kernel_ns      */
+    int64_t balanced_workers;        /* >0: tar/star ran balanced (uneven) k-slices over this
+                                        many workers, shared tiles merged by atomic-madd  */
 } starmm_stats;
 
 int  starmm_abi_version(void);

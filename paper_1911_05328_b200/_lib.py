@@ -39,7 +39,7 @@ class StarmmStats(ctypes.Structure):
         "pool_reuse_count", "tile_serializations", "pair_count", "pair_transitions",
         "lazy_temp_acquires", "raw_alloc_count", "raw_alloc_bytes", "tasks", "workers",
         "ksplit", "tar_levels", "kernel_launches", "path", "executes", "main_kernel_ns",
-        "main_kernel_launches")]
+        "main_kernel_launches", "balanced_workers")]
 
     def to_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -107,7 +107,7 @@ def lib():
         L.starmm_madd.restype = ci
         L.starmm_atomic_accumulate.argtypes = [ci, vp, i64, vp, i64, i64, i64, vp, ci]
         L.starmm_atomic_accumulate.restype = ci
-        if L.starmm_abi_version() != 1:
+        if L.starmm_abi_version() != 2:
             raise errors.NativeUnavailable("libstarmm_b200.so ABI version mismatch")
         _lib = L
     return _lib

@@ -103,6 +103,11 @@ struct TaskGrid {
     int group_m;
     int num_tasks;
     long long kslice;      // k extent of one slice (multiple of the k-stage)
+    // balanced slices (TAR with uneven k-slices, "stream-K"): worker b runs the
+    // flattened (tile, k-stage) range [b*T/W, (b+1)*T/W) of T = tiles * kstages
+    // iterations; a tile split between workers is merged with the atomic-madd
+    int balanced;
+    long long kstages;     // k-stages per tile (balanced mode)
 };
 
 STARMM_DEV void decode_task(const TaskGrid& g, int t, int& tm, int& tn, int& s, int& tile) {

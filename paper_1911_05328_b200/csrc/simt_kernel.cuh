@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     const int ty = (warp >> 1) * 4 + (lane >> 3);      // 0..15
     const int tx = (warp & 1) * 8 + (lane & 7);        // 0..15
     const TaskGrid& g = p.g;
-    const int nk = (int)(g.kslice / BK);
     const Tp* Ap = reinterpret_cast<const Tp*>(p.Ap);
     const Tp* Bp = reinterpret_cast<const Tp*>(p.Bp);
     if constexpr (MB) {          // mbarrier ring (see dmma_fp64_kernel_mb); off by default:
@@ -261,15 +260,11 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     }
     long long gk = 0;
 
-    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
-        int tm, tn, s, tile;
-        decode_task(g, t, tm, tn, s, tile);
-        const int mode = task_mode(p.w, g, s);
-        int pair_seen = PAIR_EMPTY;
-        if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
-
+    // one output tile over k-stages [kst0, kst0 + nk) with write-back protocol `mode`
+    auto process = [&](int tm, int tn, int s, int tile, int mode, int pair_seen, long long kst0,
+                       int nk) {
         // k-group row kg of A covers Mp*G contiguous elements, of B (Np/OUTS)*G
-        const long long kg0 = (long long)s * g.kslice / KSTEP;
+        const long long kg0 = kst0 * KG;
         const long long Nw = p.Np / OUTS;
         const Tp* Ag = Ap + kg0 * p.Mp * G + (long long)tm * BM * G;
         const Tp* Bg = Bp + kg0 * Nw * G + (long long)tn * BNW * G;
@@ -374,6 +369,38 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                     }
                 }
         });
+    };
+
+    if (g.balanced) {
+        // Balanced slices (TAR with uneven k-slices): every worker gets the same number
+        // of k-stages of the flattened (tile, k-stage) space; whole tiles fold (or store)
+        // exclusively, pieces of a tile shared by workers merge with the atomic-madd.
+        TaskGrid g1 = g;
+        g1.S = 1; g1.log2S = 0;
+        const long long T = (long long)g.tiles_m * g.tiles_n * g.kstages;
+        long long it = T * blockIdx.x / gridDim.x;
+        const long long end = T * (blockIdx.x + 1) / gridDim.x;
+        while (it < end) {
+            const long long tl = it / g.kstages;
+            const long long ks = it - tl * g.kstages;
+            const long long ke = min(g.kstages, ks + (end - it));
+            int tm, tn, s0, tile;
+            decode_task(g1, (int)tl, tm, tn, s0, tile);
+            int mode = WB_RED;
+            if (ks == 0 && ke == g.kstages && p.w.remote_parts == 0)
+                mode = p.w.init_identity ? WB_STORE : WB_FOLD;
+            process(tm, tn, 0, tile, mode, PAIR_EMPTY, ks, (int)(ke - ks));
+            it += ke - ks;
+        }
+        return;
+    }
+    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
+        int tm, tn, s, tile;
+        decode_task(g, t, tm, tn, s, tile);
+        const int mode = task_mode(p.w, g, s);
+        int pair_seen = PAIR_EMPTY;
+        if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
+        process(tm, tn, s, tile, mode, pair_seen, (long long)s * g.kslice / BK, (int)(g.kslice / BK));
     }
 }
 

@@ -575,6 +575,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     bool is_dmma = false;
     PathShape shape;
     int BK = 0, TBM = 0, TBN = 0, per_sm = 1, gpu_workers = 0, s_log2 = 0, S = 1, tar_levels = 0;
+    bool balanced = false;
     long long tiles_m = 0, tiles_n = 0, tiles = 0, Mp = 0, Np = 0, Kp = 0, kslice = 0, ntasks = 0;
     TaskGrid g;
     auto plan_geometry = [&]() -> int {
@@ -584,6 +585,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
         tiles = tiles_m * tiles_n;
         gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
+        balanced = false;
         const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
         const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
         if (simt_path && (P->ksplit_req < 0 || !may_split)) {
@@ -612,6 +614,18 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
                     if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
                 }
+            }
+            // Balanced slices (TAR with uneven k-slices, "stream-K"): every worker gets the
+            // same share of the flattened (tile, k-stage) space, pieces of shared tiles merge
+            // with the atomic-madd.  Only for tar/star (their split write-back IS the
+            // atomic-madd) and exact, cheap atomics (int64 red.add, int32 red.min).
+            const char* benv = getenv("STARMM_NO_BALANCED");
+            if (may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
+                (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32) &&
+                P->remote_parts == 0 && !(benv && benv[0] == '1')) {
+                const double Gw = (double)P->sms * per_sm;
+                const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw * per_sm;
+                if (c < 0.97 * best) { balanced = true; best_occ = per_sm; best_s = 0; }
             }
             per_sm = best_occ;
             gpu_workers = P->sms * per_sm;
@@ -645,6 +659,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         // raster groups sized so one wave of resident CTAs covers a near-square block of
         // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
         g.group_m = is_dmma ? 24 : 12;
+        g.balanced = balanced ? 1 : 0;
+        g.kstages = Kp / std::max(1, BK);
         ntasks = tiles * S;
         if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
         g.num_tasks = (int)ntasks;
@@ -854,7 +870,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             }
             P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
         }
-        if (init_identity && S > 1 && P->algo != STARMM_CO3 && P->remote_parts == 0) {
+        if (init_identity && (S > 1 || balanced) && P->algo != STARMM_CO3 && P->remote_parts == 0) {
             if ((rc = fill_dispatch(P->sr, C, P->m, P->n, ldc, s))) break;
             ++launches;
         }
@@ -870,7 +886,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         w.remote_parts = P->remote_parts; w.remote_rows = P->remote_rows; w.remote_ld = P->remote_ld;
         for (int i = 0; i < 8; ++i) w.remote_base[i] = P->remote_base[i];
 
-        int grid = occupancy_grid(P, per_sm, ntasks);
+        int grid = occupancy_grid(P, per_sm, balanced ? ntasks * g.kstages : ntasks);
         const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
         if (timed) {
             if (!P->ev0) {
@@ -961,6 +977,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     P->st.tasks = ntasks;
     P->st.workers = std::min<long long>(ntasks, (long long)P->sms * per_sm);
     P->st.ksplit = S;
+    P->st.balanced_workers = balanced ? std::min<long long>(ntasks * g.kstages, (long long)P->sms * per_sm) : 0;
     P->st.tar_levels = tar_levels;
     P->st.kernel_launches = launches;
     P->st.path = path;

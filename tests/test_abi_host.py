@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_version_and_strerror():
     L = _lib.lib()
-    assert L.starmm_abi_version() == 1
+    assert L.starmm_abi_version() == 2
     assert L.starmm_strerror(0) == b"ok"
     assert L.starmm_strerror(2).startswith(b"InvalidSplit")
     assert L.starmm_strerror(1).startswith(b"DimMismatch")
