@@ -126,6 +126,40 @@ def test_integer_and_minplus_results_deterministic(sid, algo, ksplit):
         assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
 
 
+@pytest.mark.parametrize("sid", ["int", "tropical_i32"])
+@pytest.mark.parametrize("algo", ["tar", "star"])
+@pytest.mark.parametrize("store", [False, True])
+def test_balanced_slices_exact(sid, algo, store):
+    """Balanced (stream-K) k-slices: at n = 2560 (400 tiles = 1.35 waves of 296 CTAs)
+    the planner spreads the flattened (tile, k-stage) space evenly; tiles shared by
+    two CTAs merge with the atomic-madd.  Exact vs the oracle, with C folded or
+    overwritten (STARMM_F_INIT_IDENTITY), and identical bits with the mode disabled."""
+    n = 2560
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(33)
+    lo, hi = (0, 10 ** 5) if sid == "tropical_i32" else (-16, 17)
+    A = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    B = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    C0 = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    want = (np.full((n, n), O.I32_INF, np.int32) if sid == "tropical_i32" else
+            np.zeros((n, n), np.int64)) if store else C0.copy()
+    O.gemm_fold(SR_OF[sid], want, A, B, par=True)
+    outs = []
+    for disable in ("0", "1"):
+        os.environ["STARMM_NO_BALANCED"] = disable
+        try:
+            C = torch.from_numpy(C0.copy()).cuda()
+            with sm.Executor(sm.Config(base_dim=64, workers=148, allow_nonpow2=True)) as ex:
+                st = ex.execute(algo, C, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), s,
+                                flags=0x4 if store else 0)
+            assert (st["balanced_workers"] > 0) == (disable == "0"), st
+            outs.append(C.cpu().numpy())
+        finally:
+            del os.environ["STARMM_NO_BALANCED"]
+    assert np.array_equal(outs[0], want)
+    assert np.array_equal(outs[1], want)
+
+
 # ---- BASELINE config 1 (PR1) ----------------------------------------------
 def test_pr1_star_fp64_vs_reference():
     from bench_configs import make_inputs
