@@ -118,42 +118,41 @@ __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long
         if (kw < kp / 4 && r < rowsp) P[kw * rowsp + r] = tile[tx][i];
     }
 }
-// B (kdim x cols) -> P[kp/4][colsp]
+// B (kdim x cols) -> P[kp/4][colsp].  2-D grid (x: columns, y: k-words), no 64-bit
+// division per element (the grid-stride form spent 3x pack_a's time on it).
 __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
                                    int* P, long long colsp, long long kp, unsigned long long* range) {
     RangeAcc acc;
-    long long total = (kp / 4) * colsp;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long kw = idx / colsp, c = idx - kw * colsp;
-        unsigned w = 0;
+    for (long long kw = blockIdx.y; kw < kp / 4; kw += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < colsp;
+             c += (long long)gridDim.x * blockDim.x) {
+            unsigned w = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            long long k = kw * 4 + i;
-            long long v = (c < cols && k < kdim) ? B[k * ldb + c] : 0;
-            acc.add(v);
-            w |= ((unsigned)(v & 0xff)) << (8 * i);
+            for (int i = 0; i < 4; ++i) {
+                long long k = kw * 4 + i;
+                long long v = (c < cols && k < kdim) ? B[k * ldb + c] : 0;
+                acc.add(v);
+                w |= ((unsigned)(v & 0xff)) << (8 * i);
+            }
+            P[kw * colsp + c] = (int)w;
         }
-        P[idx] = (int)w;
-    }
-    if (range) acc.flush(range);
+    if (range) acc.flush(range);   // every thread reaches the flush (full-warp shuffles)
 }
 // (min,+) B (kdim x cols) -> P[kp][colsp/2] words (enc(B[k][2w]), enc(B[k][2w+1]))
 template <class T>
 __global__ void pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, long long ldb,
                                     unsigned* P, long long colsp, long long kp, unsigned long long* range) {
     RangeAcc acc;
-    long long wpr = colsp / 2;
-    long long total = kp * wpr;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long k = idx / wpr, w = idx - k * wpr;
-        long long c0 = 2 * w;
-        unsigned lo = 16383u, hi = 16383u;
-        if (k < kdim && c0 < cols) { T v = B[k * ldb + c0]; acc.add(v); lo = s16_enc<T>(v); }
-        if (k < kdim && c0 + 1 < cols) { T v = B[k * ldb + c0 + 1]; acc.add(v); hi = s16_enc<T>(v); }
-        P[idx] = lo | (hi << 16);
-    }
+    const long long wpr = colsp / 2;
+    for (long long k = blockIdx.y; k < kp; k += gridDim.y)      // 2-D grid, no division
+        for (long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x; w < wpr;
+             w += (long long)gridDim.x * blockDim.x) {
+            const long long c0 = 2 * w;
+            unsigned lo = 16383u, hi = 16383u;
+            if (k < kdim && c0 < cols) { T v = B[k * ldb + c0]; acc.add(v); lo = s16_enc<T>(v); }
+            if (k < kdim && c0 + 1 < cols) { T v = B[k * ldb + c0 + 1]; acc.add(v); hi = s16_enc<T>(v); }
+            P[k * wpr + w] = lo | (hi << 16);
+        }
     if (range) acc.flush(range);
 }
 
@@ -193,22 +192,21 @@ __global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long
                               Tp* P, long long colsp, long long kp, Tp pad,
                               unsigned long long* range = nullptr) {
     RangeAcc acc;
-    long long total = (kp / G) * colsp;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long kg = idx / colsp, c = idx - kg * colsp;
+    for (long long kg = blockIdx.y; kg < kp / G; kg += gridDim.y)   // 2-D grid, no division
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < colsp;
+             c += (long long)gridDim.x * blockDim.x) {
 #pragma unroll
-        for (int g = 0; g < G; ++g) {
-            long long k = kg * G + g;
-            Tp v = pad;
-            if (k < kdim && c < cols) {
-                Tin x = B[k * ldb + c];
-                acc.add(x);
-                v = (Tp)Conv::cvt(x);
+            for (int g = 0; g < G; ++g) {
+                long long k = kg * G + g;
+                Tp v = pad;
+                if (k < kdim && c < cols) {
+                    Tin x = B[k * ldb + c];
+                    acc.add(x);
+                    v = (Tp)Conv::cvt(x);
+                }
+                P[(kg * colsp + c) * G + g] = v;
             }
-            P[idx * G + g] = v;
         }
-    }
     if (range) acc.flush(range);
 }
 
@@ -219,40 +217,44 @@ __global__ void publish_range_kernel(const unsigned long long* d_range, unsigned
     __threadfence_system();
 }
 
+// 2-D grids (x: columns, y: rows, grid-stride in both) -- no 64-bit division per element
 template <class T>
 __global__ void pad_copy_kernel(const T* src, long long rows, long long cols, long long ld,
                                 T* dst, long long rp, long long cp) {
-    long long total = rp * cp;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cp, c = idx - r * cp;
-        dst[idx] = (r < rows && c < cols) ? src[r * ld + c] : (T)0;
-    }
+    for (long long r = blockIdx.y; r < rp; r += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cp;
+             c += (long long)gridDim.x * blockDim.x)
+            dst[r * cp + c] = (r < rows && c < cols) ? src[r * ld + c] : (T)0;
 }
 
 template <class Sr>
 __global__ void fill_kernel(typename Sr::T* C, long long rows, long long cols, long long ld) {
-    long long total = rows * cols;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cols, c = idx - r * cols;
-        C[r * ld + c] = Sr::identity();
-    }
+    for (long long r = blockIdx.y; r < rows; r += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+             c += (long long)gridDim.x * blockDim.x)
+            C[r * ld + c] = Sr::identity();
 }
 
 // C <- C (+) D.  atomic = 1 merges with the semiring's atomic-madd.
 template <class Sr>
 __global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr::T* D, long long ldd,
                             long long rows, long long cols, int atomic) {
-    long long total = rows * cols;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cols, c = idx - r * cols;
-        typename Sr::T d = D[r * ldd + c];
-        typename Sr::T* p = &C[r * ldc + c];
-        if (atomic) Sr::atomic_fold(p, d);
-        else *p = Sr::fold(*p, d);
-    }
+    for (long long r = blockIdx.y; r < rows; r += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+             c += (long long)gridDim.x * blockDim.x) {
+            typename Sr::T d = D[r * ldd + c];
+            typename Sr::T* p = &C[r * ldc + c];
+            if (atomic) Sr::atomic_fold(p, d);
+            else *p = Sr::fold(*p, d);
+        }
+}
+
+// launch shape for the 2-D elementwise kernels (x: 256-column blocks, y: rows, both
+// grid-strided): about 16 CTAs per SM in total, so each thread handles several rows
+inline dim3 grid2d(long long rows, long long cols) {
+    const long long bx = std::max<long long>(1, std::min<long long>((cols + 255) / 256, 64));
+    const long long by = std::max<long long>(1, std::min<long long>(rows, (148LL * 16 + bx - 1) / bx));
+    return dim3((unsigned)bx, (unsigned)by);
 }
 
 }  // namespace starmm
@@ -276,16 +278,15 @@ template <class T>
 __global__ void ring_combine_kernel(T* D, long long ldd, const T* X, long long ldx, const T* Y,
                                     long long ldy, long long rows, long long cols, int beta, int ax,
                                     int ay) {
-    long long total = rows * cols;
-    for (long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
-         idx += (long long)gridDim.x * blockDim.x) {
-        long long r = idx / cols, c = idx - r * cols;
-        T acc = beta ? D[r * ldd + c] : (T)0;
-        if (beta < 0) acc = ring_mac<T>((T)0, -1, acc);
-        if (ax) acc = ring_mac<T>(acc, ax, X[r * ldx + c]);
-        if (ay) acc = ring_mac<T>(acc, ay, Y[r * ldy + c]);
-        D[r * ldd + c] = acc;
-    }
+    for (long long r = blockIdx.y; r < rows; r += gridDim.y)
+        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
+             c += (long long)gridDim.x * blockDim.x) {
+            T acc = beta ? D[r * ldd + c] : (T)0;
+            if (beta < 0) acc = ring_mac<T>((T)0, -1, acc);
+            if (ax) acc = ring_mac<T>(acc, ax, X[r * ldx + c]);
+            if (ay) acc = ring_mac<T>(acc, ay, Y[r * ldy + c]);
+            D[r * ldd + c] = acc;
+        }
 }
 
 }  // namespace starmm

@@ -216,14 +216,13 @@ int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
     return STARMM_OK;
 }
 
-int grid_blocks(long long n) { return (int)std::min<long long>((n + 255) / 256, 148LL * 16); }
 
 template <class Sr>
 int launch_madd(void* C, long long ldc, const void* D, long long ldd, long long rows, long long cols,
                 int atomic, cudaStream_t s) {
     if (rows <= 0 || cols <= 0) return STARMM_OK;
     using T = typename Sr::T;
-    madd_kernel<Sr><<<grid_blocks(rows * cols), 256, 0, s>>>((T*)C, ldc, (const T*)D, ldd, rows, cols,
+    madd_kernel<Sr><<<grid2d(rows, cols), 256, 0, s>>>((T*)C, ldc, (const T*)D, ldd, rows, cols,
                                                            atomic);
     CK(cudaGetLastError());
     return STARMM_OK;
@@ -243,7 +242,7 @@ int madd_dispatch(int sr, void* C, long long ldc, const void* D, long long ldd, 
 
 template <class Sr>
 int launch_fill(void* C, long long rows, long long cols, long long ld, cudaStream_t s) {
-    fill_kernel<Sr><<<grid_blocks(rows * cols), 256, 0, s>>>((typename Sr::T*)C, rows, cols, ld);
+    fill_kernel<Sr><<<grid2d(rows, cols), 256, 0, s>>>((typename Sr::T*)C, rows, cols, ld);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -267,7 +266,7 @@ int launch_pack(const void* A, long long lda, const void* B, long long ldb, long
     pack_a_kernel<Tin, Tp, G, Conv><<<ga, dim3(32, 8), 0, s>>>((const Tin*)A, m, k, lda, (Tp*)Ap, Mp,
                                                               Kp, pad, range);
     CK(cudaGetLastError());
-    pack_b_kernel<Tin, Tp, G, Conv><<<grid_blocks((Kp / G) * Np), 256, 0, s>>>(
+    pack_b_kernel<Tin, Tp, G, Conv><<<grid2d(Kp / G, Np), 256, 0, s>>>(
         (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad, range);
     CK(cudaGetLastError());
     return STARMM_OK;
@@ -692,9 +691,9 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                 void *pa, *pb;
                 if ((rc = stage_acquire((size_t)(Mp * Kp * 8), &pa))) break;
                 if ((rc = stage_acquire((size_t)(Kp * Np * 8), &pb))) break;
-                pad_copy_kernel<double><<<grid_blocks(Mp * Kp), 256, 0, s>>>((const double*)A, P->m, P->k,
+                pad_copy_kernel<double><<<grid2d(Mp, Kp), 256, 0, s>>>((const double*)A, P->m, P->k,
                                                                             lda, (double*)pa, Mp, Kp);
-                pad_copy_kernel<double><<<grid_blocks(Kp * Np), 256, 0, s>>>((const double*)B, P->k, P->n,
+                pad_copy_kernel<double><<<grid2d(Kp, Np), 256, 0, s>>>((const double*)B, P->k, P->n,
                                                                             ldb, (double*)pb, Kp, Np);
                 if ((rc = cuda_status(cudaGetLastError()))) break;
                 launches += 2;
@@ -733,7 +732,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             case PATH_SIMT_I64_DP4A:
                 pack_a_s8x4_kernel<<<dim3((unsigned)((Kp / 4 + 31) / 32), (unsigned)(Mp / 32)), dim3(32, 8), 0, s>>>(
                     (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
-                pack_b_s8x4_kernel<<<grid_blocks((Kp / 4) * Np), 256, 0, s>>>(
+                pack_b_s8x4_kernel<<<grid2d(Kp / 4, Np), 256, 0, s>>>(
                     (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
@@ -767,17 +766,17 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                 if (path == PATH_SIMT_F64T_S16X2) {
                     pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                         (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<double><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                    pack_b_s16x2_kernel<double><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
                         (const double*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
                 } else if (path == PATH_SIMT_F32_S16X2) {
                     pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                         (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<float><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                    pack_b_s16x2_kernel<float><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
                         (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
                 } else {
                     pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                         (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<int><<<grid_blocks(Kp * Np / 2), 256, 0, s>>>(
+                    pack_b_s16x2_kernel<int><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
                         (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
                 }
                 rc = cuda_status(cudaGetLastError());
@@ -1027,7 +1026,7 @@ char* quad(const void* base, long long ld, int i, int j, long long h, size_t eb)
 
 int ring_combine(StrCtx& x, void* D, long long ldd, const void* X, long long ldx, const void* Y,
                  long long ldy, long long n, int beta, int ax, int ay) {
-    int blocks = grid_blocks(n * n);
+    const dim3 blocks = grid2d(n, n);
     if (x.P->sr == STARMM_SR_INT64)
         ring_combine_kernel<long long><<<blocks, 256, 0, x.s>>>((long long*)D, ldd, (const long long*)X,
                                                                ldx, (const long long*)Y, ldy, n, n,
