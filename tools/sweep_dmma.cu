@@ -49,5 +49,12 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2) {   // round-1 follow-up: k-stage depth vs stage count at the 2-CTA smem budget
+        run<DmmaCfg<64, 128, 2, 2, 20, 3, 2>, true>("mbar_64x128_bk20_s3", n, A, B, C, cnt, sms, 24, true);
+        run<DmmaCfg<64, 128, 2, 2, 12, 5, 2>, true>("mbar_64x128_bk12_s5", n, A, B, C, cnt, sms, 24, true);
+        run<DmmaCfg<64, 128, 2, 2, 8, 8, 2>, true>("mbar_64x128_bk8_s8", n, A, B, C, cnt, sms, 24, true);
+        run<P, true>("mbar_64x128_s4_g48", n, A, B, C, cnt, sms, 48, true);
+        run<P, true>("mbar_64x128_s4_g12", n, A, B, C, cnt, sms, 12, true);
+    }
     return 0;
 }
