@@ -124,6 +124,8 @@ struct starmm_plan {
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
     int last_guarded_path = 0;                  // optimistic first guess for the next execute
     int split_half_waves = 8;                   // auto k-split: grow s until tasks >= this many half waves
+    starmm_plan* twin = nullptr;                // host path: the second compute stream's plan
+                                                // (own arena: staging reuse is stream-ordered)
     long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
     long long str_issued = 0;                   // Strassen temporaries currently issued
     // peer destinations of the fused k-split combine (starmm_plan_set_peers)
@@ -492,6 +494,7 @@ void starmm_plan_destroy(starmm_plan* P) {
     if (P->ev0) cudaEventDestroy(P->ev0);
     if (P->ev1) cudaEventDestroy(P->ev1);
     if (P->h_range) cudaFreeHost((void*)P->h_range);
+    if (P->twin) starmm_plan_destroy(P->twin);
     P->arena.destroy();
     cudaSetDevice(prev);
     delete P;
@@ -1342,12 +1345,30 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const long long nblk = (m + R - 1) / R;
     const bool staged_c0 = nq > 0 && !user_init;    // phase 1 owns dC, C0 goes to a staging buffer
     cudaStream_t cs = (cudaStream_t)stream;
-    cudaStream_t up = nullptr, down = nullptr;
+    cudaStream_t up = nullptr, down = nullptr, cs2 = nullptr;
     CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
     CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    // Phase-2 row blocks alternate between two compute streams so that block i+1's CTAs
+    // fill the SMs block i's last partial wave leaves idle (each block is its own
+    // persistent launch).  The second stream runs on a twin plan with its own arena,
+    // because staging buffers are reused in stream order only.
+    const char* tsenv = getenv("STARMM_HOST_ONE_STREAM");
+    const bool two_streams = nblk > 1 && !(tsenv && tsenv[0] == '1');
+    if (two_streams) {
+        if (!P->twin) {
+            TRY(starmm_plan_create(&P->twin, P->sr, P->algo, P->alloc, P->m, P->n, P->k, P->base_dim,
+                                   P->workers, P->ksplit_req, P->device, P->flags));
+            P->twin->strassen_leaf = P->strassen_leaf;
+        }
+        P->twin->flags = P->flags;
+        P->twin->ksplit_req = P->ksplit_req;
+        CK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+    }
+    const starmm_stats twin_before = two_streams ? P->twin->st : starmm_stats{};
     std::vector<cudaEvent_t> ev_q(nq), ev_a(nblk), ev_c(nblk), ev_done(nblk);
-    cudaEvent_t ev_rest = nullptr;
+    cudaEvent_t ev_rest = nullptr, ev_p1 = nullptr;
     CK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_p1, cudaEventDisableTiming));
     for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
         for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     // STARMM_HOST_TRACE=1: timing events on the three streams, printed as one JSON line
@@ -1382,18 +1403,19 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const char* k2env = getenv("STARMM_HOST_KSPLIT2");   // phase-2 k-split override (tuning)
     const int ks2 = k2env ? atoi(k2env) : -2;
     const int saved_ks = P->ksplit_req;
-    auto run = [&](void* Cd, const void* Ad, const void* Bd, long long rows, long long kk, bool store) {
-        P->m = rows; P->k = kk;
+    auto run = [&](starmm_plan* Q, cudaStream_t st, void* Cd, const void* Ad, const void* Bd, long long rows,
+                   long long kk, bool store) {
+        Q->m = rows; Q->k = kk;
         // phase-2 row blocks are slices of a larger problem: split k only while the
         // tiles fill less than half a wave (k-split partials cost atomics -- CAS loops
         // for float minima -- which cost more than an idle fraction of one wave)
         if (kk == k - kq) {
-            P->split_half_waves = 1;
-            if (ks2 >= -1) P->ksplit_req = ks2;
+            Q->split_half_waves = 1;
+            if (ks2 >= -1) Q->ksplit_req = ks2;
         }
-        P->flags = store ? (saved_flags | STARMM_F_INIT_IDENTITY) : (saved_flags & ~STARMM_F_INIT_IDENTITY);
-        int r = execute_impl(P, Cd, n, Ad, k, Bd, n, cs, true);
-        P->m = m; P->k = k; P->flags = saved_flags; P->ksplit_req = saved_ks; P->split_half_waves = 8;
+        Q->flags = store ? (saved_flags | STARMM_F_INIT_IDENTITY) : (saved_flags & ~STARMM_F_INIT_IDENTITY);
+        int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true);
+        Q->m = m; Q->k = k; Q->flags = saved_flags; Q->ksplit_req = saved_ks; Q->split_half_waves = 8;
         return r;
     };
     do {
@@ -1435,28 +1457,36 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         for (int c = 0; c < nq && !rc; ++c) {
             const long long k0 = kb[c], k1 = kb[c + 1];
             if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_q[c], 0)))) break;
-            rc = run(dC, (char*)dA + k0 * eb, (char*)dB + k0 * n * eb, m, k1 - k0, c == 0);
+            rc = run(P, cs, dC, (char*)dA + k0 * eb, (char*)dB + k0 * n * eb, m, k1 - k0, c == 0);
             mark("mm_chunk" + std::to_string(c), cs);
         }
         if (rc) break;
         // ---- phase 2: row blocks over [kq, k), C0 fold, download ----
         if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_rest, 0)))) break;
+        if (two_streams) {
+            if ((rc = cuda_status(cudaEventRecord(ev_p1, cs)))) break;     // phase 1 + B resident
+            if ((rc = cuda_status(cudaStreamWaitEvent(cs2, ev_p1, 0)))) break;
+        }
         for (long long b = 0; b < nblk && !rc; ++b) {
             const long long r0 = b * R, rows = std::min(R, m - r0);
             char* Cb = (char*)dC + r0 * n * eb;
+            starmm_plan* Q = (two_streams && (b & 1)) ? P->twin : P;
+            cudaStream_t sb = (two_streams && (b & 1)) ? cs2 : cs;
+            // C0 is folded in BEFORE the block's tile kernel: a small kernel queued behind a
+            // persistent launch on the other stream would wait for that launch to end
+            if (staged_c0) {
+                if ((rc = cuda_status(cudaStreamWaitEvent(sb, ev_c[b], 0)))) break;
+                if ((rc = madd_dispatch(P->sr, Cb, n, (char*)dC0 + r0 * n * eb, n, rows, n, 0, sb))) break;
+            }
             if (kq < k) {
-                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_a[b], 0)))) break;
-                if (nq == 0 && (rc = cuda_status(cudaStreamWaitEvent(cs, ev_c[b], 0)))) break;
-                rc = run(Cb, (char*)dA + (r0 * k + kq) * eb, (char*)dB + kq * n * eb, rows, k - kq,
+                if ((rc = cuda_status(cudaStreamWaitEvent(sb, ev_a[b], 0)))) break;
+                if (nq == 0 && (rc = cuda_status(cudaStreamWaitEvent(sb, ev_c[b], 0)))) break;
+                rc = run(Q, sb, Cb, (char*)dA + (r0 * k + kq) * eb, (char*)dB + kq * n * eb, rows, k - kq,
                          nq == 0 && user_init);
                 if (rc) break;
-                mark("mm_blk" + std::to_string(b), cs);
+                mark("mm_blk" + std::to_string(b), sb);
             }
-            if (staged_c0) {
-                if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev_c[b], 0)))) break;
-                if ((rc = madd_dispatch(P->sr, Cb, n, (char*)dC0 + r0 * n * eb, n, rows, n, 0, cs))) break;
-            }
-            if ((rc = cuda_status(cudaEventRecord(ev_done[b], cs)))) break;
+            if ((rc = cuda_status(cudaEventRecord(ev_done[b], sb)))) break;
             if ((rc = cuda_status(cudaStreamWaitEvent(down, ev_done[b], 0)))) break;
             rc = cuda_status(cudaMemcpy2DAsync((char*)C + r0 * ldc * eb, ldc * eb, Cb, n * eb, n * eb, rows,
                                                cudaMemcpyDeviceToHost, down));
@@ -1464,12 +1494,21 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         }
         if (rc) break;
         if ((rc = cuda_status(cudaStreamSynchronize(down)))) break;
+        if (cs2 && (rc = cuda_status(cudaStreamSynchronize(cs2)))) break;
         rc = cuda_status(cudaStreamSynchronize(cs));
     } while (0);
+    if (two_streams) {   // the twin's executes and launches count as this plan's
+        const starmm_stats& t = P->twin->st;
+        P->st.executes += t.executes - twin_before.executes;
+        P->st.kernel_launches += t.kernel_launches;
+        P->st.main_kernel_ns += t.main_kernel_ns - twin_before.main_kernel_ns;
+        P->st.main_kernel_launches += t.main_kernel_launches - twin_before.main_kernel_launches;
+    }
     P->m = m; P->k = k; P->flags = saved_flags;
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(down);
     cudaStreamSynchronize(cs);
+    if (cs2) cudaStreamSynchronize(cs2);
     for (auto& t : trace) {
         float ms = 0;
         cudaEventElapsedTime(&ms, trace[0].second, t.second);
@@ -1481,6 +1520,8 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (dB && !same_ab) P->arena.release(dB, b_bytes);
     if (dA) P->arena.release(dA, a_bytes);
     cudaEventDestroy(ev_rest);
+    cudaEventDestroy(ev_p1);
+    if (cs2) cudaStreamDestroy(cs2);
     for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
         for (auto& e : *v) cudaEventDestroy(e);
     cudaStreamDestroy(up);
