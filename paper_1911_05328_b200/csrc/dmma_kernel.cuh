@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel(Dm
         cp_async_wait<0>();
         __syncthreads();
 
-        writeback<SrFp64, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
+        writeback<SrFp64, BM, BN, K::THREADS, 0>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                                   [&](auto f) {
 #pragma unroll
             for (int i = 0; i < MI; ++i)
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
         }
         gk += nk;
 
-        writeback<SrFp64, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
+        writeback<SrFp64, BM, BN, K::THREADS, 0>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                                   [&](auto f) {
 #pragma unroll
             for (int i = 0; i < MI; ++i)

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
             __syncthreads();
         }
         using T = typename Sr::T;
-        writeback<Sr, BM, BN>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
+        writeback<Sr, BM, BN, THREADS, 16>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                               [&](auto f) {
 #pragma unroll
             for (int i = 0; i < 8; ++i)

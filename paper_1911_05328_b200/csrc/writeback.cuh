@@ -24,9 +24,46 @@ STARMM_DEV int pair_arrive(const WbParams& w, const TaskGrid& g, int tile, int s
     return seen;
 }
 
-template <class Sr, int BM, int BN, class Each>
+// Read-fold-write of the calling thread's NE elements, CH at a time: all CH loads of a
+// chunk are issued before any store.  (Folding element by element, ptxas cannot hoist a
+// load above the previous element's store -- rows are ldc apart, ldc unknown -- so every
+// element paid a full HBM round trip: LDG DADD STG LDG DADD STG ... in the SASS.)
+template <class Sr, int NE, int CH, class Each, class Addr>
+STARMM_DEV void fold_batched(Each each, Addr addr, bool cg) {
+    using T = typename Sr::T;
+    static_assert(CH >= 1 && NE % CH == 0, "fold chunk");   // (FOLD_CH == 0 never gets here)
+#pragma unroll
+    for (int q = 0; q < NE / CH; ++q) {
+        T old[CH];
+        int idx = 0;
+        each([&](int r, int c, T v) {
+            if (idx / CH == q) {
+                T* p = addr(r, c);
+                old[idx % CH] = p ? (cg ? __ldcg(p) : *p) : v;
+            }
+            ++idx;
+        });
+        idx = 0;
+        each([&](int r, int c, T v) {
+            if (idx / CH == q) {
+                T* p = addr(r, c);
+                if (p) {
+                    T x = Sr::fold(old[idx % CH], v);
+                    if (cg) __stcg(p, x); else *p = x;
+                }
+            }
+            ++idx;
+        });
+    }
+}
+
+// FOLD_CH: elements per batched read-fold-write chunk; 0 = element by element (the DMMA
+// kernel: its epilogue is hidden by the co-resident CTA, and any change to this code
+// shifted its register allocation and cost 1-3% -- profiles/r01k_epilogue_ab.md)
+template <class Sr, int BM, int BN, int NTHREADS, int FOLD_CH, class Each>
 STARMM_DEV void writeback(const WbParams& w, const TaskGrid& g, int tm, int tn, int s, int tile,
                           int worker, int mode, int pair_seen, Each each) {
+    constexpr int NE = BM * BN / NTHREADS;     // elements per thread
     using T = typename Sr::T;
     const long long m0 = (long long)tm * BM, n0 = (long long)tn * BN;
     T* C = reinterpret_cast<T*>(w.C);
@@ -47,13 +84,20 @@ STARMM_DEV void writeback(const WbParams& w, const TaskGrid& g, int tm, int tn, 
         return;
     }
     if (mode == WB_FOLD) {
-        each([&](int r, int c, T v) {
-            long long gr = m0 + r, gc = n0 + c;
-            if (gr < M && gc < N) {
-                T* p = &C[gr * ldc + gc];
-                *p = Sr::fold(*p, v);
-            }
-        });
+        if constexpr (FOLD_CH == 0) {
+            each([&](int r, int c, T v) {
+                long long gr = m0 + r, gc = n0 + c;
+                if (gr < M && gc < N) {
+                    T* p = &C[gr * ldc + gc];
+                    *p = Sr::fold(*p, v);
+                }
+            });
+        } else {
+            fold_batched<Sr, NE, FOLD_CH>(each, [&](int r, int c) -> T* {
+                long long gr = m0 + r, gc = n0 + c;
+                return (gr < M && gc < N) ? &C[gr * ldc + gc] : nullptr;
+            }, false);
+        }
         return;
     }
     const long long tile_bytes = (long long)BM * BN * (long long)sizeof(T);
@@ -100,14 +144,28 @@ STARMM_DEV void writeback(const WbParams& w, const TaskGrid& g, int tm, int tn, 
     __syncthreads();
     if (threadIdx.x == 0) lock_slot(&w.slots[tile]);
     __syncthreads();
-    each([&](int r, int c, T v) {
-        long long gr = m0 + r, gc = n0 + c;
-        if (lazy) v = __ldcg(&tmp[r * BN + c]);
-        if (gr < M && gc < N) {
-            T* p = &C[gr * ldc + gc];
-            __stcg(p, Sr::fold(__ldcg(p), v));
+    auto fold_each = [&]() {
+        each([&](int r, int c, T v) {
+            long long gr = m0 + r, gc = n0 + c;
+            if (lazy) v = __ldcg(&tmp[r * BN + c]);
+            if (gr < M && gc < N) {
+                T* p = &C[gr * ldc + gc];
+                __stcg(p, Sr::fold(__ldcg(p), v));
+            }
+        });
+    };
+    if constexpr (FOLD_CH == 0) {
+        fold_each();
+    } else {
+        if (lazy) {
+            fold_each();
+        } else {
+            fold_batched<Sr, NE, FOLD_CH>(each, [&](int r, int c) -> T* {
+                long long gr = m0 + r, gc = n0 + c;
+                return (gr < M && gc < N) ? &C[gr * ldc + gc] : nullptr;
+            }, true);
         }
-    });
+    }
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) {
