@@ -21,5 +21,9 @@ for c in $CFGS; do
   $B2 > /dev/null 2>&1 || exit 3
   ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
       -o gpurun_out/${TAG}_prof_c$c $B2 > gpurun_out/${TAG}_ncu_c$c.log 2>&1 || exit 4
+  # raw page as CSV (what tools/summarize_ncu.py reads); the 12-16 MB report only with KEEP_REP=1
+  ncu -i gpurun_out/${TAG}_prof_c$c.ncu-rep --page raw --csv > gpurun_out/${TAG}_prof_c$c.raw.csv 2>/dev/null
+  ncu -i gpurun_out/${TAG}_prof_c$c.ncu-rep --page details --csv > gpurun_out/${TAG}_prof_c$c.details.csv 2>/dev/null
+  [ "$KEEP_REP" = "1" ] || rm -f gpurun_out/${TAG}_prof_c$c.ncu-rep
 done
 echo done

@@ -59,8 +59,14 @@ def launches(path):
 
 
 def raw(rep):
-    txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                         text=True).stdout
+    # a raw-page CSV exported on the GPU box (tools/ncu_capture.sh, keeps gpurun_out/ under
+    # the 64 MiB copy-back limit) is used when present, else the .ncu-rep itself
+    csv_path = rep.replace(".ncu-rep", ".raw.csv")
+    if os.path.exists(csv_path):
+        txt = open(csv_path).read()
+    else:
+        txt = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                             text=True).stdout
     rows = list(csv.reader(io.StringIO(txt)))
     h, u, v = rows[0], rows[1], rows[2]
     d = {h[i]: (v[i], u[i]) for i in range(len(h))}
