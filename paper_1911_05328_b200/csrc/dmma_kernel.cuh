@@ -210,7 +210,10 @@ STARMM_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
         "@!p bra WAIT_%=;\n\t}\n" ::"r"(a), "r"(parity) : "memory");
 }
 
-template <class K>
+// EPI = 1: the exclusive FOLD write-back reads its 2-double fragment pairs as 16-byte
+// vectors, a whole fragment row (NJ pairs) in flight before any store (EPI = 0: the
+// generic element-by-element writeback).  Other protocols always use the generic one.
+template <class K, int EPI = 0>
 __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb(DmmaParams p) {
     constexpr int BM = K::BM, BN = K::BN, BK = K::BK, STAGES = K::STAGES;
     constexpr int A_LD = K::A_LD, B_LD = K::B_LD, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
@@ -302,6 +305,25 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
         }
         gk += nk;
 
+        if constexpr (EPI == 1) {
+            const long long m0 = (long long)tm * BM, n0 = (long long)tn * BN;
+            if (mode == WB_FOLD && m0 + BM <= p.w.M && n0 + BN <= p.w.N && (p.w.ldc & 1) == 0 &&
+                (reinterpret_cast<uintptr_t>(p.w.C) & 15) == 0) {
+                double* C = reinterpret_cast<double*>(p.w.C);
+#pragma unroll
+                for (int i = 0; i < MI; ++i) {
+                    const long long r = m0 + wm * K::WTM + i * 8 + gi;
+                    double2* row = reinterpret_cast<double2*>(C + r * p.w.ldc + n0 + wn * K::WTN + ti * 2);
+                    double2 old[NJ];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j) old[j] = row[j * 4];
+#pragma unroll
+                    for (int j = 0; j < NJ; ++j)
+                        row[j * 4] = make_double2(old[j].x + acc[i][j][0], old[j].y + acc[i][j][1]);
+                }
+                continue;
+            }
+        }
         writeback<SrFp64, BM, BN, K::THREADS, 0>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                                   [&](auto f) {
 #pragma unroll

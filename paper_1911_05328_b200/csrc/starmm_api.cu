@@ -207,13 +207,13 @@ int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
     using K = DmmaProd;
     static bool attr_done = false;
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 K::SMEM_BYTES));
         attr_done = true;
     }
     // mbarrier-pipelined k-loop (tools/sweep_dmma.cu: 35.4 vs 34.4 TF/s with per-stage
     // __syncthreads)
-    dmma_fp64_kernel_mb<K><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
+    dmma_fp64_kernel_mb<K, 1><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
     CK(cudaGetLastError());
     return STARMM_OK;
 }

@@ -7,7 +7,7 @@
 #include "../paper_1911_05328_b200/csrc/dmma_kernel.cuh"
 using namespace starmm;
 
-template <class K, bool MB = false>
+template <class K, bool MB = false, int EPI = 0>
 void run(const char* name, int n, double* A, double* B, double* C, unsigned long long* cnt, int sms,
          int group_m = 8, bool persistent = true) {
     DmmaParams p{};
@@ -18,7 +18,7 @@ void run(const char* name, int n, double* A, double* B, double* C, unsigned long
     WbParams& w = p.w;
     w.mode_base = 0; w.init_identity = 0; w.C = C; w.ldc = n; w.M = n; w.N = n;
     w.counters = cnt;
-    auto kern = MB ? dmma_fp64_kernel_mb<K> : dmma_fp64_kernel<K>;
+    auto kern = MB ? dmma_fp64_kernel_mb<K, EPI> : dmma_fp64_kernel<K>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K::THREADS, K::SMEM_BYTES);
@@ -49,6 +49,13 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'e') {   // epilogue A/B: generic vs vectorised batched FOLD
+        for (int rep = 0; rep < 2; ++rep) {
+            run<P, true, 0>("mbar_64x128_s4_epi0", n, A, B, C, cnt, sms, 24, true);
+            run<P, true, 1>("mbar_64x128_s4_epi1", n, A, B, C, cnt, sms, 24, true);
+        }
+        return 0;
+    }
     if (argc > 2) {   // round-1 follow-up: k-stage depth vs stage count at the 2-CTA smem budget
         run<DmmaCfg<64, 128, 2, 2, 20, 3, 2>, true>("mbar_64x128_bk20_s3", n, A, B, C, cnt, sms, 24, true);
         run<DmmaCfg<64, 128, 2, 2, 12, 5, 2>, true>("mbar_64x128_bk12_s5", n, A, B, C, cnt, sms, 24, true);
