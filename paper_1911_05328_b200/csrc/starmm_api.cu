@@ -1307,7 +1307,9 @@ static int host_phase1_chunks(long long m, long long n, long long k, int sr, dou
     if ((env && env[0] == '0') || m < 512 || k < 512) return 0;
     const double t_mm = 2.0 * (double)m * (double)n * (double)k / host_nominal_ops(sr);
     if (!(env && env[0] == '1') && t_mm < h2d_bytes / 50e9) return 0;
-    long long w = std::max<long long>(128, round_up((k + 31) / 32, 128)), sum = 0;
+    // first chunk k/64 (k >= 8192) or k/32: its upload is the exposed head of the schedule
+    const long long div = k >= 8192 ? 64 : 32;
+    long long w = std::max<long long>(128, round_up((k + div - 1) / div, 128)), sum = 0;
     while (sum + w <= k / 2) {
         sum += w;
         kb.push_back(sum);
@@ -1342,7 +1344,16 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     long long R = block_rows > 0 ? block_rows
                                  : std::max<long long>(128, round_up((m + auto_blocks - 1) / auto_blocks, 128));
     R = std::min(R, m);
-    const long long nblk = (m + R - 1) / R;
+    // row-block starts; with the automatic size the last block is cut in quarters so the
+    // download after the final kernel (the exposed tail) is a quarter block
+    std::vector<long long> bst;
+    for (long long r = 0; r < m; r += R) bst.push_back(r);
+    if (block_rows <= 0 && bst.size() >= 4 && R >= 512) {
+        const long long last = bst.back(), q = round_up((m - last + 3) / 4, 128);
+        for (long long r = last + q; r < m; r += q) bst.push_back(r);
+    }
+    bst.push_back(m);
+    const long long nblk = (long long)bst.size() - 1;
     const bool staged_c0 = nq > 0 && !user_init;    // phase 1 owns dC, C0 goes to a staging buffer
     cudaStream_t cs = (cudaStream_t)stream;
     cudaStream_t up = nullptr, down = nullptr, cs2 = nullptr;
@@ -1444,7 +1455,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if (!rc) rc = cuda_status(cudaEventRecord(ev_rest, up));
         mark("up_rest", up);
         for (long long b = 0; b < nblk && !rc; ++b) {
-            const long long r0 = b * R, rows = std::min(R, m - r0);
+            const long long r0 = bst[b], rows = bst[b + 1] - bst[b];
             if (!same_ab) rc = up_block(dA, k, A, lda, r0, kq, rows, k - kq);      // A[blk, kq:]
             if (!rc) rc = cuda_status(cudaEventRecord(ev_a[b], up));
             mark("up_a" + std::to_string(b), up);
@@ -1468,7 +1479,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             if ((rc = cuda_status(cudaStreamWaitEvent(cs2, ev_p1, 0)))) break;
         }
         for (long long b = 0; b < nblk && !rc; ++b) {
-            const long long r0 = b * R, rows = std::min(R, m - r0);
+            const long long r0 = bst[b], rows = bst[b + 1] - bst[b];
             char* Cb = (char*)dC + r0 * n * eb;
             starmm_plan* Q = (two_streams && (b & 1)) ? P->twin : P;
             cudaStream_t sb = (two_streams && (b & 1)) ? cs2 : cs;
