@@ -1321,6 +1321,9 @@ static int host_phase1_chunks(long long m, long long n, long long k, int sr, dou
 int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* stream, int64_t block_rows) {
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
+    // classical schedules only (the Strassen family overwrites C; host_mm checks the same),
+    // and no fused peer combine (its owners' rows live on other GPUs, not in host C)
+    if (P->algo >= STARMM_STRASSEN || P->remote_parts > 0) return STARMM_CONTRACT_VIOLATION;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
     int prev_dev = 0;
     CK(cudaGetDevice(&prev_dev));

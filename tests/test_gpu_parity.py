@@ -738,6 +738,17 @@ def test_abi_error_paths():
     with pytest.raises(sm.ContractViolation):     # NULL operand
         plan.execute(0, 64, t.data_ptr(), 64, t.data_ptr(), 64, stream)
     plan.close()
+    # the host path: classical schedules only, and not with a fused peer combine
+    h = torch.zeros(64, 64, dtype=torch.float64).pin_memory()
+    sp = _lib.Plan(s.sr_id, "strassen", "pooled", 64, 64, 64, 8, 1, -1, 0, 0)
+    with pytest.raises(sm.ContractViolation):
+        sp.execute_host(h.data_ptr(), 64, h.data_ptr(), 64, h.data_ptr(), 64, stream)
+    sp.close()
+    pp = _lib.Plan(s.sr_id, "tar", "pooled", 64, 64, 64, 8, 1, -1, 0, 0)
+    pp.set_peers([t.data_ptr()], 64, 64)
+    with pytest.raises(sm.ContractViolation):
+        pp.execute_host(h.data_ptr(), 64, h.data_ptr(), 64, h.data_ptr(), 64, stream)
+    pp.close()
 
 
 def test_int64_extreme_values_wrap():
