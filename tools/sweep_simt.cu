@@ -32,6 +32,12 @@ void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long lon
     fflush(stdout);
 }
 
+// dp4a policy variants (k-stage depth)
+struct PolI8Dp4aBK128 : PolI8Dp4a { static constexpr int BK = 128; };
+struct PolI8Dp4aBK32 : PolI8Dp4a { static constexpr int BK = 32; };
+template <> struct starmm::Finish<PolI8Dp4aBK128, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
+template <> struct starmm::Finish<PolI8Dp4aBK32, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
+
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 8192;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -39,6 +45,14 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
+    if (argc > 2 && argv[2][0] == 'd') {   // dp4a k-stage depth
+        for (int rep = 0; rep < 2; ++rep) {
+            run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_bk64_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aBK128, SrInt64, 2, false>("i64_dp4a_bk128_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aBK32, SrInt64, 2, false>("i64_dp4a_bk32_occ2", n, A, B, C, cnt, sms);
+        }
+        return 0;
+    }
     run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1", n, A, B, C, cnt, sms);
     run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_occ2", n, A, B, C, cnt, sms);
     run<PolS16x2Min, SrTropF32, 1, false>("minplus_s16x2_occ1", n, A, B, C, cnt, sms);
