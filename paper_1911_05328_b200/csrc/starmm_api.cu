@@ -123,7 +123,6 @@ struct starmm_plan {
     long long raw_count = 0, raw_bytes = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
     int last_guarded_path = 0;                  // optimistic first guess for the next execute
-    int split_half_waves = 8;                   // auto k-split: grow s until tasks >= this many half waves
     starmm_plan* twin = nullptr;                // host path: the second compute stream's plan
                                                 // (own arena: staging reuse is stream-ordered)
     long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
@@ -590,7 +589,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         balanced = false;
         const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
         const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
-        if (simt_path && (P->ksplit_req < 0 || !may_split)) {
+        if ((simt_path || is_dmma) && (P->ksplit_req < 0 || !may_split)) {
             // CUDA-core paths: pick (CTAs per SM, split depth) by a wave cost model
             //   time ~ ceil(tasks / CTAs) * (stages per task + overhead) / per-CTA rate
             // overhead = 4.5 stages of prologue/epilogue per task, plus the split write-back
@@ -599,7 +598,25 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             // full SM (tools/ksplit_ab.py, profiles/r01i_ksplit_c2.json).  Small problems
             // such as config 2 (1024 tiles = 3.46 waves of 296 CTAs) then prefer one CTA
             // per SM (co2: +5.5%) or a split to two.  co2 never splits (classic.py:125-128).
+            // The split write-back's cost depends on the schedule's protocol (tools/ksplit_ab.py,
+            // profiles/r01k_ksplit_*.json; DMMA n=2048: S=2/4 cost +6%/+1.6% for tar -- which the
+            // model reproduces -- and +30%/+48% for sar): TAR atomic-madd 2 stages (20 for the CAS
+            // of float minima), CO3 workspace + merge 3, SAR pair states + locks + lazy
+            // temporaries 60 on DMMA (the sibling folds serialise under the tile lock; n=1024:
+            // +40% at S=2) and 6 on the CUDA-core paths (2-4x longer stages, batched folds);
+            // STAR levels above switch_depth are TAR, deeper ones SAR.  The DMMA path always
+            // runs two CTAs per SM.
             const bool cas_min = P->sr == STARMM_SR_TROPICAL_F32 || P->sr == STARMM_SR_TROPICAL_F64;
+            const double pen_tar = cas_min ? 20.0 : 2.0, pen_sar = is_dmma ? 60.0 : 6.0;
+            auto split_pen = [&](int sl) -> double {
+                if (sl == 0) return 0.0;
+                switch (P->algo) {
+                case STARMM_TAR: return pen_tar;
+                case STARMM_CO3: return 3.0;
+                case STARMM_SAR: return pen_sar;
+                default: return sl <= switch_depth(P->workers) ? pen_tar : pen_sar;   // star
+                }
+            };
             const double kst = (double)round_up(P->k, BK) / BK;
             int smax = 0;
             if (may_split)
@@ -608,11 +625,11 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     ++smax;
             double best = 0;
             int best_occ = per_sm, best_s = 0;
-            for (int occ = per_sm; occ >= 1; --occ) {
+            for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
                 const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : 0.89) : 1.0 / occ;
                 for (int sl = 0; sl <= smax; ++sl) {
                     const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
-                    const double ovh = 4.5 + (sl == 0 ? 0.0 : (cas_min ? 20.0 : 2.0));
+                    const double ovh = 4.5 + split_pen(sl);
                     const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
                     if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
                 }
@@ -622,7 +639,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             // with the atomic-madd.  Only for tar/star (their split write-back IS the
             // atomic-madd) and exact, cheap atomics (int64 red.add, int32 red.min).
             const char* benv = getenv("STARMM_NO_BALANCED");
-            if (may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
+            if (simt_path && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
                 (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32) &&
                 P->remote_parts == 0 && !(benv && benv[0] == '1')) {
                 const double Gw = (double)P->sms * per_sm;
@@ -638,12 +655,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         } else if (P->ksplit_req >= 0) {
             s_log2 = P->ksplit_req;
         } else {
-            // Work-first, like the reference's work-stealing runtime: sibling k-halves only
-            // run concurrently when the output tiles alone cannot keep every persistent CTA
-            // busy for several waves; otherwise each worker runs its tile's k range serially
-            // (the in-place, temporary-free order of serial TAR/SAR).
+            // (the opt-in tcgen05 paths never reach here: they keep whole-K tiles)
             s_log2 = 0;
-            while (2 * (tiles << s_log2) < (long long)P->split_half_waves * gpu_workers) ++s_log2;
         }
         // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels
         // than the recursion has (log2(k / b))
@@ -1420,16 +1433,10 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     auto run = [&](starmm_plan* Q, cudaStream_t st, void* Cd, const void* Ad, const void* Bd, long long rows,
                    long long kk, bool store) {
         Q->m = rows; Q->k = kk;
-        // phase-2 row blocks are slices of a larger problem: split k only while the
-        // tiles fill less than half a wave (k-split partials cost atomics -- CAS loops
-        // for float minima -- which cost more than an idle fraction of one wave)
-        if (kk == k - kq) {
-            Q->split_half_waves = 1;
-            if (ks2 >= -1) Q->ksplit_req = ks2;
-        }
+        if (kk == k - kq && ks2 >= -1) Q->ksplit_req = ks2;   // phase-2 split override (tuning)
         Q->flags = store ? (saved_flags | STARMM_F_INIT_IDENTITY) : (saved_flags & ~STARMM_F_INIT_IDENTITY);
         int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true);
-        Q->m = m; Q->k = k; Q->flags = saved_flags; Q->ksplit_req = saved_ks; Q->split_half_waves = 8;
+        Q->m = m; Q->k = k; Q->flags = saved_flags; Q->ksplit_req = saved_ks;
         return r;
     };
     do {

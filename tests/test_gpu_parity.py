@@ -160,6 +160,38 @@ def test_balanced_slices_exact(sid, algo, store):
     assert np.array_equal(outs[1], want)
 
 
+@pytest.mark.parametrize("sid", ["float", "int"])
+def test_spec_soft_throughput_gate(sid):
+    """SPEC.md:568's soft gate on the schedules, GPU analogue: at n = 2048, b = 64 and
+    >= 8 workers, TAR <= 1.15 x CO2 and SAR <= 1.15 x CO3 (median of 7 timed runs)."""
+    n = 2048
+    s = sm.get_semiring(sid)
+    g = torch.Generator(device="cuda").manual_seed(5)
+    if sid == "float":
+        A = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+        B = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    else:
+        A = torch.randint(-16, 17, (n, n), dtype=torch.int64, device="cuda", generator=g)
+        B = torch.randint(-16, 17, (n, n), dtype=torch.int64, device="cuda", generator=g)
+    med = {}
+    with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
+        for algo in ("co2", "co3", "tar", "sar"):
+            C = sm.Matrix(torch.zeros(n, n, dtype=s.torch_dtype, device="cuda"), s)
+            Am, Bm = sm.Matrix(A, s), sm.Matrix(B, s)
+            ts = []
+            for it in range(9):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record()
+                sm.run_algorithm(ex, algo, C, Am, Bm, s)
+                e1.record()
+                torch.cuda.synchronize()
+                if it >= 2:
+                    ts.append(e0.elapsed_time(e1))
+            med[algo] = sorted(ts)[len(ts) // 2]
+    assert med["tar"] <= 1.15 * med["co2"], med
+    assert med["sar"] <= 1.15 * med["co3"], med
+
+
 # ---- BASELINE config 1 (PR1) ----------------------------------------------
 def test_pr1_star_fp64_vs_reference():
     from bench_configs import make_inputs

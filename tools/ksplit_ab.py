@@ -6,15 +6,18 @@ import paper_1911_05328_b200 as sm
 sid, n = sys.argv[1], int(sys.argv[2])
 s = sm.get_semiring(sid)
 g = torch.Generator(device="cuda"); g.manual_seed(1)
-if sid == "int":
+if sid == "float":
+    A = torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)
+    B = torch.randn(n, n, generator=g, device="cuda", dtype=torch.float64)
+elif sid == "int":
     A = torch.randint(-16, 17, (n, n), generator=g, device="cuda", dtype=torch.int64)
     B = torch.randint(-16, 17, (n, n), generator=g, device="cuda", dtype=torch.int64)
 else:
     A = torch.randint(1, 101, (n, n), generator=g, device="cuda").to(s.torch_dtype)
     B = torch.randint(1, 101, (n, n), generator=g, device="cuda").to(s.torch_dtype)
 res = {}
-for algo in ("co2", "star", "tar"):
-    for ks in ((None,) if algo == "co2" else (0, 1, 2, None)):
+for algo in (sys.argv[3].split(",") if len(sys.argv) > 3 else ("co2", "star", "tar")):
+    for ks in ((None,) if algo == "co2" else (0, 1, 2, 3, None)):
         C = torch.zeros(n, n, dtype=s.torch_dtype, device="cuda")
         with sm.Executor(sm.Config(base_dim=64, workers=148, ksplit=ks)) as ex:
             M, Am, Bm = sm.Matrix(C, s), sm.Matrix(A, s), sm.Matrix(B, s)
