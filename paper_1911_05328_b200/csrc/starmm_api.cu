@@ -1338,9 +1338,32 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     // and no fused peer combine (its owners' rows live on other GPUs, not in host C)
     if (P->algo >= STARMM_STRASSEN || P->remote_parts > 0) return STARMM_CONTRACT_VIOLATION;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
-    int prev_dev = 0;
-    CK(cudaGetDevice(&prev_dev));
-    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
+    // streams / events / the caller's device are released or restored on every return path
+    struct HostRes {
+        std::vector<cudaStream_t> streams;
+        std::vector<cudaEvent_t> events;
+        int prev_dev = -1, dev = -1;
+        ~HostRes() {
+            for (auto x : streams) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+            for (auto x : events) cudaEventDestroy(x);
+            if (prev_dev >= 0 && prev_dev != dev) cudaSetDevice(prev_dev);
+        }
+        int stream(cudaStream_t* out) {
+            cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+            if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
+            streams.push_back(*out);
+            return STARMM_OK;
+        }
+        int event(cudaEvent_t* out) {
+            cudaError_t e = cudaEventCreateWithFlags(out, cudaEventDisableTiming);
+            if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
+            events.push_back(*out);
+            return STARMM_OK;
+        }
+    } res;
+    CK(cudaGetDevice(&res.prev_dev));
+    res.dev = P->device;
+    if (res.prev_dev != P->device) CK(cudaSetDevice(P->device));
     const size_t eb = (size_t)elem_bytes(P->sr);
     const long long m = P->m, n = P->n, k = P->k;
     const int saved_flags = P->flags;
@@ -1373,8 +1396,8 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const bool staged_c0 = nq > 0 && !user_init;    // phase 1 owns dC, C0 goes to a staging buffer
     cudaStream_t cs = (cudaStream_t)stream;
     cudaStream_t up = nullptr, down = nullptr, cs2 = nullptr;
-    CK(cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking));
-    CK(cudaStreamCreateWithFlags(&down, cudaStreamNonBlocking));
+    TRY(res.stream(&up));
+    TRY(res.stream(&down));
     // Phase-2 row blocks alternate between two compute streams so that block i+1's CTAs
     // fill the SMs block i's last partial wave leaves idle (each block is its own
     // persistent launch).  The second stream runs on a twin plan with its own arena,
@@ -1389,15 +1412,15 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         }
         P->twin->flags = P->flags;
         P->twin->ksplit_req = P->ksplit_req;
-        CK(cudaStreamCreateWithFlags(&cs2, cudaStreamNonBlocking));
+        TRY(res.stream(&cs2));
     }
     const starmm_stats twin_before = two_streams ? P->twin->st : starmm_stats{};
     std::vector<cudaEvent_t> ev_q(nq), ev_a(nblk), ev_c(nblk), ev_done(nblk);
     cudaEvent_t ev_rest = nullptr, ev_p1 = nullptr;
-    CK(cudaEventCreateWithFlags(&ev_rest, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_p1, cudaEventDisableTiming));
+    TRY(res.event(&ev_rest));
+    TRY(res.event(&ev_p1));
     for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
-        for (auto& e : *v) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        for (auto& e : *v) TRY(res.event(&e));
     // STARMM_HOST_TRACE=1: timing events on the three streams, printed as one JSON line
     // per event to stderr (label, ms since the start) -- the schedule's timeline
     const char* tenv = getenv("STARMM_HOST_TRACE");
@@ -1526,7 +1549,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         P->st.main_kernel_launches += t.main_kernel_launches - twin_before.main_kernel_launches;
     }
     P->m = m; P->k = k; P->flags = saved_flags;
-    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(up);       // nothing may still read or write the arena blocks
     cudaStreamSynchronize(down);
     cudaStreamSynchronize(cs);
     if (cs2) cudaStreamSynchronize(cs2);
@@ -1540,14 +1563,6 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (dC) P->arena.release(dC, c_bytes);
     if (dB && !same_ab) P->arena.release(dB, b_bytes);
     if (dA) P->arena.release(dA, a_bytes);
-    cudaEventDestroy(ev_rest);
-    cudaEventDestroy(ev_p1);
-    if (cs2) cudaStreamDestroy(cs2);
-    for (auto* v : {&ev_q, &ev_a, &ev_c, &ev_done})
-        for (auto& e : *v) cudaEventDestroy(e);
-    cudaStreamDestroy(up);
-    cudaStreamDestroy(down);
-    if (prev_dev != P->device) cudaSetDevice(prev_dev);
     return rc;
 }
 
