@@ -15,6 +15,7 @@
 #include <cstring>
 #include <map>
 #include <vector>
+#include <type_traits>
 #include <string>
 #include <algorithm>
 #include <cmath>
@@ -188,10 +189,28 @@ PathShape path_shape(int path) {
     return simt_shape<PolI64>();
 }
 
+// Policies that also ship a one-CTA-per-SM build (register budget 255 instead of 128):
+// the planner's occupancy-1 choice then runs at 0.97 of a full SM instead of 0.89
+// (tools/sweep_simt.cu; config 2 = 1024 tiles, 6.9 waves of 148 CTAs).
+template <class Pol> constexpr bool has_occ1_build() { return std::is_same<Pol, PolI8Dp4a>::value; }
+
 template <class Pol, class Sr>
-int launch_simt(const SimtParams& p, int grid, cudaStream_t s) {
-    auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
+int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
     constexpr int smem = simt::smem_bytes<Pol>();
+    if constexpr (has_occ1_build<Pol>() && Pol::OCC > 1) {
+        if (grid <= sms) {
+            auto k1 = simt_mm_kernel<Pol, Sr, 1>;
+            static bool attr1 = false;
+            if (!attr1) {
+                CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+                attr1 = true;
+            }
+            k1<<<grid, simt::THREADS, smem, s>>>(p);
+            CK(cudaGetLastError());
+            return STARMM_OK;
+        }
+    }
+    auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
     static bool attr_done = false;
     if (!attr_done) {
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -626,7 +645,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             double best = 0;
             int best_occ = per_sm, best_s = 0;
             for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
-                const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : 0.89) : 1.0 / occ;
+                const double rate1 = path == PATH_SIMT_I64_DP4A ? 0.97 : 0.89;   // has_occ1_build
+                const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
                 for (int sl = 0; sl <= smax; ++sl) {
                     const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
                     const double ovh = 4.5 + split_pen(sl);
@@ -936,18 +956,18 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             SimtParams sp;
             sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = g; sp.w = w;
             switch (path) {
-            case PATH_SIMT_F32_PAIR: rc = launch_simt<PolF32Pair, SrTropF32>(sp, grid, s); break;
-            case PATH_SIMT_I32_CARRIER: rc = launch_simt<PolF32Pair, SrTropI32>(sp, grid, s); break;
-            case PATH_SIMT_I32_VMIN: rc = launch_simt<PolI32Vmin, SrTropI32>(sp, grid, s); break;
-            case PATH_SIMT_I32_SAT: rc = launch_simt<PolI32Sat, SrTropI32>(sp, grid, s); break;
-            case PATH_SIMT_I64: rc = launch_simt<PolI64, SrInt64>(sp, grid, s); break;
-            case PATH_SIMT_I64_NARROW: rc = launch_simt<PolI64Narrow, SrInt64>(sp, grid, s); break;
-            case PATH_SIMT_F64_MIN: rc = launch_simt<PolF64Min, SrTropF64>(sp, grid, s); break;
-            case PATH_SIMT_I64_DP4A: rc = launch_simt<PolI8Dp4a, SrInt64>(sp, grid, s); break;
-            case PATH_SIMT_F32_S16X2: rc = launch_simt<PolS16x2Min, SrTropF32>(sp, grid, s); break;
-            case PATH_SIMT_I32_S16X2: rc = launch_simt<PolS16x2Min, SrTropI32>(sp, grid, s); break;
-            case PATH_SIMT_F64T_S16X2: rc = launch_simt<PolS16x2Min, SrTropF64>(sp, grid, s); break;
-            case PATH_SIMT_F64T_CARRIER: rc = launch_simt<PolF32Pair, SrTropF64>(sp, grid, s); break;
+            case PATH_SIMT_F32_PAIR: rc = launch_simt<PolF32Pair, SrTropF32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I32_CARRIER: rc = launch_simt<PolF32Pair, SrTropI32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I32_VMIN: rc = launch_simt<PolI32Vmin, SrTropI32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I32_SAT: rc = launch_simt<PolI32Sat, SrTropI32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I64: rc = launch_simt<PolI64, SrInt64>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I64_NARROW: rc = launch_simt<PolI64Narrow, SrInt64>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_F64_MIN: rc = launch_simt<PolF64Min, SrTropF64>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I64_DP4A: rc = launch_simt<PolI8Dp4a, SrInt64>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_F32_S16X2: rc = launch_simt<PolS16x2Min, SrTropF32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_I32_S16X2: rc = launch_simt<PolS16x2Min, SrTropI32>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_F64T_S16X2: rc = launch_simt<PolS16x2Min, SrTropF64>(sp, grid, P->sms, s); break;
+            case PATH_SIMT_F64T_CARRIER: rc = launch_simt<PolF32Pair, SrTropF64>(sp, grid, P->sms, s); break;
             }
         }
         if (rc) break;
