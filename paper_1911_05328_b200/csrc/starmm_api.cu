@@ -192,7 +192,10 @@ PathShape path_shape(int path) {
 // Policies that also ship a one-CTA-per-SM build (register budget 255 instead of 128):
 // the planner's occupancy-1 choice then runs at 0.97 of a full SM instead of 0.89
 // (tools/sweep_simt.cu; config 2 = 1024 tiles, 6.9 waves of 148 CTAs).
-template <class Pol> constexpr bool has_occ1_build() { return std::is_same<Pol, PolI8Dp4a>::value; }
+template <class Pol> constexpr bool has_occ1_build() {
+    return std::is_same<Pol, PolI8Dp4a>::value || std::is_same<Pol, PolF32Pair>::value ||
+           std::is_same<Pol, PolS16x2Min>::value;
+}
 
 template <class Pol, class Sr>
 int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
@@ -645,7 +648,11 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             double best = 0;
             int best_occ = per_sm, best_s = 0;
             for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
-                const double rate1 = path == PATH_SIMT_I64_DP4A ? 0.97 : 0.89;   // has_occ1_build
+                const bool occ1_build = path == PATH_SIMT_I64_DP4A || path == PATH_SIMT_F32_PAIR ||
+                                        path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER ||
+                                        path == PATH_SIMT_F32_S16X2 || path == PATH_SIMT_I32_S16X2 ||
+                                        path == PATH_SIMT_F64T_S16X2;                // has_occ1_build
+                const double rate1 = occ1_build ? 0.97 : 0.89;
                 const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
                 for (int sl = 0; sl <= smax; ++sl) {
                     const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
