@@ -29,6 +29,7 @@
 #include "aux_kernels.cuh"
 #include "tc_gemm.cuh"
 #include "ozaki.cuh"
+#include "simt_launch.h"
 
 using namespace starmm;
 
@@ -136,13 +137,7 @@ struct starmm_plan {
 
 namespace {
 
-// ---- kernel instantiation table ----------------------------------------------
-enum PathId : int {
-    PATH_DMMA_F64 = 1, PATH_SIMT_I64 = 2, PATH_SIMT_I64_NARROW = 3, PATH_SIMT_F32_PAIR = 4,
-    PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
-    PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11,
-    PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13, PATH_TC_I8 = 14, PATH_OZAKI_F64 = 15
-};
+// ---- kernel instantiation table: PathId in simt_launch.h ----------------------
 
 // Tile / packing geometry of one kernel path (mirrors the device-side constants).
 struct PathShape {
@@ -187,41 +182,6 @@ PathShape path_shape(int path) {
     }
     }
     return simt_shape<PolI64>();
-}
-
-// Policies that also ship a one-CTA-per-SM build (register budget 255 instead of 128):
-// the planner's occupancy-1 choice then runs at 0.97 of a full SM instead of 0.89
-// (tools/sweep_simt.cu; config 2 = 1024 tiles, 6.9 waves of 148 CTAs).
-template <class Pol> constexpr bool has_occ1_build() {
-    return std::is_same<Pol, PolI8Dp4a>::value || std::is_same<Pol, PolF32Pair>::value ||
-           std::is_same<Pol, PolS16x2Min>::value;
-}
-
-template <class Pol, class Sr>
-int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
-    constexpr int smem = simt::smem_bytes<Pol>();
-    if constexpr (has_occ1_build<Pol>() && Pol::OCC > 1) {
-        if (grid <= sms) {
-            auto k1 = simt_mm_kernel<Pol, Sr, 1>;
-            static bool attr1 = false;
-            if (!attr1) {
-                CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr1 = true;
-            }
-            k1<<<grid, simt::THREADS, smem, s>>>(p);
-            CK(cudaGetLastError());
-            return STARMM_OK;
-        }
-    }
-    auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_done = true;
-    }
-    kern<<<grid, simt::THREADS, smem, s>>>(p);
-    CK(cudaGetLastError());
-    return STARMM_OK;
 }
 
 int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
@@ -444,6 +404,17 @@ int ensure_bookkeeping(starmm_plan* P) {
 }  // namespace
 
 // ============================================================================
+int starmm_simt_launch(int path, const starmm::SimtParams& sp, int grid, int sms, cudaStream_t s) {
+    switch (path) {
+    case PATH_SIMT_I64: case PATH_SIMT_I64_NARROW: case PATH_SIMT_I64_DP4A:
+        return starmm_simt_launch_int(path, sp, grid, sms, s);
+    case PATH_SIMT_F32_PAIR: case PATH_SIMT_I32_CARRIER: case PATH_SIMT_F64T_CARRIER:
+        return starmm_simt_launch_pair(path, sp, grid, sms, s);
+    default:
+        return starmm_simt_launch_min(path, sp, grid, sms, s);
+    }
+}
+
 extern "C" {
 
 int starmm_abi_version(void) { return STARMM_ABI_VERSION; }
@@ -962,20 +933,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         } else {
             SimtParams sp;
             sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = g; sp.w = w;
-            switch (path) {
-            case PATH_SIMT_F32_PAIR: rc = launch_simt<PolF32Pair, SrTropF32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I32_CARRIER: rc = launch_simt<PolF32Pair, SrTropI32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I32_VMIN: rc = launch_simt<PolI32Vmin, SrTropI32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I32_SAT: rc = launch_simt<PolI32Sat, SrTropI32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I64: rc = launch_simt<PolI64, SrInt64>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I64_NARROW: rc = launch_simt<PolI64Narrow, SrInt64>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_F64_MIN: rc = launch_simt<PolF64Min, SrTropF64>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I64_DP4A: rc = launch_simt<PolI8Dp4a, SrInt64>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_F32_S16X2: rc = launch_simt<PolS16x2Min, SrTropF32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_I32_S16X2: rc = launch_simt<PolS16x2Min, SrTropI32>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_F64T_S16X2: rc = launch_simt<PolS16x2Min, SrTropF64>(sp, grid, P->sms, s); break;
-            case PATH_SIMT_F64T_CARRIER: rc = launch_simt<PolF32Pair, SrTropF64>(sp, grid, P->sms, s); break;
-            }
+            // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
+            rc = cuda_status((cudaError_t)starmm_simt_launch(path, sp, grid, P->sms, s));
         }
         if (rc) break;
         ++launches;
