@@ -1443,7 +1443,10 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                    long long kk, bool store) {
         Q->m = rows; Q->k = kk;
         if (kk == k - kq && ks2 >= -1) Q->ksplit_req = ks2;   // phase-2 split override (tuning)
-        Q->flags = store ? (saved_flags | STARMM_F_INIT_IDENTITY) : (saved_flags & ~STARMM_F_INIT_IDENTITY);
+        // (STARMM_F_TIME_MAIN would synchronise the host after every launch and serialise the
+        // schedule, so the host path never times its kernels)
+        const int f = saved_flags & ~STARMM_F_TIME_MAIN;
+        Q->flags = store ? (f | STARMM_F_INIT_IDENTITY) : (f & ~STARMM_F_INIT_IDENTITY);
         int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true);
         Q->m = m; Q->k = k; Q->flags = saved_flags; Q->ksplit_req = saved_ks;
         return r;
