@@ -596,18 +596,22 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             // model reproduces -- and +30%/+48% for sar): TAR atomic-madd 2 stages (20 for the CAS
             // of float minima), CO3 workspace + merge 3, SAR pair states + locks + lazy
             // temporaries 60 on DMMA (the sibling folds serialise under the tile lock; n=1024:
-            // +40% at S=2) and 6 on the CUDA-core paths (2-4x longer stages, batched folds);
+            // +40% at S=2) and 16 on the CUDA-core paths (2-4x longer stages, batched folds;
+            // int64 n=1024: S=2 cost +23%);
             // STAR levels above switch_depth are TAR, deeper ones SAR.  The DMMA path always
             // runs two CTAs per SM.
             const bool cas_min = P->sr == STARMM_SR_TROPICAL_F32 || P->sr == STARMM_SR_TROPICAL_F64;
-            const double pen_tar = cas_min ? 20.0 : 2.0, pen_sar = is_dmma ? 60.0 : 6.0;
+            const double pen_tar = cas_min ? 20.0 : 2.0, pen_sar = is_dmma ? 60.0 : 16.0;
+            // (the SAR folds of one tile serialise under its lock: cost grows with the 2^sl
+            // slices per tile -- tropical n=1024, S=8: -27% vs co2 with a flat penalty)
             auto split_pen = [&](int sl) -> double {
                 if (sl == 0) return 0.0;
+                const double sar = pen_sar * (double)(1 << sl) / 2.0;
                 switch (P->algo) {
                 case STARMM_TAR: return pen_tar;
                 case STARMM_CO3: return 3.0;
-                case STARMM_SAR: return pen_sar;
-                default: return sl <= switch_depth(P->workers) ? pen_tar : pen_sar;   // star
+                case STARMM_SAR: return sar;
+                default: return sl <= switch_depth(P->workers) ? pen_tar : sar;   // star
                 }
             };
             const double kst = (double)round_up(P->k, BK) / BK;
