@@ -343,32 +343,33 @@ struct EpiOzakiResidues {
     }
 };
 
-// CRT reconstruction, exact scaling and the fold into C.  One thread per 16
-// consecutive output columns of one row, in 4 groups of 4: per group one 32-bit
-// residue word per plane and the C loads are issued before the arithmetic.
-constexpr int OZ_CRT_W = 16;
-__global__ void __launch_bounds__(256)
+// CRT reconstruction, exact scaling and the fold into C.  One thread per 8 consecutive
+// output columns of one row: per plane ONE 8-byte load of its 8 residue bytes (a warp
+// reads 256 contiguous bytes of each plane -- with 4-byte loads of 16-column groups
+// only a quarter of every sector was used and the kernel was L1/L2-throughput bound,
+// ncu: 84% memory throughput at 2.2 TB/s of DRAM), then 2 groups of 4 columns.
+constexpr int OZ_CRT_W = 8;
+__global__ void __launch_bounds__(128)
 oz_crt_kernel(const unsigned char* __restrict__ R, long long Mp, long long Np,
               const unsigned long long* __restrict__ rowmax, const unsigned long long* __restrict__ colmax,
               int t, const OzCrt crt, const TcgOut o) {
-    // grid: x over 16-column groups of a row, y strides over rows (no divisions)
+    // grid: x over 8-column groups of a row, y strides over rows (no divisions)
     const long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * OZ_CRT_W;
     if (c0 >= o.N) return;
+    const size_t plane = (size_t)Mp * Np;
     for (long long row = blockIdx.y; row < o.M; row += gridDim.y) {
-        const unsigned char* rbase = R + (size_t)row * Np + c0;
+        const unsigned char* rbase = R + (size_t)row * Np + c0;   // 8-byte aligned (c0 % 8 == 0)
         const bool local = o.remote_parts == 0;
         const int ncol = (int)min((long long)OZ_CRT_W, o.N - c0);
         double* crow = (double*)o.C + row * o.ldc + c0;
         const int sig = oz_sigma(rowmax[row], t);
-        // 4 groups of 4 columns: the group loop stays rolled (code size: the body is
-        // ~250 instructions per element), the 4 elements of a group are unrolled so the
-        // residue bytes and C values stay in registers; C loads lead the arithmetic
+        uint2 word8[oz::P];                          // residue bytes of the 8 columns
+#pragma unroll
+        for (int p = 0; p < oz::P; ++p) word8[p] = __ldcs(reinterpret_cast<const uint2*>(rbase + p * plane));
+        // 2 groups of 4 columns: the group loop stays rolled (code size: the body is
+        // ~250 instructions per element); C loads lead the arithmetic
 #pragma unroll 1
         for (int g = 0; g < OZ_CRT_W / 4; ++g) {
-            uint32_t word[oz::P];                    // residue bytes of these 4 columns
-#pragma unroll
-            for (int p = 0; p < oz::P; ++p)
-                word[p] = *reinterpret_cast<const uint32_t*>(rbase + (size_t)p * Mp * Np + 4 * g);
             double cv[4];
             int tau[4];
 #pragma unroll
@@ -383,7 +384,8 @@ oz_crt_kernel(const unsigned char* __restrict__ R, long long Mp, long long Np,
                 uint32_t rho[oz::P];
 #pragma unroll
                 for (int p = 0; p < oz::P; ++p) {
-                    rho[p] = (word[p] >> (8 * jj)) & 0xff;
+                    const uint32_t w = g ? word8[p].y : word8[p].x;
+                    rho[p] = (w >> (8 * jj)) & 0xff;
                 }
                 if (j < ncol) {
                     int ex;
