@@ -757,7 +757,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             case PATH_TC_I8:
                 pack_i8_rows_kernel<<<dim3((unsigned)((Kp / 8 + 255) / 256), (unsigned)std::min<long long>(Mp, 4096)), 256, 0, s>>>(
                     (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, Kp, rng);
-                pack_i8_transpose_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 32)), dim3(32, 8), 0, s>>>(
+                pack_i8_transpose_kernel<<<dim3((unsigned)(Np / 32), (unsigned)((Kp + 127) / 128)), dim3(32, 8), 0, s>>>(
                     (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;

@@ -400,13 +400,23 @@ __global__ void pack_i8_rows_kernel(const long long* A, long long rows, long lon
     const long long k0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 8;
     if (k0 < kp) {
         for (long long r = blockIdx.y; r < rowsp; r += gridDim.y) {
+            long long v[8];
+            const long long* src = A + r * lda + k0;
+            if (r < rows && k0 + 8 <= kdim && (reinterpret_cast<uintptr_t>(src) & 15) == 0) {
+#pragma unroll
+                for (int e = 0; e < 8; e += 2) {          // 16-byte loads
+                    const longlong2 x = *reinterpret_cast<const longlong2*>(src + e);
+                    v[e] = x.x; v[e + 1] = x.y;
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < 8; ++e) v[e] = (r < rows && k0 + e < kdim) ? src[e] : 0;
+            }
             uint32_t w[2] = {0u, 0u};
 #pragma unroll
             for (int e = 0; e < 8; ++e) {
-                const long long k = k0 + e;
-                const long long v = (r < rows && k < kdim) ? A[r * lda + k] : 0;
-                acc.add(v);
-                w[e >> 2] |= (uint32_t)(unsigned char)(signed char)v << (8 * (e & 3));
+                acc.add(v[e]);
+                w[e >> 2] |= (uint32_t)(unsigned char)(signed char)v[e] << (8 * (e & 3));
             }
             *reinterpret_cast<uint2*>(P + r * kp + k0) = make_uint2(w[0], w[1]);
         }
@@ -414,24 +424,39 @@ __global__ void pack_i8_rows_kernel(const long long* A, long long rows, long lon
     if (range) acc.flush(range);
 }
 
-__global__ void pack_i8_transpose_kernel(const long long* B, long long kdim, long long cols, long long ldb,
-                                         signed char* P, long long colsp, long long kp,
-                                         unsigned long long* range) {
-    __shared__ signed char tile[32][33];
+// B [k][n] -> P [n][kp] int8.  Block (32, 8) covers 128 k x 32 columns: coalesced 256-byte
+// row reads, then every warp writes one column's 128 k-bytes as 32 words (a full line).
+__global__ void __launch_bounds__(256)
+pack_i8_transpose_kernel(const long long* B, long long kdim, long long cols, long long ldb,
+                         signed char* P, long long colsp, long long kp,
+                         unsigned long long* range) {
+    constexpr int TK = 128;
+    __shared__ uint32_t tile[32][TK / 4 + 1];     // [column][k-word]
     RangeAcc acc;
-    const long long k0 = (long long)blockIdx.y * 32, c0 = (long long)blockIdx.x * 32;
+    const long long k0 = (long long)blockIdx.y * TK, c0 = (long long)blockIdx.x * 32;
     const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-    for (int i = ty; i < 32; i += 8) {
-        long long k = k0 + i, c = c0 + tx;
-        long long v = (k < kdim && c < cols) ? B[k * ldb + c] : 0;
-        acc.add(v);
-        tile[i][tx] = (signed char)v;
+    const long long c = c0 + tx;
+    // thread (tx, ty) reads k = k0 + 4*ty + 32*i + e (e = 0..3) of column tx: packs one word
+#pragma unroll
+    for (int i = 0; i < TK / 32; ++i) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            const long long k = k0 + 32 * i + 4 * ty + e;
+            const long long v = (k < kdim && c < cols) ? B[k * ldb + c] : 0;
+            acc.add(v);
+            w |= (uint32_t)(unsigned char)(signed char)v << (8 * e);
+        }
+        tile[tx][8 * i + ty] = w;
     }
     if (range) acc.flush(range);
     __syncthreads();
-    for (int i = ty; i < 32; i += 8) {
-        long long c = c0 + i, k = k0 + tx;
-        if (c < colsp && k < kp) P[c * kp + k] = tile[tx][i];
+    // warp ty writes columns ty, ty + 8, ty + 16, ty + 24: lane tx = k-word tx
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int col = ty + 8 * j;
+        const long long cc = c0 + col, kk = k0 + 4 * tx;
+        if (cc < colsp && kk < kp) *reinterpret_cast<uint32_t*>(P + cc * kp + kk) = tile[col][tx];
     }
 }
 
