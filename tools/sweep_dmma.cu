@@ -49,6 +49,14 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'w') {   // 8 warps of 32x32 (4 warps per SMSP at 2 CTAs/SM)
+        for (int rep = 0; rep < 2; ++rep) {
+            run<P, true, 1>("mbar_64x128_2x2_s4_epi1", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<64, 128, 2, 4, 16, 4, 2>, true, 1>("mbar_64x128_2x4_s4_epi1", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<128, 128, 4, 4, 16, 3, 1>, true, 1>("mbar_128x128_4x4_s3_occ1", n, A, B, C, cnt, sms, 24, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'e') {   // epilogue A/B: generic vs vectorised batched FOLD
         for (int rep = 0; rep < 2; ++rep) {
             run<P, true, 0>("mbar_64x128_s4_epi0", n, A, B, C, cnt, sms, 24, true);
