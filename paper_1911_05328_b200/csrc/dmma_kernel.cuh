@@ -61,6 +61,7 @@ struct DmmaParams {
     const double* B; long long ldb;
     TaskGrid g;
     WbParams w;
+    unsigned* gate = nullptr;         // wave gate counter (zeroed per launch), GATE builds only
 };
 
 template <class K>
@@ -213,7 +214,11 @@ STARMM_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
 // EPI = 1: the exclusive FOLD write-back reads its 2-double fragment pairs as 16-byte
 // vectors, a whole fragment row (NJ pairs) in flight before any store (EPI = 0: the
 // generic element-by-element writeback).  Other protocols always use the generic one.
-template <class K, int EPI = 0>
+// GATE = 1: wave gate -- a CTA starts its i-th tile only after every CTA has finished
+// its (i-1)-th (one global counter; bounded wait, so a grid that is not fully
+// co-resident cannot hang), keeping the persistent CTAs of a wave in step in k so the
+// wave's A/B panel slices are shared in L2 instead of re-read from DRAM.
+template <class K, int EPI = 0, int GATE = 0>
 __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb(DmmaParams p) {
     constexpr int BM = K::BM, BN = K::BN, BK = K::BK, STAGES = K::STAGES;
     constexpr int A_LD = K::A_LD, B_LD = K::B_LD, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
@@ -239,7 +244,25 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
     __syncthreads();
     long long gk = 0;   // global stage counter: slot = gk % STAGES, use = gk / STAGES
 
-    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
+    int iter = 0;
+    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x, ++iter) {
+        if constexpr (GATE >= 1) {
+            if (iter > 0) {
+                if (tid == 0) {
+                    // slack: GATE 1 = none, 2 = a quarter wave, 3 = half a wave
+                    const unsigned slack = GATE == 1 ? 0u : (GATE == 2 ? gridDim.x / 4 : gridDim.x / 2);
+                    const unsigned need = (unsigned)iter * gridDim.x - slack;
+                    const long long t0 = clock64();
+                    unsigned v;
+                    for (;;) {
+                        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.gate) : "memory");
+                        if (v >= need || clock64() - t0 > 4000000LL) break;   // ~2 ms cap
+                        __nanosleep(128);
+                    }
+                }
+                __syncthreads();
+            }
+        }
         int tm, tn, s, tile;
         decode_task(g, t, tm, tn, s, tile);
         const int mode = task_mode(p.w, g, s);
@@ -321,6 +344,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
                     for (int j = 0; j < NJ; ++j)
                         row[j * 4] = make_double2(old[j].x + acc[i][j][0], old[j].y + acc[i][j][1]);
                 }
+                if constexpr (GATE >= 1) {
+                    __syncthreads();
+                    if (tid == 0) { __threadfence(); atomicAdd(p.gate, 1u); }
+                }
                 continue;
             }
         }
@@ -336,6 +363,10 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
                     f(r, c + 1, acc[i][j][1]);
                 }
         });
+        if constexpr (GATE >= 1) {
+            __syncthreads();
+            if (tid == 0) { __threadfence(); atomicAdd(p.gate, 1u); }
+        }
     }
 }
 

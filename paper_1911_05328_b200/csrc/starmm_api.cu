@@ -119,6 +119,8 @@ struct starmm_plan {
     volatile unsigned long long* h_range = nullptr;
     unsigned long long* h_range_dev = nullptr;
     unsigned* d_worker_used = nullptr;          // per persistent worker
+    unsigned* d_gate = nullptr;                 // DMMA wave-gate counter
+    int dmma_gate = 1;                          // 0 inside the host path (overlapping launches)
     int max_workers = 0;
     starmm_stats st;
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
@@ -184,17 +186,26 @@ PathShape path_shape(int path) {
     return simt_shape<PolI64>();
 }
 
-int launch_dmma(const DmmaParams& p, int grid, cudaStream_t s) {
+// mbarrier-pipelined k-loop (tools/sweep_dmma.cu: 35.4 vs 34.4 TF/s with per-stage
+// __syncthreads), vectorised FOLD epilogue.  With `gate` (p.gate zeroed here) the
+// wave gate with a quarter-wave slack keeps the persistent CTAs in step: DRAM reads
+// per n=16384 launch 240-263 GB -> 51 GB at -0.1% (profiles/r01l_dmma_gate.md).
+int launch_dmma(const DmmaParams& p, int grid, bool gate, cudaStream_t s) {
     using K = DmmaProd;
     static bool attr_done = false;
     if (!attr_done) {
-        CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                K::SMEM_BYTES));
+        CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 K::SMEM_BYTES));
         attr_done = true;
     }
-    // mbarrier-pipelined k-loop (tools/sweep_dmma.cu: 35.4 vs 34.4 TF/s with per-stage
-    // __syncthreads)
-    dmma_fp64_kernel_mb<K, 1><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
+    if (gate && p.gate) {
+        CK(cudaMemsetAsync(p.gate, 0, sizeof(unsigned), s));
+        dmma_fp64_kernel_mb<K, 1, 2><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
+    } else {
+        dmma_fp64_kernel_mb<K, 1, 0><<<grid, K::THREADS, K::SMEM_BYTES, s>>>(p);
+    }
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -388,12 +399,13 @@ int ensure_bookkeeping(starmm_plan* P) {
     P->max_workers = P->sms * 2;
     long long fr = 0, ru = 0;
     void* p = nullptr;
-    size_t bytes = CNT__N * 8 + 16 + (size_t)P->max_workers * 4;
+    size_t bytes = CNT__N * 8 + 16 + (size_t)P->max_workers * 4 + 16;
     TRY(P->arena.acquire(bytes, &p, false, &fr, &ru));
     CK(cudaMemset(p, 0, bytes));
     P->d_counters = (unsigned long long*)p;
     P->d_range = P->d_counters + CNT__N;
     P->d_worker_used = (unsigned*)(P->d_range + 2);
+    P->d_gate = P->d_worker_used + P->max_workers;
     void* h = nullptr;
     CK(cudaHostAlloc(&h, 16, cudaHostAllocMapped));
     P->h_range = (volatile unsigned long long*)h;
@@ -933,7 +945,11 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             DmmaParams dp;
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
             dp.g = g; dp.w = w;
-            rc = launch_dmma(dp, grid, s);
+            dp.gate = P->d_gate;
+            // the wave gate needs the whole grid co-resident and pays only over several
+            // waves; the host path's overlapping launches run without it
+            const bool gate = P->dmma_gate && ntasks >= 4LL * grid;
+            rc = launch_dmma(dp, grid, gate, s);
         } else {
             SimtParams sp;
             sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = g; sp.w = w;
@@ -1405,6 +1421,12 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         TRY(res.stream(&cs2));
     }
     const starmm_stats twin_before = two_streams ? P->twin->st : starmm_stats{};
+    struct GateOff {            // the schedule's launches overlap: no wave gate inside it
+        starmm_plan* a; starmm_plan* b;
+        ~GateOff() { a->dmma_gate = 1; if (b) b->dmma_gate = 1; }
+    } gate_off{P, two_streams ? P->twin : nullptr};
+    P->dmma_gate = 0;
+    if (two_streams) P->twin->dmma_gate = 0;
     std::vector<cudaEvent_t> ev_q(nq), ev_a(nblk), ev_c(nblk), ev_done(nblk);
     cudaEvent_t ev_rest = nullptr, ev_p1 = nullptr;
     TRY(res.event(&ev_rest));

@@ -7,7 +7,7 @@
 #include "../paper_1911_05328_b200/csrc/dmma_kernel.cuh"
 using namespace starmm;
 
-template <class K, bool MB = false, int EPI = 0>
+template <class K, bool MB = false, int EPI = 0, int GATE = 0>
 void run(const char* name, int n, double* A, double* B, double* C, unsigned long long* cnt, int sms,
          int group_m = 8, bool persistent = true) {
     DmmaParams p{};
@@ -18,16 +18,20 @@ void run(const char* name, int n, double* A, double* B, double* C, unsigned long
     WbParams& w = p.w;
     w.mode_base = 0; w.init_identity = 0; w.C = C; w.ldc = n; w.M = n; w.N = n;
     w.counters = cnt;
-    auto kern = MB ? dmma_fp64_kernel_mb<K, EPI> : dmma_fp64_kernel<K>;
+    auto kern = MB ? dmma_fp64_kernel_mb<K, EPI, GATE> : dmma_fp64_kernel<K>;
+    static unsigned* gate = nullptr;
+    if (!gate) cudaMalloc(&gate, 4);
+    p.gate = gate;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, K::THREADS, K::SMEM_BYTES);
     int grid = sms * (occ > 0 ? occ : 1);
     if (grid > g.num_tasks || !persistent) grid = g.num_tasks;
+    cudaMemset(gate, 0, 4);
     kern<<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
     cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
     cudaEventRecord(e0);
-    for (int i = 0; i < 3; ++i) kern<<<grid, K::THREADS, K::SMEM_BYTES>>>(p);
+    for (int i = 0; i < 3; ++i) { cudaMemsetAsync(gate, 0, 4); kern<<<grid, K::THREADS, K::SMEM_BYTES>>>(p); }
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1); ms /= 3;
     cudaError_t e = cudaGetLastError();
@@ -49,6 +53,15 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'g') {   // wave gate A/B
+        for (int rep = 0; rep < 2; ++rep) {
+            run<P, true, 1, 0>("mbar_s4_epi1_nogate", n, A, B, C, cnt, sms, 24, true);
+            run<P, true, 1, 1>("mbar_s4_epi1_gate", n, A, B, C, cnt, sms, 24, true);
+            run<P, true, 1, 2>("mbar_s4_epi1_gate_q", n, A, B, C, cnt, sms, 24, true);
+            run<P, true, 1, 3>("mbar_s4_epi1_gate_h", n, A, B, C, cnt, sms, 24, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'w') {   // 8 warps of 32x32 (4 warps per SMSP at 2 CTAs/SM)
         for (int rep = 0; rep < 2; ++rep) {
             run<P, true, 1>("mbar_64x128_2x2_s4_epi1", n, A, B, C, cnt, sms, 24, true);
