@@ -245,10 +245,11 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
     long long gk = 0;   // global stage counter: slot = gk % STAGES, use = gk / STAGES
 
     int iter = 0;
+    bool gate_on = true;      // (thread 0) a wait that hit the cap turns this CTA's gate off
     for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x, ++iter) {
         if constexpr (GATE >= 1) {
             if (iter > 0) {
-                if (tid == 0) {
+                if (tid == 0 && gate_on) {
                     // slack: GATE 1 = none, 2 = a quarter wave, 3 = half a wave
                     const unsigned slack = GATE == 1 ? 0u : (GATE == 2 ? gridDim.x / 4 : gridDim.x / 2);
                     const unsigned need = (unsigned)iter * gridDim.x - slack;
@@ -256,7 +257,8 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
                     unsigned v;
                     for (;;) {
                         asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p.gate) : "memory");
-                        if (v >= need || clock64() - t0 > 4000000LL) break;   // ~2 ms cap
+                        if (v >= need) break;
+                        if (clock64() - t0 > 4000000LL) { gate_on = false; break; }   // ~2 ms cap
                         __nanosleep(128);
                     }
                 }

@@ -192,6 +192,34 @@ def test_spec_soft_throughput_gate(sid):
     assert med["sar"] <= 1.15 * med["co3"], med
 
 
+def test_dmma_wave_gate_with_concurrent_launches():
+    """Two gated DMMA launches on two streams at once (neither grid fully co-resident):
+    the bounded gate wait turns itself off instead of stalling, results stay correct."""
+    n = 4096
+    s = sm.FLOAT_RING
+    g = torch.Generator(device="cuda").manual_seed(9)
+    A = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    B = torch.randn(n, n, dtype=torch.float64, device="cuda", generator=g)
+    want = A @ B
+    from paper_1911_05328_b200 import _lib
+    plans = [_lib.Plan(s.sr_id, "co2", "pooled", n, n, n, 64, 148, -1, 0, _lib.F_INIT_IDENTITY | _lib.F_ASYNC)
+             for _ in range(2)]
+    outs = [torch.empty(n, n, dtype=torch.float64, device="cuda") for _ in range(2)]
+    streams = [torch.cuda.Stream() for _ in range(2)]
+    torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    for p, o, st in zip(plans, outs, streams):
+        p.execute(o.data_ptr(), n, A.data_ptr(), n, B.data_ptr(), n, st.cuda_stream)
+    torch.cuda.synchronize()
+    dt = time.perf_counter() - t0
+    for p in plans:
+        p.close()
+    for o in outs:
+        assert torch.allclose(o, want, rtol=1e-10, atol=1e-9)
+    assert dt < 1.0, dt      # 2 x 0.137 Tflop ~ 8 ms of work; a stalled gate would take seconds
+
+
 # ---- BASELINE config 1 (PR1) ----------------------------------------------
 def test_pr1_star_fp64_vs_reference():
     from bench_configs import make_inputs
