@@ -470,7 +470,11 @@ def e2e_run(args, sm, s, cid, dmm, A, B, C, device, world, grid, group_ks):
     if ex is not None:
         ex.close()
     es = Ah.element_size()
-    h2d = (Ah.numel() + (0 if Bh is Ah else Bh.numel()) + Ch.numel()) * es
+    c_up = Ch.numel()
+    if world > 1 and dmm.combine_mode == "fused":     # only the owner's C0 rows go up
+        lo, hi = dmm.owned_rows()
+        c_up = (hi - lo) * dmm.nn
+    h2d = (Ah.numel() + (0 if Bh is Ah else Bh.numel()) + c_up) * es
     d2h = (Ch.numel() if world == 1 else out.numel()) * es
     return {"value": 2.0 * dmm.n ** 3 / float(t[0]) / 1e12, "unit": "Tops/s",
             "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),

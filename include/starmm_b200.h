@@ -141,8 +141,10 @@ int  starmm_execute(starmm_plan* plan, void* C, int64_t ldc, const void* A, int6
  * chunks and B's row chunks arrive, then the rest of k in row blocks of
  * `block_rows` rows (0 = auto) whose results (C0 folded in) stream back while the
  * next block computes; PCIe-bound ones upload B, then stream A/C row blocks.
- * Blocking.  DESIGN.md §7b.  Classical schedules only, and not after
- * starmm_plan_set_peers (both: STARMM_CONTRACT_VIOLATION).
+ * Blocking.  DESIGN.md §7b.  Classical schedules only (else
+ * STARMM_CONTRACT_VIOLATION).  After starmm_plan_set_peers (a k-split rank of the
+ * fused combine) only A and B stream in, in k-chunks, and C is not touched: the tile
+ * kernels fold into the owners' rows, which the owners pre-load and read back.
  * The reference's entry points take host (numpy) matrices (classic.py:294-316);
  * this is their host-buffer form. */
 int  starmm_execute_host(starmm_plan* plan, void* C, int64_t ldc, const void* A, int64_t lda,

@@ -1307,6 +1307,31 @@ int starmm_ipc_close(void* dptr) {
 // "cross" of row block c (columns >= kb_c) and column block c (rows >= kb_{c+1}),
 // and the bottom-right square [kq, m) x [kq, n) completes the matrix before phase 2.
 // STARMM_HOST_PHASE1=0 disables phase 1 (row blocks only, C0 uploaded in place).
+// streams / events / the caller's device of a host-path call, released or restored on
+// every return path
+struct HostRes {
+    std::vector<cudaStream_t> streams;
+    std::vector<cudaEvent_t> events;
+    int prev_dev = -1, dev = -1;
+    ~HostRes() {
+        for (auto x : streams) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
+        for (auto x : events) cudaEventDestroy(x);
+        if (prev_dev >= 0 && prev_dev != dev) cudaSetDevice(prev_dev);
+    }
+    int stream(cudaStream_t* out) {
+        cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
+        if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
+        streams.push_back(*out);
+        return STARMM_OK;
+    }
+    int event(cudaEvent_t* out) {
+        cudaError_t e = cudaEventCreateWithFlags(out, cudaEventDisableTiming);
+        if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
+        events.push_back(*out);
+        return STARMM_OK;
+    }
+};
+
 // Phase 1 pays only when the problem is compute-bound over PCIe: the estimated compute
 // time (a nominal per-semiring B200 rate) must exceed the H2D time (50 GB/s); PCIe-bound
 // problems (config 2) upload B first and run row blocks only.  STARMM_HOST_PHASE1=0/1
@@ -1337,36 +1362,73 @@ static int host_phase1_chunks(long long m, long long n, long long k, int sr, dou
     return (int)kb.size() - 1;
 }
 
+// Host path of a k-split rank with the fused combine (starmm_plan_set_peers): every
+// tile kernel folds its partials straight into the owners' rows over peer memory, so
+// there is no local C to upload or download -- only A and B stream in, in k-chunks of
+// doubling width (k/32, k/16, ...), each chunk one execute over all rows as soon as its
+// operands have landed (the owners pre-load C0 and download their rows themselves).
+static int execute_host_remote(starmm_plan* P, const void* A, int64_t lda, const void* B, int64_t ldb,
+                               void* stream) {
+    HostRes res;
+    CK(cudaGetDevice(&res.prev_dev));
+    res.dev = P->device;
+    if (res.prev_dev != P->device) CK(cudaSetDevice(P->device));
+    const size_t eb = (size_t)elem_bytes(P->sr);
+    const long long m = P->m, n = P->n, k = P->k;
+    std::vector<long long> kb(1, 0);
+    for (long long w = std::max<long long>(128, round_up((k + 31) / 32, 128)); kb.back() < k; w *= 2)
+        kb.push_back(std::min(k, kb.back() + w));
+    const int nq = (int)kb.size() - 1;
+    cudaStream_t cs = (cudaStream_t)stream, up = nullptr;
+    TRY(res.stream(&up));
+    std::vector<cudaEvent_t> ev(nq);
+    for (auto& e : ev) TRY(res.event(&e));
+    void *dA = nullptr, *dB = nullptr;
+    long long fr = 0, ru = 0;
+    const size_t a_bytes = (size_t)m * k * eb, b_bytes = (size_t)k * n * eb;
+    int rc = STARMM_OK;
+    const int saved_flags = P->flags;
+    do {
+        if ((rc = P->arena.acquire(a_bytes, &dA, false, &fr, &ru))) break;
+        if ((rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
+        for (int c = 0; c < nq && !rc; ++c) {
+            const long long k0 = kb[c], kc = kb[c + 1] - kb[c];
+            rc = cuda_status(cudaMemcpy2DAsync((char*)dB + k0 * n * eb, n * eb, (const char*)B + k0 * ldb * eb,
+                                               ldb * eb, n * eb, kc, cudaMemcpyHostToDevice, up));
+            if (!rc) rc = cuda_status(cudaMemcpy2DAsync((char*)dA + k0 * eb, k * eb, (const char*)A + k0 * eb,
+                                                        lda * eb, kc * eb, m, cudaMemcpyHostToDevice, up));
+            if (!rc) rc = cuda_status(cudaEventRecord(ev[c], up));
+        }
+        if (rc) break;
+        P->flags = saved_flags & ~(STARMM_F_TIME_MAIN | STARMM_F_INIT_IDENTITY);
+        for (int c = 0; c < nq && !rc; ++c) {
+            const long long k0 = kb[c];
+            if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev[c], 0)))) break;
+            P->k = kb[c + 1] - k0;
+            // (C is not touched: every write-back goes to the peers)
+            rc = execute_impl(P, dA, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true);
+            P->k = k;
+        }
+        if (rc) break;
+        rc = cuda_status(cudaStreamSynchronize(cs));
+    } while (0);
+    P->k = k; P->flags = saved_flags;
+    cudaStreamSynchronize(up);
+    cudaStreamSynchronize(cs);
+    if (dB) P->arena.release(dB, b_bytes);
+    if (dA) P->arena.release(dA, a_bytes);
+    return rc;
+}
+
 int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* stream, int64_t block_rows) {
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
-    // classical schedules only (the Strassen family overwrites C; host_mm checks the same),
-    // and no fused peer combine (its owners' rows live on other GPUs, not in host C)
-    if (P->algo >= STARMM_STRASSEN || P->remote_parts > 0) return STARMM_CONTRACT_VIOLATION;
+    // classical schedules only (the Strassen family overwrites C; host_mm checks the same);
+    // with a fused peer combine the owners' rows live on the GPUs: execute_host_remote
+    if (P->algo >= STARMM_STRASSEN) return STARMM_CONTRACT_VIOLATION;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
-    // streams / events / the caller's device are released or restored on every return path
-    struct HostRes {
-        std::vector<cudaStream_t> streams;
-        std::vector<cudaEvent_t> events;
-        int prev_dev = -1, dev = -1;
-        ~HostRes() {
-            for (auto x : streams) { cudaStreamSynchronize(x); cudaStreamDestroy(x); }
-            for (auto x : events) cudaEventDestroy(x);
-            if (prev_dev >= 0 && prev_dev != dev) cudaSetDevice(prev_dev);
-        }
-        int stream(cudaStream_t* out) {
-            cudaError_t e = cudaStreamCreateWithFlags(out, cudaStreamNonBlocking);
-            if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
-            streams.push_back(*out);
-            return STARMM_OK;
-        }
-        int event(cudaEvent_t* out) {
-            cudaError_t e = cudaEventCreateWithFlags(out, cudaEventDisableTiming);
-            if (e != cudaSuccess) { *out = nullptr; return cuda_status(e); }
-            events.push_back(*out);
-            return STARMM_OK;
-        }
-    } res;
+    if (P->remote_parts > 0) return execute_host_remote(P, A, lda, B, ldb, stream);
+    HostRes res;
     CK(cudaGetDevice(&res.prev_dev));
     res.dev = P->device;
     if (res.prev_dev != P->device) CK(cudaSetDevice(P->device));

@@ -210,6 +210,8 @@ class DistributedMM:
         starmm_execute_host: uploads, tile kernels and downloads overlap,
         and C_h is updated in place.  With a k-split the panels are uploaded, the
         combine runs on the device, and the owned rows are copied into ``out_h``."""
+        if self.combine_mode == "fused":
+            return self._step_host_fused(C_h, A_h, B_h, out_h)
         if self.grid.ks == 1 and self.plan is not None:
             for t in (C_h, A_h, B_h):
                 if t.device.type != "cpu" or (t.shape[1] > 1 and t.stride(1) != 1):
@@ -227,6 +229,29 @@ class DistributedMM:
         if out_h is None:
             out_h = torch.empty(r.shape, dtype=r.dtype).pin_memory()
         out_h.copy_(r, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out_h
+
+    def _step_host_fused(self, C_h, A_h, B_h, out_h):
+        """k-split rank with the fused combine, host panels: the owner uploads its C0 rows
+        into the shared owner buffer, then starmm_execute_host streams A and B in k-chunks
+        and every chunk's tile kernels fold into the owners' rows over peer memory (the
+        uploads overlap the math); the owner reads its rows back."""
+        for t in (C_h, A_h, B_h):
+            if t.device.type != "cpu" or (t.shape[1] > 1 and t.stride(1) != 1):
+                raise ContractViolation("step_host needs row-major CPU panels")
+        lo, hi = self.owned_rows()
+        r = hi - lo
+        self.owned[:r].copy_(C_h[lo - self.r0:hi - self.r0], non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        dist.barrier(group=self.group_ks)
+        stream = torch.cuda.current_stream().cuda_stream
+        self.plan.execute_host(C_h.data_ptr(), max(1, C_h.stride(0)), A_h.data_ptr(),
+                               max(1, A_h.stride(0)), B_h.data_ptr(), max(1, B_h.stride(0)), stream)
+        dist.barrier(group=self.group_ks)
+        if out_h is None:
+            out_h = torch.empty((r, self.nn), dtype=self.owned.dtype).pin_memory()
+        out_h.copy_(self.owned[:r], non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return out_h
 

@@ -703,7 +703,7 @@ def test_strassen_space_straightforward_vs_sar():
         sm.sar_strassen(T, T, T, sm.TROPICAL, sm.Config(base_dim=2))
 
 
-def _fused_two_process_worker(rank, world, port, sid, n, q):
+def _fused_two_process_worker(rank, world, port, sid, n, q, host=False):
     import os
     import torch.distributed as dist
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
@@ -724,10 +724,14 @@ def _fused_two_process_worker(rank, world, port, sid, n, q):
         dmm = DistributedMM(n, s, grid, rank, algo="star", base_dim=32, workers=148,
                             group_ks=ks_groups(grid), device=0, combine="fused")
         assert dmm.combine_mode == "fused"
-        Cb = torch.from_numpy(np.ascontiguousarray(dmm.c_block(C0))).cuda()
-        Ap = torch.from_numpy(np.ascontiguousarray(dmm.a_panel(A))).cuda()
-        Bp = torch.from_numpy(np.ascontiguousarray(dmm.b_panel(B))).cuda()
-        out = dmm.step(Cb, Ap, Bp).cpu().numpy()
+        if host:   # host panels: strided views of pinned full matrices, k-streamed
+            Ah, Bh, Ch = (torch.from_numpy(x).pin_memory() for x in (A, B, C0))
+            out = dmm.step_host(dmm.c_block(Ch), dmm.a_panel(Ah), dmm.b_panel(Bh)).numpy()
+        else:
+            Cb = torch.from_numpy(np.ascontiguousarray(dmm.c_block(C0))).cuda()
+            Ap = torch.from_numpy(np.ascontiguousarray(dmm.a_panel(A))).cuda()
+            Bp = torch.from_numpy(np.ascontiguousarray(dmm.b_panel(B))).cuda()
+            out = dmm.step(Cb, Ap, Bp).cpu().numpy()
         want = C0.copy()
         O.gemm_fold(O.SR_BY_NAME[sid], want, A, B)
         lo, hi = dmm.owned_rows()
@@ -740,17 +744,18 @@ def _fused_two_process_worker(rank, world, port, sid, n, q):
 
 
 @pytest.mark.parametrize("sid", ["int", "tropical_i32", "tropical_f32"])
-def test_fused_combine_two_processes_cuda_ipc(sid):
+@pytest.mark.parametrize("host", [False, True])
+def test_fused_combine_two_processes_cuda_ipc(sid, host):
     """The real DistributedMM(combine='fused') path -- owner rows shared through CUDA IPC
     (torch reduce_tensor / rebuild), tile epilogues folding into the peer's buffer -- run
     as two processes on ONE GPU.  Host collectives go over gloo; no kernel waits on any
     other, so sharing the device is safe (B200_PROFILING.md)."""
     import torch.multiprocessing as mp
-    n, world = 512, 2
+    n, world = 768 if host else 512, 2
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    port = 31000 + hash(sid) % 1000
-    procs = [ctx.Process(target=_fused_two_process_worker, args=(r, world, port, sid, n, q))
+    port = 31000 + hash(sid) % 1000 + (500 if host else 0)
+    procs = [ctx.Process(target=_fused_two_process_worker, args=(r, world, port, sid, n, q, host))
              for r in range(world)]
     for p in procs:
         p.start()
@@ -798,17 +803,12 @@ def test_abi_error_paths():
     with pytest.raises(sm.ContractViolation):     # NULL operand
         plan.execute(0, 64, t.data_ptr(), 64, t.data_ptr(), 64, stream)
     plan.close()
-    # the host path: classical schedules only, and not with a fused peer combine
+    # the host path: classical schedules only
     h = torch.zeros(64, 64, dtype=torch.float64).pin_memory()
     sp = _lib.Plan(s.sr_id, "strassen", "pooled", 64, 64, 64, 8, 1, -1, 0, 0)
     with pytest.raises(sm.ContractViolation):
         sp.execute_host(h.data_ptr(), 64, h.data_ptr(), 64, h.data_ptr(), 64, stream)
     sp.close()
-    pp = _lib.Plan(s.sr_id, "tar", "pooled", 64, 64, 64, 8, 1, -1, 0, 0)
-    pp.set_peers([t.data_ptr()], 64, 64)
-    with pytest.raises(sm.ContractViolation):
-        pp.execute_host(h.data_ptr(), 64, h.data_ptr(), 64, h.data_ptr(), 64, stream)
-    pp.close()
 
 
 def test_int64_extreme_values_wrap():
