@@ -1352,7 +1352,7 @@ static int host_phase1_chunks(long long m, long long n, long long k, int sr, dou
     const double t_mm = 2.0 * (double)m * (double)n * (double)k / host_nominal_ops(sr);
     if (!(env && env[0] == '1') && t_mm < h2d_bytes / 50e9) return 0;
     // first chunk k/64 (k >= 8192) or k/32: its upload is the exposed head of the schedule
-    const long long div = k >= 8192 ? 64 : 32;
+    const long long div = (k >= 8192 && sr == STARMM_SR_FP64) ? 64 : 32;   // DMMA calls have no packing / guard
     long long w = std::max<long long>(128, round_up((k + div - 1) / div, 128)), sum = 0;
     while (sum + w <= k / 2) {
         sum += w;

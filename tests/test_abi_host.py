@@ -216,9 +216,9 @@ def test_host_schedule_phase1_rule_on_baseline_configs(monkeypatch):
     from _host_schedule import host_phase1
     monkeypatch.delenv("STARMM_HOST_PHASE1", raising=False)
     assert host_phase1(4096, 4096, 4096, "int") == [0]
-    assert host_phase1(8192, 8192, 8192, "tropical_f32", aliased=True) == [0, 128, 384, 896, 1920, 3968]
+    assert host_phase1(8192, 8192, 8192, "tropical_f32", aliased=True) == [0, 256, 768, 1792, 3840]
     assert host_phase1(16384, 16384, 16384, "float") == [0, 256, 768, 1792, 3840, 7936]
-    assert host_phase1(49152, 49152, 49152, "tropical_i32", aliased=True)[-1] == 23808
+    assert host_phase1(49152, 49152, 49152, "tropical_i32", aliased=True)[-1] == 23040
     assert host_phase1(256, 256, 256, "float") == [0]
     monkeypatch.setenv("STARMM_HOST_PHASE1", "1")
     assert host_phase1(4096, 4096, 4096, "int") == [0, 128, 384, 896, 1920]
