@@ -1,0 +1,5 @@
+import torch
+n = 16384
+a = torch.randn(n, n, dtype=torch.float64, device="cuda"); b = torch.randn(n, n, dtype=torch.float64, device="cuda")
+for _ in range(2): c = a @ b
+torch.cuda.synchronize()

@@ -53,6 +53,15 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'c') {   // cuBLAS-like: 64x64 tiles, 4 warps of 32x32, 3 CTAs/SM
+        for (int rep = 0; rep < 2; ++rep) {
+            run<P, true, 1, 0>("prod_64x128_2x2_s4_occ2", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<64, 64, 2, 2, 16, 3, 3>, true, 1, 0>("mbar_64x64_2x2_s3_occ3", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<64, 64, 2, 2, 16, 4, 3>, true, 1, 0>("mbar_64x64_2x2_s4_occ3", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<64, 64, 2, 2, 16, 3, 3>, true, 1, 0>("mbar_64x64_2x2_s3_occ3_g48", n, A, B, C, cnt, sms, 48, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'g') {   // wave gate A/B
         for (int rep = 0; rep < 2; ++rep) {
             run<P, true, 1, 0>("mbar_s4_epi1_nogate", n, A, B, C, cnt, sms, 24, true);
