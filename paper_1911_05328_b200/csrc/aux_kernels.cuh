@@ -118,23 +118,36 @@ __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long
         if (kw < kp / 4 && r < rowsp) P[kw * rowsp + r] = tile[tx][i];
     }
 }
-// B (kdim x cols) -> P[kp/4][colsp].  2-D grid (x: columns, y: k-words), no 64-bit
-// division per element (the grid-stride form spent 3x pack_a's time on it).
+// B (kdim x cols) -> P[kp/4][colsp].  2-D grid (x: column pairs, y: k-words), no 64-bit
+// division per element (the grid-stride form spent 3x pack_a's time on it); two columns
+// per thread with 16-byte loads when the rows allow it.
 __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
                                    int* P, long long colsp, long long kp, unsigned long long* range) {
     RangeAcc acc;
+    const bool vec = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
     for (long long kw = blockIdx.y; kw < kp / 4; kw += gridDim.y)
-        for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < colsp;
-             c += (long long)gridDim.x * blockDim.x) {
-            unsigned w = 0;
+        for (long long c = 2 * ((long long)blockIdx.x * blockDim.x + threadIdx.x); c < colsp;
+             c += 2 * (long long)gridDim.x * blockDim.x) {
+            unsigned w0 = 0, w1 = 0;
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                long long k = kw * 4 + i;
-                long long v = (c < cols && k < kdim) ? B[k * ldb + c] : 0;
-                acc.add(v);
-                w |= ((unsigned)(v & 0xff)) << (8 * i);
+                const long long k = kw * 4 + i;
+                long long v0 = 0, v1 = 0;
+                if (k < kdim) {
+                    if (vec && c + 1 < cols) {
+                        const longlong2 x = *reinterpret_cast<const longlong2*>(B + k * ldb + c);
+                        v0 = x.x; v1 = x.y;
+                    } else {
+                        v0 = c < cols ? B[k * ldb + c] : 0;
+                        v1 = c + 1 < cols ? B[k * ldb + c + 1] : 0;
+                    }
+                }
+                acc.add(v0);
+                acc.add(v1);
+                w0 |= ((unsigned)(v0 & 0xff)) << (8 * i);
+                w1 |= ((unsigned)(v1 & 0xff)) << (8 * i);
             }
-            P[kw * colsp + c] = (int)w;
+            *reinterpret_cast<uint2*>(P + kw * colsp + c) = make_uint2(w0, w1);   // colsp is even
         }
     if (range) acc.flush(range);   // every thread reaches the flush (full-warp shuffles)
 }

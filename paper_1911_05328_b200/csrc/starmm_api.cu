@@ -762,7 +762,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             case PATH_SIMT_I64_DP4A:
                 pack_a_s8x4_kernel<<<dim3((unsigned)((Kp / 4 + 31) / 32), (unsigned)(Mp / 32)), dim3(32, 8), 0, s>>>(
                     (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
-                pack_b_s8x4_kernel<<<grid2d(Kp / 4, Np), 256, 0, s>>>(
+                pack_b_s8x4_kernel<<<grid2d(Kp / 4, Np / 2), 256, 0, s>>>(
                     (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
                 rc = cuda_status(cudaGetLastError());
                 break;
