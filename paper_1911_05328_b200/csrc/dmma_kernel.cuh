@@ -50,11 +50,12 @@ struct DmmaCfg {
                   "cp.async chunking");
 };
 
-// The production configuration (selected by tools/sweep_dmma.cu on B200):
-// 64x128 tiles, 4 warps of 32x64, 4-stage ring, two CTAs per SM so one CTA's
-// stage boundaries / epilogue overlap the other's DMMA stream; launched as the
-// mbarrier-pipelined dmma_fp64_kernel_mb (below).
-using DmmaProd = DmmaCfg<64, 128, 2, 2, 16, 4, 2>;
+// The production configuration (selected by tools/sweep_dmma.cu on B200): one 128x128
+// CTA per SM of 8 warps (4 x 2) with 32x64 warp tiles, 4-stage mbarrier ring --
+// 36.1 TF/s vs 35.4 for two 64x128 CTAs of 4 warps (profiles/r01l_sweep_dmma_128.jsonl):
+// the warps of one CTA drift across the ring's stages (no CTA-wide barrier), and the
+// larger tile halves the fragment loads per DMMA and the L2 traffic per flop.
+using DmmaProd = DmmaCfg<128, 128, 4, 2, 16, 4, 1>;
 
 struct DmmaParams {
     const double* A; long long lda;   // tile-aligned (padded if needed), 16-byte rows

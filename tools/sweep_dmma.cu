@@ -53,6 +53,25 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'n') {   // the 128x128 4x2 candidate: gate / raster group
+        using Q = DmmaCfg<128, 128, 4, 2, 16, 4, 1>;
+        for (int rep = 0; rep < 2; ++rep) {
+            run<Q, true, 1, 0>("q128_g12_nogate", n, A, B, C, cnt, sms, 12, true);
+            run<Q, true, 1, 2>("q128_g12_gate", n, A, B, C, cnt, sms, 12, true);
+            run<Q, true, 1, 2>("q128_g8_gate", n, A, B, C, cnt, sms, 8, true);
+            run<Q, true, 1, 2>("q128_g16_gate", n, A, B, C, cnt, sms, 16, true);
+        }
+        return 0;
+    }
+    if (argc > 2 && argv[2][0] == 'b') {   // one 128x128 CTA of 8 warps (32x64), mbarrier ring
+        for (int rep = 0; rep < 2; ++rep) {
+            run<P, true, 1, 0>("prod_64x128_2x2_s4_occ2", n, A, B, C, cnt, sms, 24, true);
+            run<DmmaCfg<128, 128, 4, 2, 16, 4, 1>, true, 1, 0>("mbar_128x128_4x2_s4_occ1", n, A, B, C, cnt, sms, 12, true);
+            run<DmmaCfg<128, 128, 4, 2, 16, 5, 1>, true, 1, 0>("mbar_128x128_4x2_s5_occ1", n, A, B, C, cnt, sms, 12, true);
+            run<DmmaCfg<128, 128, 2, 4, 16, 4, 1>, true, 1, 0>("mbar_128x128_2x4_s4_occ1", n, A, B, C, cnt, sms, 12, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'c') {   // cuBLAS-like: 64x64 tiles, 4 warps of 32x32, 3 CTAs/SM
         for (int rep = 0; rep < 2; ++rep) {
             run<P, true, 1, 0>("prod_64x128_2x2_s4_occ2", n, A, B, C, cnt, sms, 24, true);
