@@ -50,12 +50,13 @@ struct DmmaCfg {
                   "cp.async chunking");
 };
 
-// The production configuration (selected by tools/sweep_dmma.cu on B200): one 128x128
-// CTA per SM of 8 warps (4 x 2) with 32x64 warp tiles, 4-stage mbarrier ring --
-// 36.1 TF/s vs 35.4 for two 64x128 CTAs of 4 warps (profiles/r01l_sweep_dmma_128.jsonl):
-// the warps of one CTA drift across the ring's stages (no CTA-wide barrier), and the
-// larger tile halves the fragment loads per DMMA and the L2 traffic per flop.
-using DmmaProd = DmmaCfg<128, 128, 4, 2, 16, 4, 1>;
+// The production configuration (selected by tools/sweep_dmma.cu on B200): one 256x64
+// CTA per SM of 8 warps stacked along M (8 x 1) with 32x64 warp tiles, 4-stage
+// mbarrier ring -- 36.3 TF/s vs 36.1 for 128x128 (4 x 2) and 35.4 for two 64x128 CTAs
+// of 4 warps (profiles/r01l_sweep_dmma_128.jsonl, r01n_sweep_dmma_aspect.jsonl): the
+// warps of one CTA drift across the ring's stages (no CTA-wide barrier), and the large
+// tile halves the fragment loads per DMMA and the L2 traffic per flop.
+using DmmaProd = DmmaCfg<256, 64, 8, 1, 16, 4, 1>;
 
 struct DmmaParams {
     const double* A; long long lda;   // tile-aligned (padded if needed), 16-byte rows

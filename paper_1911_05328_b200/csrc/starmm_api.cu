@@ -687,7 +687,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         g.tar_levels = tar_levels; g.kslice = kslice;
         // raster groups sized so one wave of resident CTAs covers a near-square block of
         // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
-        g.group_m = 12;   // DMMA 128-row and SIMT 128-row tiles alike
+        g.group_m = is_dmma ? 6 : 12;   // 1536 rows: DMMA 256-row, SIMT 128-row tiles
         g.balanced = balanced ? 1 : 0;
         g.kstages = Kp / std::max(1, BK);
         ntasks = tiles * S;

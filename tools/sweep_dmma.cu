@@ -53,6 +53,15 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'a') {   // aspect ratios of the 8-warp, 1-CTA/SM design
+        for (int rep = 0; rep < 2; ++rep) {
+            run<DmmaCfg<128, 128, 4, 2, 16, 4, 1>, true, 1, 0>("q128x128_4x2_s4", n, A, B, C, cnt, sms, 12, true);
+            run<DmmaCfg<128, 128, 4, 2, 16, 3, 1>, true, 1, 0>("q128x128_4x2_s3", n, A, B, C, cnt, sms, 12, true);
+            run<DmmaCfg<256, 64, 8, 1, 16, 4, 1>, true, 1, 0>("q256x64_8x1_s4", n, A, B, C, cnt, sms, 6, true);
+            run<DmmaCfg<64, 256, 2, 4, 16, 4, 1>, true, 1, 0>("q64x256_2x4_s4", n, A, B, C, cnt, sms, 24, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'n') {   // the 128x128 4x2 candidate: gate / raster group
         using Q = DmmaCfg<128, 128, 4, 2, 16, 4, 1>;
         for (int rep = 0; rep < 2; ++rep) {
