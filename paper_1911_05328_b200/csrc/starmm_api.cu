@@ -687,7 +687,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         g.tar_levels = tar_levels; g.kslice = kslice;
         // raster groups sized so one wave of resident CTAs covers a near-square block of
         // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
-        g.group_m = is_dmma ? 6 : 12;   // 1536 rows: DMMA 256-row, SIMT 128-row tiles
+        g.group_m = is_dmma ? 4 : 12;   // DMMA: 4 x 256 rows (58 GB vs 61 GB at 6), SIMT 12 x 128
         g.balanced = balanced ? 1 : 0;
         g.kstages = Kp / std::max(1, BK);
         ntasks = tiles * S;
@@ -946,9 +946,14 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
             dp.g = g; dp.w = w;
             dp.gate = P->d_gate;
-            // the wave gate needs the whole grid co-resident and pays only over several
-            // waves; the host path's overlapping launches run without it
-            const bool gate = P->dmma_gate && ntasks >= 4LL * grid;
+            // Wave gate: off by default since the one-CTA-per-SM 256x64 kernel keeps its
+            // persistent CTAs close enough on its own (58 GB of DRAM reads per n=16384
+            // launch without, 53 GB with, at -0.1..0.3%; the two-CTA 64x128 kernel needed
+            // it: 250 -> 51 GB).  STARMM_DMMA_GATE=1 turns it on; it needs the whole grid
+            // co-resident and pays only over several waves, and the host path's
+            // overlapping launches never use it.
+            const char* genv = getenv("STARMM_DMMA_GATE");
+            const bool gate = genv && genv[0] == '1' && P->dmma_gate && ntasks >= 4LL * grid;
             rc = launch_dmma(dp, grid, gate, s);
         } else {
             SimtParams sp;

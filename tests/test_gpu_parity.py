@@ -192,9 +192,11 @@ def test_spec_soft_throughput_gate(sid):
     assert med["sar"] <= 1.15 * med["co3"], med
 
 
-def test_dmma_wave_gate_with_concurrent_launches():
+def test_dmma_wave_gate_with_concurrent_launches(monkeypatch):
     """Two gated DMMA launches on two streams at once (neither grid fully co-resident):
-    the bounded gate wait turns itself off instead of stalling, results stay correct."""
+    the bounded gate wait turns itself off instead of stalling, results stay correct.
+    (The gate is opt-in, STARMM_DMMA_GATE=1, for the one-CTA-per-SM kernel.)"""
+    monkeypatch.setenv("STARMM_DMMA_GATE", "1")
     n = 4096
     s = sm.FLOAT_RING
     g = torch.Generator(device="cuda").manual_seed(9)
