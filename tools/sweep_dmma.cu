@@ -53,6 +53,13 @@ int main(int argc, char** argv) {
     run<DmmaCfg<64, 128, 2, 2, 16, 3, 2>, true>("mbar_64x128_s3", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 32, 2, 2>, true>("mbar_64x128_bk32_s2", n, A, B, C, cnt, sms, 24, true);
     run<DmmaCfg<64, 128, 2, 2, 16, 4, 2, true>, true>("mbar_64x128_s4_db", n, A, B, C, cnt, sms, 24, true);
+    if (argc > 2 && argv[2][0] == 'k') {   // 256x64 8x1: k-stage depth vs ring depth at ~200 KB
+        for (int rep = 0; rep < 2; ++rep) {
+            run<DmmaCfg<256, 64, 8, 1, 16, 4, 1>, true, 1, 0>("q256_bk16_s4", n, A, B, C, cnt, sms, 4, true);
+            run<DmmaCfg<256, 64, 8, 1, 16, 4, 1, true>, true, 1, 0>("q256_bk16_s4_db", n, A, B, C, cnt, sms, 4, true);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'r') {   // 256x64 refinements: warp tile shape, raster group
         for (int rep = 0; rep < 2; ++rep) {
             run<DmmaCfg<256, 64, 8, 1, 16, 4, 1>, true, 1, 0>("q256x64_8x1_g6", n, A, B, C, cnt, sms, 6, true);
