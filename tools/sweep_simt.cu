@@ -45,6 +45,15 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
+    if (argc > 2 && argv[2][0] == 'm') {   // one CTA per SM: barrier ring vs mbarrier ring
+        for (int rep = 0; rep < 2; ++rep) {
+            run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1_bar", n, A, B, C, cnt, sms);
+            run<PolI8Dp4a, SrInt64, 1, true>("i64_dp4a_occ1_mbar", n, A, B, C, cnt, sms);
+            run<PolS16x2Min, SrTropF32, 1, false>("s16x2_occ1_bar", n, A, B, C, cnt, sms);
+            run<PolS16x2Min, SrTropF32, 1, true>("s16x2_occ1_mbar", n, A, B, C, cnt, sms);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'd') {   // dp4a k-stage depth
         for (int rep = 0; rep < 2; ++rep) {
             run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_bk64_occ2", n, A, B, C, cnt, sms);
