@@ -49,7 +49,7 @@
 extern "C" {
 #endif
 
-#define STARMM_ABI_VERSION 2
+#define STARMM_ABI_VERSION 3
 
 /* ---- status codes (errors.py:4-41) ------------------------------------- */
 enum starmm_status {
@@ -123,7 +123,26 @@ typedef struct {
     int64_t main_kernel_launches;    /* launches that contributed to main_kernel_ns      */
     int64_t balanced_workers;        /* >0: tar/star ran balanced (uneven) k-slices over this
                                         many workers, shared tiles merged by atomic-madd  */
+    int64_t live_leaves_max;         /* leaf gauge: most leaf tasks observed in flight at once
+                                        (task_enter/base_enter, metrics.py:63-95)         */
+    int64_t guard_syncs;             /* host waits on the range guard (0 once a plan has a
+                                        verdict: the device decides)        */
+    int64_t candidates;              /* paths queued behind the device-side verdict (1: none) */
 } starmm_stats;
+
+/* The device's block pool (pool.py:67-167): one per device, shared by every plan and
+ * one-shot call, surviving across calls until starmm_pool_reset.  Exact-size stacks,
+ * LIFO reuse, blocks never cleared; reuse across streams is ordered on the device. */
+typedef struct {
+    int64_t allocated_bytes;     /* owned by the pool (issued + cached)              */
+    int64_t cached_bytes;        /* on the free stacks                               */
+    int64_t issued_bytes;        /* handed out now                                   */
+    int64_t high_water_bytes;    /* max issued since the last reset                  */
+    int64_t fresh_count;         /* acquisitions served by cudaMalloc                */
+    int64_t reuse_count;         /* acquisitions served from a free stack            */
+    int64_t cross_stream_waits;  /* reuses ordered by cudaStreamWaitEvent            */
+    int64_t trims;               /* cached blocks returned to the driver             */
+} starmm_pool_counts;
 
 int  starmm_abi_version(void);
 const char* starmm_strerror(int status);
@@ -182,6 +201,17 @@ int  starmm_atomic_accumulate(int semiring, void* C, int64_t ldc, const void* P,
 
 /* device facts used by the Python layer for planning / reporting */
 int  starmm_device_sm_count(int device);
+
+/* the device block pool: Pool.acquire / release / reset / snapshot_counts
+ * (pool.py:89-167).  acquire hands out an exact-size block (not cleared) usable on
+ * `stream` (*fresh = 1 when it was newly allocated, like pool.py:99-111); release
+ * returns it, fenced by the work queued on `stream` so far.
+ * discipline: 0 LIFO (the reference), 1 FIFO (the negative control, pool.py:70-74). */
+int  starmm_pool_acquire(int device, int64_t bytes, void* stream, void** out, int* fresh);
+int  starmm_pool_release(int device, void* block, void* stream);
+int  starmm_pool_counts_get(int device, starmm_pool_counts* out);
+int  starmm_pool_reset(int device);
+int  starmm_pool_set_discipline(int device, int fifo);
 
 #ifdef __cplusplus
 }

@@ -12,6 +12,10 @@ Outputs (committed):
   tests/golden/ref_spec.json   -- the SPEC.md known answers, evaluated by the reference
   tests/golden/ref_pr1.npz     -- BASELINE config 1 (PR1): star_mm fp64 n=256 b=32,
                                   A,B ~ U[-1,1) seed 0, C=0, workers=1
+  tests/golden/ref_signed_zero.npz -- tropical (float64) with +-0.0-heavy operands: every
+                                  classical schedule at workers=1, naive_mm and madd, so the
+                                  signed-zero tie rules (semiring.py:56-58 "if v < out",
+                                  np.minimum's second-operand tie) are pinned bit for bit
   tests/golden/ref_tiles.json  -- sha256 of reference-computed 128x128 output tiles at
                                   the BASELINE configs' generators (bench/configs.py),
                                   for the larger configs (pins the sampled-tile oracle)
@@ -70,6 +74,32 @@ def gen_small(ref):
                 out[f"{key}_{name}"] = C.data
     np.savez_compressed(os.path.join(GOLDEN, "ref_small.npz"), **out)
     print("ref_small.npz:", len(out), "arrays")
+
+
+def gen_signed_zero(ref):
+    out = {}
+    s = ref.TROPICAL
+    algos = [("co2", ref.co2), ("co3", ref.co3), ("tar", ref.tar_mm),
+             ("sar", ref.sar_mm), ("star", ref.star_mm)]
+    rng = np.random.default_rng(1911)
+    vals = np.array([0.0, -0.0, 1.0, -1.0, 2.0, np.inf])
+    prob = [0.3, 0.3, 0.1, 0.1, 0.1, 0.1]
+    for b, n in [(1, 4), (2, 8), (4, 16), (8, 32), (16, 32), (32, 32)]:
+        A = rng.choice(vals, (n, n), p=prob)
+        B = rng.choice(vals, (n, n), p=prob)
+        C0 = rng.choice(vals, (n, n), p=prob)
+        key = f"n{n}_b{b}"
+        out[f"{key}_A"], out[f"{key}_B"], out[f"{key}_C0"] = A, B, C0
+        out[f"{key}_naive"] = ref.naive_mm(ref.Matrix(A, s), ref.Matrix(B, s), s).data
+        for name, fn in algos:
+            C = ref.Matrix(C0.copy(), s)
+            fn(C, ref.Matrix(A, s), ref.Matrix(B, s), s, ref.Config(base_dim=b, workers=1))
+            out[f"{key}_{name}"] = C.data
+        C = ref.Matrix(C0.copy(), s)
+        ref.madd(C, ref.Matrix(A, s), s)
+        out[f"{key}_madd"] = C.data
+    np.savez_compressed(os.path.join(GOLDEN, "ref_signed_zero.npz"), **out)
+    print("ref_signed_zero.npz:", len(out), "arrays")
 
 
 def gen_spec(ref):
@@ -144,7 +174,7 @@ def gen_tiles(ref):
 if __name__ == "__main__":
     os.makedirs(GOLDEN, exist_ok=True)
     ref = import_reference()
-    which = sys.argv[1:] or ["small", "spec", "pr1", "tiles"]
+    which = sys.argv[1:] or ["small", "spec", "pr1", "tiles", "signed_zero"]
     if "small" in which:
         gen_small(ref)
     if "spec" in which:
@@ -153,3 +183,5 @@ if __name__ == "__main__":
         gen_pr1(ref)
     if "tiles" in which:
         gen_tiles(ref)
+    if "signed_zero" in which:
+        gen_signed_zero(ref)

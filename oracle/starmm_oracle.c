@@ -218,13 +218,15 @@ void oracle_fold_f64(double* C, const double* D, int64_t r, int64_t c,
         for (int64_t j = 0; j < c; ++j) C[i * ldc + j] += D[i * ldd + j];
 }
 
-/* np.minimum: NaN if either operand is NaN. */
+/* np.minimum(C, D): NaN if either operand is NaN; on a tie the SECOND operand wins
+ * (np.minimum(+0.0, -0.0) == -0.0, np.minimum(-0.0, +0.0) == +0.0 -- MINPD order,
+ * pinned by tests/golden/ref_signed_zero.npz). */
 void oracle_fold_min_f64(double* C, const double* D, int64_t r, int64_t c,
                          int64_t ldc, int64_t ldd) {
     for (int64_t i = 0; i < r; ++i)
         for (int64_t j = 0; j < c; ++j) {
             double x = C[i * ldc + j], y = D[i * ldd + j];
-            C[i * ldc + j] = (x != x || y != y) ? NAN : (y < x ? y : x);
+            C[i * ldc + j] = (x != x || y != y) ? NAN : (x < y ? x : y);
         }
 }
 
@@ -233,7 +235,7 @@ void oracle_fold_min_f32(float* C, const float* D, int64_t r, int64_t c,
     for (int64_t i = 0; i < r; ++i)
         for (int64_t j = 0; j < c; ++j) {
             float x = C[i * ldc + j], y = D[i * ldd + j];
-            C[i * ldc + j] = (x != x || y != y) ? NAN : (y < x ? y : x);
+            C[i * ldc + j] = (x != x || y != y) ? NAN : (x < y ? x : y);
         }
 }
 

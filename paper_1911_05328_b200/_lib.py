@@ -30,7 +30,8 @@ PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f
               8: "simt_f64_min", 9: "simt_i64_dp4a", 10: "simt_f32_s16x2_viaddmnmx",
               11: "simt_i32_s16x2_viaddmnmx", 12: "simt_f64trop_s16x2_viaddmnmx",
               13: "simt_f64trop_via_f32_carrier", 14: "tcgen05_i8_umma",
-              15: "ozaki2_fp64_tcgen05_i8x16"}
+              15: "ozaki2_fp64_tcgen05_i8x16", 16: "minplus_ordered_leaf_order"}
+ABI_VERSION = 3
 
 
 class StarmmStats(ctypes.Structure):
@@ -39,7 +40,18 @@ class StarmmStats(ctypes.Structure):
         "pool_reuse_count", "tile_serializations", "pair_count", "pair_transitions",
         "lazy_temp_acquires", "raw_alloc_count", "raw_alloc_bytes", "tasks", "workers",
         "ksplit", "tar_levels", "kernel_launches", "path", "executes", "main_kernel_ns",
-        "main_kernel_launches", "balanced_workers")]
+        "main_kernel_launches", "balanced_workers", "live_leaves_max", "guard_syncs",
+        "candidates")]
+
+    def to_dict(self):
+        return {name: int(getattr(self, name)) for name, _ in self._fields_}
+
+
+class PoolCounts(ctypes.Structure):
+    """starmm_pool_counts: the device block pool's counters (pool.py:158-167)."""
+    _fields_ = [(name, ctypes.c_int64) for name in (
+        "allocated_bytes", "cached_bytes", "issued_bytes", "high_water_bytes", "fresh_count",
+        "reuse_count", "cross_stream_waits", "trims")]
 
     def to_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}
@@ -107,7 +119,17 @@ def lib():
         L.starmm_madd.restype = ci
         L.starmm_atomic_accumulate.argtypes = [ci, vp, i64, vp, i64, i64, i64, vp, ci]
         L.starmm_atomic_accumulate.restype = ci
-        if L.starmm_abi_version() != 2:
+        L.starmm_pool_acquire.argtypes = [ci, i64, vp, ctypes.POINTER(vp), ctypes.POINTER(ci)]
+        L.starmm_pool_acquire.restype = ci
+        L.starmm_pool_release.argtypes = [ci, vp, vp]
+        L.starmm_pool_release.restype = ci
+        L.starmm_pool_counts_get.argtypes = [ci, ctypes.POINTER(PoolCounts)]
+        L.starmm_pool_counts_get.restype = ci
+        L.starmm_pool_reset.argtypes = [ci]
+        L.starmm_pool_reset.restype = ci
+        L.starmm_pool_set_discipline.argtypes = [ci, ci]
+        L.starmm_pool_set_discipline.restype = ci
+        if L.starmm_abi_version() != ABI_VERSION:
             raise errors.NativeUnavailable("libstarmm_b200.so ABI version mismatch")
         _lib = L
     return _lib
@@ -192,3 +214,31 @@ def ipc_open(handle: bytes) -> int:
 
 def ipc_close(ptr: int) -> None:
     check(lib().starmm_ipc_close(ptr), "starmm_ipc_close")
+
+
+# ---- the device block pool (starmm_pool_*, csrc/arena.h) ----------------------
+def pool_acquire(device: int, nbytes: int, stream: int = 0):
+    """(device pointer, fresh) of an exact-size block from the device's pool."""
+    out = ctypes.c_void_p()
+    fresh = ctypes.c_int(0)
+    check(lib().starmm_pool_acquire(device, nbytes, stream, ctypes.byref(out), ctypes.byref(fresh)),
+          "starmm_pool_acquire")
+    return int(out.value), bool(fresh.value)
+
+
+def pool_release(device: int, ptr: int, stream: int = 0) -> None:
+    check(lib().starmm_pool_release(device, ptr, stream), "starmm_pool_release")
+
+
+def pool_counts(device: int) -> dict:
+    c = PoolCounts()
+    check(lib().starmm_pool_counts_get(device, ctypes.byref(c)), "starmm_pool_counts_get")
+    return c.to_dict()
+
+
+def pool_reset(device: int) -> None:
+    check(lib().starmm_pool_reset(device), "starmm_pool_reset")
+
+
+def pool_set_discipline(device: int, fifo: bool) -> None:
+    check(lib().starmm_pool_set_discipline(device, 1 if fifo else 0), "starmm_pool_set_discipline")

@@ -6,9 +6,15 @@ absent from the reference package).
   python -m paper_1911_05328_b200 verify [--suite correctness|space|all]
 
 Exit codes: 0 ok, 1 verification failure, 2 invalid input.
-`run` and `verify` check every schedule against ``naive_mm`` (kernels.py:28-32)
--- here the single-pass device product -- exactly for int / (min,+) and within
-rel 1e-9 for float.  `bench` reports the paper's speedup formula
+`run` and `verify` check every schedule against an INDEPENDENT plain-PyTorch
+product (the role of ``naive_mm``, kernels.py:28-32, which on this build would run
+the same tile kernels as the schedules): torch.matmul in float64 and int64 (wraps
+mod 2^64) on the CPU, and a broadcast (min,+) reduction in the k order of the
+reference for the tropical semirings -- exactly for int / (min,+) and within rel
+1e-9 for float.  `verify --suite pool` is the allocator's property
+test (one fresh block per size, LIFO re-issue order) on the DEVICE
+pool; `--sabotage-lifo` runs every suite with the device pool in FIFO order, the
+reference's negative control (pool.py:70-74), and must exit 1.  `bench` reports the paper's speedup formula
 (t_peer / t_algo - 1) * 100% against CO2 and CO3, with one
 shared base kernel and one b per comparison set (the fairness rule,
 PAPER.md:1464-1467).  `analyze` and `simulate` belong to the analysis engine,
@@ -26,7 +32,6 @@ import time
 
 import numpy as np
 
-from . import kernels
 from .errors import StarMMError
 from .matrix import Config, Matrix, matrices_equal, random_matrix
 from .registry import ALGORITHMS, CLASSICAL, run_algorithm
@@ -34,6 +39,29 @@ from .runtime import Executor
 from .semiring import get_semiring
 
 EXIT_OK, EXIT_MISMATCH, EXIT_INVALID = 0, 1, 2
+
+
+def _torch_fold_product(s, C0, A, B):
+    """fold_add(C0, A (x) B) in plain PyTorch on the CPU, independent of libstarmm's
+    kernels: the checker of `run` / `verify`.  (min,+): first minimum over k in
+    increasing k order (semiring.py:56-58), then np.minimum's tie rule (the second
+    operand, the product, wins a tie) -- so signed zeros agree too."""
+    import torch
+    C0, A, B = (x.detach().cpu() for x in (C0, A, B))
+    if s.id in ("int", "float"):
+        return C0 + A @ B                       # int64 wraps mod 2^64 like _mm_int
+    if s.id == "tropical_i32":
+        a, b = A.to(torch.int64), B.to(torch.int64)
+        inf = 2 ** 31 - 1
+        v = (a[:, :, None] + b[None, :, :]).clamp(-2 ** 31, inf)
+        v = torch.where((a[:, :, None] == inf) | (b[None, :, :] == inf), torch.full_like(v, inf), v)
+        return torch.minimum(C0.to(torch.int64), v.min(dim=1).values).to(torch.int32)
+    out = torch.full(C0.shape, float("inf"), dtype=C0.dtype)
+    for kk in range(A.shape[1]):               # "if v < out": NaN never wins, first zero kept
+        v = A[:, kk:kk + 1] + B[kk:kk + 1, :]
+        out = torch.where(v < out, v, out)
+    res = torch.where(C0 < out, C0, out)       # np.minimum(C0, out): a tie keeps out
+    return torch.where(torch.isnan(C0), C0, res)
 
 
 def _one(algo, sid, n, b, p, seed, mode="pooled", ksplit=None):
@@ -47,8 +75,7 @@ def _one(algo, sid, n, b, p, seed, mode="pooled", ksplit=None):
     with Executor(cfg) as ex:
         run_algorithm(ex, algo, C, A, B, s, mode=mode)
         snap = ex.metrics.snapshot(ex.pool).to_dict()
-    want = Matrix(C0.data.clone(), s)
-    s.fold_add(want.data, kernels.naive_mm(A, B, s).data)
+    want = Matrix(_torch_fold_product(s, C0.data, A.data, B.data), s)
     ok = matrices_equal(C, want) if sid != "float" else matrices_equal(
         C.numpy(), want.numpy(), tol=1e-9)
     diff = None
@@ -118,10 +145,63 @@ def cmd_bench(args) -> int:
     return EXIT_OK
 
 
+def _pool_suite():
+    """SPEC.md:562 on the device pool: a released block is the next one issued for its
+    size (one fresh allocation however often it cycles), and two released blocks come
+    back newest first; sizes are independent of each other."""
+    import torch
+    from . import _lib
+    dev = torch.cuda.current_device()
+    fresh, order_ok = 0, True
+    sizes = [3 << 20, 5 << 20]                 # sizes no schedule of this run asks for
+    for nb in sizes:
+        a, f = _lib.pool_acquire(dev, nb)
+        fresh += f
+        for _ in range(100):                   # release / acquire cycles: always `a`
+            _lib.pool_release(dev, a)
+            a2, f = _lib.pool_acquire(dev, nb)
+            fresh += f
+            order_ok &= a2 == a
+            a = a2
+        b, f = _lib.pool_acquire(dev, nb)
+        fresh += f
+        _lib.pool_release(dev, a)
+        _lib.pool_release(dev, b)
+        x, _ = _lib.pool_acquire(dev, nb)
+        y, _ = _lib.pool_acquire(dev, nb)
+        order_ok &= (x, y) == (b, a)           # LIFO re-issue (pool.py:97)
+        _lib.pool_release(dev, y)
+        _lib.pool_release(dev, x)
+    return {"fresh_allocations": int(fresh), "fresh_allowed": 2 * len(sizes),
+            "lifo_reissue_order": bool(order_ok)}
+
+
 def cmd_verify(args) -> int:
     """Acceptance suites, GPU analogues."""
+    import torch
+    from . import _lib
     report = {"suites": {}}
     failed = False
+    dev = torch.cuda.current_device()
+    if args.sabotage_lifo:
+        _lib.pool_set_discipline(dev, True)
+        report["sabotage"] = "device pool in FIFO order"
+    try:
+        failed = _verify_suites(args, report)
+    finally:
+        if args.sabotage_lifo:
+            _lib.pool_set_discipline(dev, False)
+    report["status"] = "fail" if failed else "ok"
+    print(json.dumps(report))
+    return EXIT_MISMATCH if failed else EXIT_OK
+
+
+def _verify_suites(args, report) -> bool:
+    failed = False
+    if args.suite in ("pool", "all"):
+        res = _pool_suite()
+        report["suites"]["pool"] = res
+        failed |= not (res["lifo_reissue_order"] and res["fresh_allocations"] <= res["fresh_allowed"])
     if args.suite in ("correctness", "all"):
         res = []
         for sid in ("int", "tropical", "float"):
@@ -150,9 +230,7 @@ def cmd_verify(args) -> int:
         report["suites"]["space"] = {"bounds": rows, "sar_serial_zero_temps": sar_serial,
                                      "pair_transitions_2_per_pair": pairs_ok}
         failed |= not (sar_serial and pairs_ok)
-    report["status"] = "fail" if failed else "ok"
-    print(json.dumps(report))
-    return EXIT_MISMATCH if failed else EXIT_OK
+    return failed
 
 
 def main(argv=None) -> int:
@@ -177,7 +255,9 @@ def main(argv=None) -> int:
     bn.add_argument("--seed", type=int, default=1)
     bn.add_argument("--out", default=None)
     v = sub.add_parser("verify")
-    v.add_argument("--suite", default="all", choices=["correctness", "space", "all"])
+    v.add_argument("--suite", default="all", choices=["correctness", "space", "pool", "all"])
+    v.add_argument("--sabotage-lifo", action="store_true",
+                   help="negative control: run with the device pool in FIFO order (must exit 1)")
     v.add_argument("--seeds", type=int, default=2)
     v.add_argument("--p", type=int, default=4)
     for name in ("analyze", "simulate"):

@@ -13,7 +13,11 @@ namespace starmm {
 
 // Running range guard fused into the packers (one read of A and B instead of two):
 // out[0] = max |x| over the real (non-padding) elements read, +inf / INT32_MAX
-// excluded; out[1] |= 1 if a float is non-integral, NaN or -inf.
+// excluded; out[1] |= GUARD_BAD if a float is non-integral, NaN or -inf, and
+// |= GUARD_NEG_ZERO if a float is -0.0 (the narrow encodings drop the sign of zero,
+// and the reference's leaf order decides which zero survives: such operands take
+// the ordered kernel, ordered_kernel.cuh).
+constexpr unsigned GUARD_BAD = 1u, GUARD_NEG_ZERO = 2u;
 struct RangeAcc {
     unsigned long long m = 0;
     unsigned bad = 0;
@@ -28,13 +32,15 @@ struct RangeAcc {
     }
     STARMM_DEV void add(float f) {
         if (f == __int_as_float(0x7f800000)) return;
-        if (!(f == rintf(f)) || fabsf(f) > 1e9f) { bad = 1; return; }
+        if (__float_as_uint(f) == 0x80000000u) { bad |= GUARD_NEG_ZERO; return; }
+        if (!(f == rintf(f)) || fabsf(f) > 1e9f) { bad |= GUARD_BAD; return; }
         unsigned long long a = (unsigned long long)fabsf(f);
         m = a > m ? a : m;
     }
     STARMM_DEV void add(double d) {
         if (d == __longlong_as_double(0x7ff0000000000000LL)) return;
-        if (!(d == rint(d)) || fabs(d) > 1e9) { bad = 1; return; }
+        if ((unsigned long long)__double_as_longlong(d) == 0x8000000000000000ull) { bad |= GUARD_NEG_ZERO; return; }
+        if (!(d == rint(d)) || fabs(d) > 1e9) { bad |= GUARD_BAD; return; }
         unsigned long long a = (unsigned long long)fabs(d);
         m = a > m ? a : m;
     }
@@ -51,7 +57,8 @@ struct RangeAcc {
         // on one L2 line were most of the int8 transpose packer's time.
         if ((threadIdx.x & 31) == 0) {
             if (m && m > *reinterpret_cast<volatile unsigned long long*>(&out[0])) atomicMax(&out[0], m);
-            if (bad && !*reinterpret_cast<volatile unsigned long long*>(&out[1])) atomicOr(&out[1], 1ull);
+            if (bad && (*reinterpret_cast<volatile unsigned long long*>(&out[1]) & bad) != bad)
+                atomicOr(&out[1], (unsigned long long)bad);
         }
     }
 };
@@ -174,7 +181,8 @@ __global__ void pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, 
 template <class Tin, class Tp, int G, class Conv>
 __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long long lda,
                               Tp* P, long long rowsp, long long kp, Tp pad,
-                              unsigned long long* range = nullptr) {
+                              unsigned long long* range = nullptr, Pred pr = Pred()) {
+    if (pr.off()) return;
     __shared__ Tp tile[32][33];
     RangeAcc acc;
     long long r0 = (long long)blockIdx.y * 32, k0 = (long long)blockIdx.x * 32;
@@ -203,7 +211,8 @@ __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long
 template <class Tin, class Tp, int G, class Conv>
 __global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long long ldb,
                               Tp* P, long long colsp, long long kp, Tp pad,
-                              unsigned long long* range = nullptr) {
+                              unsigned long long* range = nullptr, Pred pr = Pred()) {
+    if (pr.off()) return;
     RangeAcc acc;
     for (long long kg = blockIdx.y; kg < kp / G; kg += gridDim.y)   // 2-D grid, no division
         for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < colsp;
@@ -233,7 +242,8 @@ __global__ void publish_range_kernel(const unsigned long long* d_range, unsigned
 // 2-D grids (x: columns, y: rows, grid-stride in both) -- no 64-bit division per element
 template <class T>
 __global__ void pad_copy_kernel(const T* src, long long rows, long long cols, long long ld,
-                                T* dst, long long rp, long long cp) {
+                                T* dst, long long rp, long long cp, Pred pr = Pred()) {
+    if (pr.off()) return;
     for (long long r = blockIdx.y; r < rp; r += gridDim.y)
         for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cp;
              c += (long long)gridDim.x * blockDim.x)
@@ -241,24 +251,29 @@ __global__ void pad_copy_kernel(const T* src, long long rows, long long cols, lo
 }
 
 template <class Sr>
-__global__ void fill_kernel(typename Sr::T* C, long long rows, long long cols, long long ld) {
+__global__ void fill_kernel(typename Sr::T* C, long long rows, long long cols, long long ld, Pred pr = Pred()) {
+    if (pr.off()) return;
     for (long long r = blockIdx.y; r < rows; r += gridDim.y)
         for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
              c += (long long)gridDim.x * blockDim.x)
             C[r * ld + c] = Sr::identity();
 }
 
-// C <- C (+) D.  atomic = 1 merges with the semiring's atomic-madd.
+// C <- C (+) D.  atomic = 1 merges with the semiring's atomic-madd; rev = 1 folds in
+// the other order, C <- D (+) C (D came first in k order: the host path's C0, whose
+// place in the reference's fold sequence is before every leaf -- only the sign of a
+// tied zero can tell the two orders apart, common.cuh nan_min).
 template <class Sr>
 __global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr::T* D, long long ldd,
-                            long long rows, long long cols, int atomic) {
+                            long long rows, long long cols, int atomic, int rev = 0, Pred pr = Pred()) {
+    if (pr.off()) return;
     for (long long r = blockIdx.y; r < rows; r += gridDim.y)
         for (long long c = (long long)blockIdx.x * blockDim.x + threadIdx.x; c < cols;
              c += (long long)gridDim.x * blockDim.x) {
             typename Sr::T d = D[r * ldd + c];
             typename Sr::T* p = &C[r * ldc + c];
             if (atomic) Sr::atomic_fold(p, d);
-            else *p = Sr::fold(*p, d);
+            else *p = rev ? Sr::fold(d, *p) : Sr::fold(*p, d);
         }
 }
 

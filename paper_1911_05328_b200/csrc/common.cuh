@@ -17,6 +17,17 @@
 
 namespace starmm {
 
+// Device-side path predicate.  The range guard's verdict is computed on the device
+// (select_path_kernel, aux_kernels.cuh) into one word; every launch of a candidate
+// path after it carries (sel, id) and returns at once unless *sel == id.  So the host
+// queues the whole call without waiting for the guard (STARMM_F_ASYNC holds on every
+// path) and exactly one candidate does the work.  sel == nullptr: unconditional.
+struct Pred {
+    const unsigned* sel = nullptr;
+    unsigned id = 0;
+    STARMM_DEV bool off() const { return sel != nullptr && *reinterpret_cast<const volatile unsigned*>(sel) != id; }
+};
+
 // ---------------------------------------------------------------------------
 // Semiring traits over the OUTPUT element type (the C matrix type).
 //   identity(): additive identity (semiring.py:130-145: 0 / 0.0 / +inf)
@@ -41,10 +52,12 @@ struct SrFp64 {             // "float": float64 (+,x)
     static STARMM_DEV void atomic_fold(T* p, T d) { atomicAdd(p, d); }
 };
 
-// np.minimum semantics: NaN if either operand is NaN (semiring.py:126-127).
+// np.minimum(C, D) semantics (semiring.py:126-127): NaN if either operand is NaN, and
+// on a tie the SECOND operand -- np.minimum(+0.0, -0.0) is -0.0 and
+// np.minimum(-0.0, +0.0) is +0.0 (x86 MINPD order; measured, tests/golden/ref_signed_zero.npz).
 template <class F>
 STARMM_DEV F nan_min(F c, F d) {
-    return (c != c || d != d) ? (c != c ? c : d) : (d < c ? d : c);
+    return (c != c || d != d) ? (c != c ? c : d) : (c < d ? c : d);
 }
 
 struct SrTropF64 {          // "tropical": float64 (min,+), +inf identity
@@ -137,7 +150,9 @@ enum PairSt : int { PAIR_EMPTY = 0, PAIR_FIRST_RUNNING = 1, PAIR_FIRST_DONE = 2 
 // Device-side counters (stats), one array of 64-bit words.
 enum Counter : int {
     CNT_SERIALIZATIONS = 0, CNT_PAIR_TRANSITIONS, CNT_LAZY_ACQUIRES, CNT_POOL_ACQUIRES,
-    CNT_POOL_FRESH, CNT_POOL_ISSUED, CNT_POOL_HIGH_WATER, CNT_PAIRS, CNT__N
+    CNT_POOL_FRESH, CNT_POOL_ISSUED, CNT_POOL_HIGH_WATER, CNT_PAIRS,
+    CNT_LIVE, CNT_LIVE_MAX,          // leaf gauge: leaves in flight now / at most (metrics.py:63-95)
+    CNT__N
 };
 
 struct WbParams {
@@ -175,6 +190,20 @@ STARMM_DEV int task_mode(const WbParams& w, const TaskGrid& g, int s) {
 
 STARMM_DEV void counter_add(const WbParams& w, int c, unsigned long long v) {
     atomicAdd(&w.counters[c], v);
+}
+
+// Live leaf gauge, the GPU form of the reference's task_enter / base_enter
+// (metrics.py:63-95): thread 0 of a CTA counts its leaf task (output tile x k-slice)
+// in on entry and out on exit; the maximum observed is how many leaves really ran
+// concurrently (not a formula of the grid).  One atomic pair per leaf.
+STARMM_DEV void leaf_enter(const WbParams& w) {
+    if (threadIdx.x == 0) {
+        const unsigned long long now = atomicAdd(&w.counters[CNT_LIVE], 1ull) + 1ull;
+        atomicMax(&w.counters[CNT_LIVE_MAX], now);
+    }
+}
+STARMM_DEV void leaf_exit(const WbParams& w) {
+    if (threadIdx.x == 0) atomicAdd(&w.counters[CNT_LIVE], ~0ull);   // -1
 }
 
 STARMM_DEV void lock_slot(int* slot) {

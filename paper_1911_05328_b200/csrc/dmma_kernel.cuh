@@ -64,6 +64,7 @@ struct DmmaParams {
     TaskGrid g;
     WbParams w;
     unsigned* gate = nullptr;         // wave gate counter (zeroed per launch), GATE builds only
+    Pred pr;                          // device-side path predicate (common.cuh)
 };
 
 template <class K>
@@ -222,6 +223,7 @@ STARMM_DEV void mbar_wait(unsigned long long* bar, unsigned parity) {
 // wave's A/B panel slices are shared in L2 instead of re-read from DRAM.
 template <class K, int EPI = 0, int GATE = 0>
 __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb(DmmaParams p) {
+    if (p.pr.off()) return;
     constexpr int BM = K::BM, BN = K::BN, BK = K::BK, STAGES = K::STAGES;
     constexpr int A_LD = K::A_LD, B_LD = K::B_LD, A_STAGE = K::A_STAGE, B_STAGE = K::B_STAGE;
     constexpr int THREADS = K::THREADS, MI = K::MI, NJ = K::NJ;
@@ -269,6 +271,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
         }
         int tm, tn, s, tile;
         decode_task(g, t, tm, tn, s, tile);
+        leaf_enter(p.w);
         const int mode = task_mode(p.w, g, s);
         int pair_seen = PAIR_EMPTY;
         if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
@@ -352,6 +355,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
                     __syncthreads();
                     if (tid == 0) { __threadfence(); atomicAdd(p.gate, 1u); }
                 }
+                leaf_exit(p.w);
                 continue;
             }
         }
@@ -367,6 +371,7 @@ __global__ void __launch_bounds__(K::THREADS, K::MIN_BLOCKS) dmma_fp64_kernel_mb
                     f(r, c + 1, acc[i][j][1]);
                 }
         });
+        leaf_exit(p.w);
         if constexpr (GATE >= 1) {
             __syncthreads();
             if (tid == 0) { __threadfence(); atomicAdd(p.gate, 1u); }

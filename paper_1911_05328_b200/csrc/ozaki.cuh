@@ -147,7 +147,8 @@ __global__ void oz_amax_cols_kernel(const double* B, long long k, long long n, l
 // Grid: x over the k-words of a row, y strides over rows (no divisions).
 __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, long long lda,
                                     const unsigned long long* rowmax, int t, signed char* out,
-                                    long long Mp, long long Kp) {
+                                    long long Mp, long long Kp, Pred pr = Pred()) {
+    if (pr.off()) return;
     const long long plane = Mp * Kp;
     const long long k0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 4;
     if (k0 >= Kp) return;
@@ -178,7 +179,9 @@ __global__ void oz_pack_rows_kernel(const double* A, long long m, long long k, l
 // 32-bit word per plane; the planes leave through a 17-word-pitch transpose tile.
 __global__ void __launch_bounds__(256)
 oz_pack_cols_kernel(const double* B, long long k, long long n, long long ldb,
-                    const unsigned long long* colmax, int t, signed char* out, long long Np, long long Kp) {
+                    const unsigned long long* colmax, int t, signed char* out, long long Np, long long Kp,
+                    Pred pr = Pred()) {
+    if (pr.off()) return;
     constexpr int TK = 64, KW = TK / 4, PITCH = KW + 1;
     __shared__ uint32_t tile[oz::P][32][PITCH];
     const long long c0 = (long long)blockIdx.x * 32, k0 = (long long)blockIdx.y * TK;
@@ -352,7 +355,8 @@ constexpr int OZ_CRT_W = 8;
 __global__ void __launch_bounds__(128)
 oz_crt_kernel(const unsigned char* __restrict__ R, long long Mp, long long Np,
               const unsigned long long* __restrict__ rowmax, const unsigned long long* __restrict__ colmax,
-              int t, const OzCrt crt, const TcgOut o) {
+              int t, const OzCrt crt, const TcgOut o, Pred pr = Pred()) {
+    if (pr.off()) return;
     // grid: x over 8-column groups of a row, y strides over rows (no divisions)
     const long long c0 = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * OZ_CRT_W;
     if (c0 >= o.N) return;

@@ -219,6 +219,7 @@ struct SimtParams {
     long long Mp, Np; // padded extents (multiples of the tile)
     TaskGrid g;
     WbParams w;
+    Pred pr;          // device-side path predicate (common.cuh)
 };
 
 template <class Pol, class Sr, int MINB = 1, bool MB = false>
@@ -226,6 +227,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     using namespace simt;
     using Tp = typename Pol::Tp;
     using Acc = typename Pol::Acc;
+    if (p.pr.off()) return;
     constexpr int G = Pol::G, KSTEP = Pol::KSTEP, OUTS = Pol::OUTS, BK = Pol::BK;
     constexpr int BN = BNW * OUTS;                      // output columns per tile
     constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // positions per 16-byte load
@@ -389,7 +391,9 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
             int mode = WB_RED;
             if (ks == 0 && ke == g.kstages && p.w.remote_parts == 0)
                 mode = p.w.init_identity ? WB_STORE : WB_FOLD;
+            leaf_enter(p.w);
             process(tm, tn, 0, tile, mode, PAIR_EMPTY, ks, (int)(ke - ks));
+            leaf_exit(p.w);
             it += ke - ks;
         }
         return;
@@ -400,7 +404,9 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         const int mode = task_mode(p.w, g, s);
         int pair_seen = PAIR_EMPTY;
         if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
+        leaf_enter(p.w);
         process(tm, tn, s, tile, mode, pair_seen, (long long)s * g.kslice / BK, (int)(g.kslice / BK));
+        leaf_exit(p.w);
     }
 }
 

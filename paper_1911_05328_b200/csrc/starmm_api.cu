@@ -10,10 +10,13 @@
 //                               and Pool (pool.py:67-167): exact-size LIFO stacks,
 //                               blocks never cleared, fresh/reuse/high-water counters
 //   co3 merge ................. ops.merge_tasks (ops.py:108-155)
+//   device pool ............... Pool (pool.py:67-167) shared per device (arena.h)
+//   range guard verdict ....... guard.h, on the device (select_path_kernel)
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <vector>
 #include <type_traits>
 #include <string>
@@ -29,9 +32,14 @@
 #include "aux_kernels.cuh"
 #include "tc_gemm.cuh"
 #include "ozaki.cuh"
+#include "ordered_kernel.cuh"
 #include "simt_launch.h"
+#include "guard.h"
+#include "arena.h"
 
 using namespace starmm;
+using starmm_host::DeviceCtx;
+using starmm_host::FenceRef;
 
 namespace {
 
@@ -62,82 +70,128 @@ int switch_depth(int p) {
     return k;
 }
 
-// ---- the arena: exact-size LIFO free stacks (pool.py:89-132) -----------------
-struct Arena {
-    std::map<size_t, std::vector<void*>> free_stacks;
-    std::vector<std::pair<void*, size_t>> owned;
-    long long total_allocated = 0, issued = 0, high_water = 0, fresh = 0, reuse = 0;
+int current_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return d;
+}
 
-    int acquire(size_t bytes, void** out, bool count_as_temp, long long* fresh_ctr,
-                long long* reuse_ctr) {
-        bytes = (size_t)round_up((long long)std::max<size_t>(bytes, 256), 256);
-        auto& st = free_stacks[bytes];
-        if (!st.empty()) {
-            *out = st.back();             // LIFO pop (pool.py:97)
-            st.pop_back();
-            if (count_as_temp) ++*reuse_ctr;
-        } else {
-            void* p = nullptr;
-            cudaError_t e = cudaMalloc(&p, bytes);
-            if (e != cudaSuccess) return cuda_status(e);
-            owned.push_back({p, bytes});
-            total_allocated += (long long)bytes;
-            *out = p;
-            if (count_as_temp) ++*fresh_ctr;
+// ---- per-device state: the shared block pool and mapped host words ------------
+// Created on first use and never destroyed: the pools' blocks, events and mapped pages
+// are the process's until exit (static destructors would run after the CUDA runtime
+// has started tearing down, and a fence's destructor would touch a destroyed pool).
+DeviceCtx* g_ctx[starmm_host::MAX_DEVICES] = {};
+std::mutex g_ctx_mu;
+// starmm_matmul's plan cache (per device, most recently used last)
+std::mutex& g_mm_mu = *new std::mutex();
+std::vector<starmm_plan*>* g_mm_cache = new std::vector<starmm_plan*>[starmm_host::MAX_DEVICES];
+
+DeviceCtx* device_ctx(int dev) {
+    if (dev < 0 || dev >= starmm_host::MAX_DEVICES) return nullptr;
+    std::lock_guard<std::mutex> g(g_ctx_mu);
+    if (!g_ctx[dev]) g_ctx[dev] = new DeviceCtx();
+    DeviceCtx& c = *g_ctx[dev];
+    if (c.device < 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+            cudaGetLastError();
+            return nullptr;
         }
-        issued += (long long)bytes;
-        high_water = std::max(high_water, issued);
+        size_t fr = 0, tot = 0;
+        int prev = current_device();
+        if (prev != dev) cudaSetDevice(dev);
+        if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) cudaGetLastError();
+        if (prev != dev) cudaSetDevice(prev);
+        // cached blocks are trimmed before the pool owns more than 3/4 of HBM
+        // (STARMM_POOL_LIMIT_MB overrides; an allocation failure always trims and retries)
+        const char* lim = getenv("STARMM_POOL_LIMIT_MB");
+        c.arena.limit = lim ? atoll(lim) * (1LL << 20) : (long long)(tot / 4 * 3);
+        c.arena.device = dev;
+        c.sms = v;
+        c.device = dev;
+    }
+    return &c;
+}
+
+// cudaSetDevice for the duration of a call, restored on every return path
+struct DeviceGuard {
+    int prev = -1, dev = -1;
+    int set(int d) {
+        CK(cudaGetDevice(&prev));
+        dev = d;
+        if (prev != d) CK(cudaSetDevice(d));
         return STARMM_OK;
     }
-    void release(void* p, size_t bytes) {
-        bytes = (size_t)round_up((long long)std::max<size_t>(bytes, 256), 256);
-        free_stacks[bytes].push_back(p);  // blocks are not cleared (pool.py:4-6)
-        issued -= (long long)bytes;
-    }
-    void destroy() {
-        for (auto& o : owned) cudaFree(o.first);
-        owned.clear();
-        free_stacks.clear();
-    }
+    ~DeviceGuard() { if (prev >= 0 && prev != dev) cudaSetDevice(prev); }
 };
 
 struct Block { void* p = nullptr; size_t bytes = 0; };
+
+// per-candidate summary of one execute (the stats describe the path that ran)
+struct CandInfo {
+    int path = 0;
+    long long tasks = 0, workers = 0, S = 1, tar_levels = 0, balanced_workers = 0, pair_count = 0;
+    long long raw_count = 0, raw_bytes = 0;
+    int s_log2 = 0;
+};
 
 }  // namespace
 
 struct starmm_plan {
     int sr, algo, alloc, base_dim, workers, ksplit_req, device, flags;
     long long m, n, k;
+    long long kofs = 0;                         // global k index of the first k (host path chunks)
     int sms = 0;
-    Arena arena;
-    // persistent device bookkeeping (from the arena, kept for the plan's life)
+    DeviceCtx* ctx = nullptr;                   // the device's shared block pool
+    // persistent device bookkeeping (one pool block, kept for the plan's life)
+    void* book = nullptr;
     unsigned long long* d_counters = nullptr;   // CNT__N
-    unsigned long long* d_range = nullptr;      // 2 words
-    // the guard's verdict is published to mapped pinned host memory by a 1-thread kernel
-    // (zero-copy stores, no copy engine: a D2H memcpy here would queue behind the host
-    // path's block downloads on the D2H engine)
-    volatile unsigned long long* h_range = nullptr;
-    unsigned long long* h_range_dev = nullptr;
+    unsigned long long* d_range = nullptr;      // 2 words: max |x|, guard bits
+    unsigned* d_sel = nullptr;                  // the device-side path verdict (Pred::sel)
     unsigned* d_worker_used = nullptr;          // per persistent worker
     unsigned* d_gate = nullptr;                 // DMMA wave-gate counter
+    // mapped pinned host words (zero-copy; a D2H memcpy would queue behind the host
+    // path's downloads on the copy engine): [0..1] range, [2] selected path, [3] the
+    // narrowest allowed path (next call's first guess)
+    unsigned long long* hs = nullptr;
+    unsigned long long* hs_dev = nullptr;
     int dmma_gate = 1;                          // 0 inside the host path (overlapping launches)
     int max_workers = 0;
     starmm_stats st;
+    long long total_allocated = 0;              // bytes this plan's acquisitions cudaMalloc'ed
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
-    cudaEvent_t ev0 = nullptr, ev1 = nullptr;   // STARMM_F_TIME_MAIN
-    int last_guarded_path = 0;                  // optimistic first guess for the next execute
+    cudaEvent_t tev[6] = {};                    // STARMM_F_TIME_MAIN, a pair per candidate
+    int hint = 0;                               // narrowest path the last guard allowed
+    bool spec_used = false;                     // hs[3] carries a device-written hint
     starmm_plan* twin = nullptr;                // host path: the second compute stream's plan
-                                                // (own arena: staging reuse is stream-ordered)
     long long strassen_leaf = 1024;             // Strassen recursion stops at max(b, this)
     long long str_issued = 0;                   // Strassen temporaries currently issued
     // peer destinations of the fused k-split combine (starmm_plan_set_peers)
     int remote_parts = 0;
     long long remote_rows = 0, remote_ld = 0;
     void* remote_base[8] = {};
+    // the last fence recorded on each stream this plan ran on (destroy waits for them)
+    std::vector<FenceRef> fences;
 };
 
 namespace {
+
+// ---- the plan's view of the device pool ------------------------------------
+int plan_acquire(starmm_plan* P, size_t bytes, cudaStream_t s, void** out, bool temp) {
+    bool fresh = false;
+    CK(P->ctx->arena.acquire(bytes, s, out, &fresh));
+    if (fresh) P->total_allocated += (long long)starmm_host::DevArena::size_class(bytes);
+    if (temp) { if (fresh) ++P->ws_fresh; else ++P->ws_reuse; }
+    return STARMM_OK;
+}
+
+void plan_note_fence(starmm_plan* P, const FenceRef& f) {
+    if (!f) return;
+    for (auto& x : P->fences)
+        if (x->st == f->st) { x = f; return; }
+    P->fences.push_back(f);
+}
 
 // ---- kernel instantiation table: PathId in simt_launch.h ----------------------
 
@@ -182,6 +236,10 @@ PathShape path_shape(int path) {
         PathShape sh{2 * tcg::BM, tcg::BN, tcg::BK, 1, 1000LL * oz::P, 1000LL * oz::P};
         return sh;
     }
+    case PATH_MIN_ORDERED: {  // reads A and B in place
+        PathShape sh{ordered::TM, ordered::TN, ordered::TK, 1, 0, 0};
+        return sh;
+    }
     }
     return simt_shape<PolI64>();
 }
@@ -190,15 +248,17 @@ PathShape path_shape(int path) {
 // __syncthreads), vectorised FOLD epilogue.  With `gate` (p.gate zeroed here) the
 // wave gate with a quarter-wave slack keeps the persistent CTAs in step: DRAM reads
 // per n=16384 launch 240-263 GB -> 51 GB at -0.1% (profiles/r01l_dmma_gate.md).
+// The >48 KB smem opt-in is a per-device (per-context) attribute: set once per device.
 int launch_dmma(const DmmaParams& p, int grid, bool gate, cudaStream_t s) {
     using K = DmmaProd;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static bool attr_done[starmm_host::MAX_DEVICES] = {};
+    const int dev = current_device();
+    if (!attr_done[dev]) {
         CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 K::SMEM_BYTES));
         CK(cudaFuncSetAttribute(dmma_fp64_kernel_mb<K, 1, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 K::SMEM_BYTES));
-        attr_done = true;
+        attr_done[dev] = true;
     }
     if (gate && p.gate) {
         CK(cudaMemsetAsync(p.gate, 0, sizeof(unsigned), s));
@@ -213,41 +273,42 @@ int launch_dmma(const DmmaParams& p, int grid, bool gate, cudaStream_t s) {
 
 template <class Sr>
 int launch_madd(void* C, long long ldc, const void* D, long long ldd, long long rows, long long cols,
-                int atomic, cudaStream_t s) {
+                int atomic, cudaStream_t s, int rev = 0, Pred pr = Pred()) {
     if (rows <= 0 || cols <= 0) return STARMM_OK;
     using T = typename Sr::T;
     madd_kernel<Sr><<<grid2d(rows, cols), 256, 0, s>>>((T*)C, ldc, (const T*)D, ldd, rows, cols,
-                                                           atomic);
+                                                           atomic, rev, pr);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
 
 int madd_dispatch(int sr, void* C, long long ldc, const void* D, long long ldd, long long rows,
-                  long long cols, int atomic, cudaStream_t s) {
+                  long long cols, int atomic, cudaStream_t s, int rev = 0, Pred pr = Pred()) {
     switch (sr) {
-    case STARMM_SR_INT64: return launch_madd<SrInt64>(C, ldc, D, ldd, rows, cols, atomic, s);
-    case STARMM_SR_FP64: return launch_madd<SrFp64>(C, ldc, D, ldd, rows, cols, atomic, s);
-    case STARMM_SR_TROPICAL_F64: return launch_madd<SrTropF64>(C, ldc, D, ldd, rows, cols, atomic, s);
-    case STARMM_SR_TROPICAL_F32: return launch_madd<SrTropF32>(C, ldc, D, ldd, rows, cols, atomic, s);
-    case STARMM_SR_TROPICAL_I32: return launch_madd<SrTropI32>(C, ldc, D, ldd, rows, cols, atomic, s);
+    case STARMM_SR_INT64: return launch_madd<SrInt64>(C, ldc, D, ldd, rows, cols, atomic, s, rev, pr);
+    case STARMM_SR_FP64: return launch_madd<SrFp64>(C, ldc, D, ldd, rows, cols, atomic, s, rev, pr);
+    case STARMM_SR_TROPICAL_F64: return launch_madd<SrTropF64>(C, ldc, D, ldd, rows, cols, atomic, s, rev, pr);
+    case STARMM_SR_TROPICAL_F32: return launch_madd<SrTropF32>(C, ldc, D, ldd, rows, cols, atomic, s, rev, pr);
+    case STARMM_SR_TROPICAL_I32: return launch_madd<SrTropI32>(C, ldc, D, ldd, rows, cols, atomic, s, rev, pr);
     }
     return STARMM_CONTRACT_VIOLATION;
 }
 
 template <class Sr>
-int launch_fill(void* C, long long rows, long long cols, long long ld, cudaStream_t s) {
-    fill_kernel<Sr><<<grid2d(rows, cols), 256, 0, s>>>((typename Sr::T*)C, rows, cols, ld);
+int launch_fill(void* C, long long rows, long long cols, long long ld, cudaStream_t s, Pred pr) {
+    fill_kernel<Sr><<<grid2d(rows, cols), 256, 0, s>>>((typename Sr::T*)C, rows, cols, ld, pr);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
 
-int fill_dispatch(int sr, void* C, long long rows, long long cols, long long ld, cudaStream_t s) {
+int fill_dispatch(int sr, void* C, long long rows, long long cols, long long ld, cudaStream_t s,
+                  Pred pr = Pred()) {
     switch (sr) {
-    case STARMM_SR_INT64: return launch_fill<SrInt64>(C, rows, cols, ld, s);
-    case STARMM_SR_FP64: return launch_fill<SrFp64>(C, rows, cols, ld, s);
-    case STARMM_SR_TROPICAL_F64: return launch_fill<SrTropF64>(C, rows, cols, ld, s);
-    case STARMM_SR_TROPICAL_F32: return launch_fill<SrTropF32>(C, rows, cols, ld, s);
-    case STARMM_SR_TROPICAL_I32: return launch_fill<SrTropI32>(C, rows, cols, ld, s);
+    case STARMM_SR_INT64: return launch_fill<SrInt64>(C, rows, cols, ld, s, pr);
+    case STARMM_SR_FP64: return launch_fill<SrFp64>(C, rows, cols, ld, s, pr);
+    case STARMM_SR_TROPICAL_F64: return launch_fill<SrTropF64>(C, rows, cols, ld, s, pr);
+    case STARMM_SR_TROPICAL_F32: return launch_fill<SrTropF32>(C, rows, cols, ld, s, pr);
+    case STARMM_SR_TROPICAL_I32: return launch_fill<SrTropI32>(C, rows, cols, ld, s, pr);
     }
     return STARMM_CONTRACT_VIOLATION;
 }
@@ -255,13 +316,13 @@ int fill_dispatch(int sr, void* C, long long rows, long long cols, long long ld,
 template <class Tin, class Tp, int G, class Conv>
 int launch_pack(const void* A, long long lda, const void* B, long long ldb, long long m,
                 long long n, long long k, void* Ap, void* Bp, long long Mp, long long Np,
-                long long Kp, Tp pad, cudaStream_t s, unsigned long long* range = nullptr) {
+                long long Kp, Tp pad, cudaStream_t s, unsigned long long* range, Pred pr) {
     dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
     pack_a_kernel<Tin, Tp, G, Conv><<<ga, dim3(32, 8), 0, s>>>((const Tin*)A, m, k, lda, (Tp*)Ap, Mp,
-                                                              Kp, pad, range);
+                                                              Kp, pad, range, pr);
     CK(cudaGetLastError());
     pack_b_kernel<Tin, Tp, G, Conv><<<grid2d(Kp / G, Np), 256, 0, s>>>(
-        (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad, range);
+        (const Tin*)B, k, n, ldb, (Tp*)Bp, Np, Kp, pad, range, pr);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
@@ -291,11 +352,14 @@ int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int
 // The CTA-pair tensor-core GEMM over `passes` stacked int8 operand planes
 // (A: passes x [Mp][Kp], B^T: passes x [Np][Kp]); Mp, Np multiples of 256.
 // CTA pairs that can be co-resident (cluster 2x1x1, 1 CTA/SM): the persistent grid,
-// which the drift gate requires to be fully resident
+// which the drift gate requires to be fully resident.  Cached per device (the smem
+// attribute and the SM count are per device).
 template <class Epi>
 int tcg_max_clusters(int sms) {
-    static int cached = -1;
-    if (cached < 0) {
+    static int cached[starmm_host::MAX_DEVICES];
+    static bool init[starmm_host::MAX_DEVICES] = {};
+    const int dev = current_device();
+    if (!init[dev]) {
         auto kern = tcg_kernel<Epi>;
         CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tcg::SMEM_BYTES));
         cudaLaunchConfig_t lc = {};
@@ -309,16 +373,17 @@ int tcg_max_clusters(int sms) {
             cudaGetLastError();
             c = std::max(1, sms / 2);
         }
-        cached = c;
+        cached[dev] = c;
+        init[dev] = true;
     }
-    return cached;
+    return cached[dev];
 }
 
 // `acquire(bytes, &ptr)` hands out stream-ordered scratch (the plan's arena) for the
 // drift-gate counters: one per (pass, tile round), zeroed before the launch.
 template <class Epi, class Acquire>
 int launch_tcg(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp, int passes,
-               const Epi& epi, int sms, cudaStream_t s, Acquire&& acquire) {
+               const Epi& epi, int sms, cudaStream_t s, Acquire&& acquire, Pred pr) {
     if ((long long)passes * Mp >= (1LL << 31) || (long long)passes * Np >= (1LL << 31)) return STARMM_TOO_LARGE;
     CUtensorMap ta, tb;
     TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp * passes, Kp, tcg::BM));
@@ -330,6 +395,7 @@ int launch_tcg(const void* Ap, const void* Bp, long long Mp, long long Np, long 
     sh.group_m = 8;
     sh.nk = (int)(Kp / tcg::BK); sh.passes = passes;
     sh.a_pass_rows = (int)Mp; sh.b_pass_rows = (int)Np;
+    sh.pr = pr;
     const int pairs = std::max(1, std::min(clusters, sh.num_tiles));
     const int grid = 2 * pairs;
     // bounded drift, one wave: 16-pass n=16384 DRAM reads 274 -> 69 GB, GEMM -17%
@@ -360,24 +426,24 @@ TcgOut tcg_out(const starmm_plan* P, void* C, long long ldc, bool init_identity)
 // CRT constants of the Ozaki-II moduli (exact, host side, 128-bit)
 const OzCrt& ozaki_crt() {
     static OzCrt c;
-    static bool done = false;
-    if (done) return c;
-    typedef unsigned __int128 u128;
-    u128 M = 1;
-    for (int p = 0; p < oz::P; ++p) M *= (u128)oz::MOD[p];
-    for (int p = 0; p < oz::P; ++p) {
-        const int m = oz::MOD[p];
-        const u128 Mp = M / (u128)m;
-        const int r = (int)(Mp % (u128)m);
-        int inv = 1;
-        while ((r * inv) % m != 1) ++inv;               // m <= 256: brute force is exact
-        const u128 W = (Mp * (u128)inv) % M;
-        for (int l = 0; l < 4; ++l) c.W[p][l] = (uint32_t)(W >> (32 * l));
-    }
-    const u128 H = M / 2;
-    for (int l = 0; l < 4; ++l) { c.Ml[l] = (uint32_t)(M >> (32 * l)); c.Mh[l] = (uint32_t)(H >> (32 * l)); }
-    c.invM = 1.0 / (double)M;
-    done = true;
+    static std::once_flag once;
+    std::call_once(once, []() {
+        typedef unsigned __int128 u128;
+        u128 M = 1;
+        for (int p = 0; p < oz::P; ++p) M *= (u128)oz::MOD[p];
+        for (int p = 0; p < oz::P; ++p) {
+            const int m = oz::MOD[p];
+            const u128 Mp = M / (u128)m;
+            const int r = (int)(Mp % (u128)m);
+            int inv = 1;
+            while ((r * inv) % m != 1) ++inv;               // m <= 256: brute force is exact
+            const u128 W = (Mp * (u128)inv) % M;
+            for (int l = 0; l < 4; ++l) c.W[p][l] = (uint32_t)(W >> (32 * l));
+        }
+        const u128 H = M / 2;
+        for (int l = 0; l < 4; ++l) { c.Ml[l] = (uint32_t)(M >> (32 * l)); c.Mh[l] = (uint32_t)(H >> (32 * l)); }
+        c.invM = 1.0 / (double)M;
+    });
     return c;
 }
 
@@ -394,23 +460,39 @@ int occupancy_grid(starmm_plan* P, int per_sm, long long tasks) {
     return (int)std::max<long long>(1, std::min<long long>(g, tasks));
 }
 
-int ensure_bookkeeping(starmm_plan* P) {
-    if (P->d_counters) return STARMM_OK;
+// One pool block per plan for its device-side words: counters, the range guard, the
+// path verdict, per-worker flags, the DMMA gate; plus a mapped host slot.
+int ensure_bookkeeping(starmm_plan* P, cudaStream_t s) {
+    if (P->book) return STARMM_OK;
     P->max_workers = P->sms * 2;
-    long long fr = 0, ru = 0;
+    const size_t bytes = CNT__N * 8 + 16 + 16 + (size_t)P->max_workers * 4 + 16;
     void* p = nullptr;
-    size_t bytes = CNT__N * 8 + 16 + (size_t)P->max_workers * 4 + 16;
-    TRY(P->arena.acquire(bytes, &p, false, &fr, &ru));
-    CK(cudaMemset(p, 0, bytes));
+    TRY(plan_acquire(P, bytes, s, &p, false));
+    CK(cudaMemsetAsync(p, 0, bytes, s));
+    P->book = p;
     P->d_counters = (unsigned long long*)p;
     P->d_range = P->d_counters + CNT__N;
-    P->d_worker_used = (unsigned*)(P->d_range + 2);
+    P->d_sel = (unsigned*)(P->d_range + 2);
+    P->d_worker_used = (unsigned*)(P->d_range + 4);
     P->d_gate = P->d_worker_used + P->max_workers;
-    void* h = nullptr;
-    CK(cudaHostAlloc(&h, 16, cudaHostAllocMapped));
-    P->h_range = (volatile unsigned long long*)h;
-    CK(cudaHostGetDevicePointer((void**)&P->h_range_dev, h, 0));
+    CK(P->ctx->slots.get(&P->hs, &P->hs_dev));
     return STARMM_OK;
+}
+
+// The range guard's verdict on the device: the narrowest exact path for the observed
+// range (guard.h), and the candidate that runs -- the first guess if it is exact for
+// this data, else the ordered kernel (-0.0 in a float (min,+) operand) or the general
+// kernel of the semiring.  Published to the plan's mapped host words as well.
+__global__ void select_path_kernel(const unsigned long long* d_range, int sr, int flags, long long k,
+                                   int first, int general, int ordered_ok, unsigned* d_sel,
+                                   unsigned long long* h) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long mx = d_range[0], bits = d_range[1];
+    const int nar = guard_narrowest(sr, flags, k, mx, bits, ordered_ok);
+    const int sel = path_allowed(first, nar) ? first : (nar == PATH_MIN_ORDERED ? PATH_MIN_ORDERED : general);
+    *d_sel = (unsigned)sel;
+    h[0] = mx; h[1] = bits; h[2] = (unsigned long long)sel; h[3] = (unsigned long long)nar;
+    __threadfence_system();
 }
 
 }  // namespace
@@ -450,7 +532,10 @@ const char* starmm_strerror(int status) {
 
 int starmm_device_sm_count(int device) {
     int v = 0;
-    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) return -1;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, device) != cudaSuccess) {
+        cudaGetLastError();
+        return -1;
+    }
     return v;
 }
 
@@ -478,29 +563,34 @@ int starmm_plan_create(starmm_plan** plan, int semiring, int algo, int alloc_mod
     if (m > (1LL << 31) || n > (1LL << 31) || k > (1LL << 31)) return STARMM_TOO_LARGE;
     int ndev = 0;
     CK(cudaGetDeviceCount(&ndev));
-    if (device < 0 || device >= ndev) return STARMM_CONTRACT_VIOLATION;
+    if (device < 0 || device >= ndev || device >= starmm_host::MAX_DEVICES) return STARMM_CONTRACT_VIOLATION;
+    DeviceCtx* ctx = device_ctx(device);
+    if (!ctx) return STARMM_INTERNAL_ERROR;
     starmm_plan* P = new starmm_plan();
     P->sr = semiring; P->algo = algo; P->alloc = alloc_mode; P->base_dim = base_dim;
     P->workers = workers; P->ksplit_req = ksplit_log2; P->device = device; P->flags = flags;
     P->m = m; P->n = n; P->k = k;
     memset(&P->st, 0, sizeof(P->st));
-    P->sms = starmm_device_sm_count(device);
+    P->ctx = ctx;
+    P->sms = ctx->sms;
     *plan = P;
     return STARMM_OK;
 }
 
+// Executor.close (runtime.py:83-93).  Waits only for this plan's own work (the fences
+// of the streams it ran on), never for the device; its blocks go back to the device pool.
 void starmm_plan_destroy(starmm_plan* P) {
     if (!P) return;
-    int prev = 0;
-    cudaGetDevice(&prev);
-    cudaSetDevice(P->device);
-    cudaDeviceSynchronize();
-    if (P->ev0) cudaEventDestroy(P->ev0);
-    if (P->ev1) cudaEventDestroy(P->ev1);
-    if (P->h_range) cudaFreeHost((void*)P->h_range);
+    DeviceGuard dg;
+    dg.set(P->device);
+    for (auto& f : P->fences)
+        if (f && f->ev) cudaEventSynchronize(f->ev);
+    P->fences.clear();
+    for (auto& e : P->tev)
+        if (e) cudaEventDestroy(e);
     if (P->twin) starmm_plan_destroy(P->twin);
-    P->arena.destroy();
-    cudaSetDevice(prev);
+    if (P->book) P->ctx->arena.release(P->book, nullptr);
+    if (P->hs) P->ctx->slots.put(P->hs, P->hs_dev);
     delete P;
 }
 
@@ -528,11 +618,496 @@ int starmm_plan_stats(starmm_plan* P, starmm_stats* out) {
     out->pool_fresh_count = (int64_t)c[CNT_POOL_FRESH] + P->ws_fresh;
     out->pool_reuse_count = (int64_t)(c[CNT_POOL_ACQUIRES] - c[CNT_POOL_FRESH]) + P->ws_reuse;
     out->pool_high_water_bytes = std::max<int64_t>((int64_t)c[CNT_POOL_HIGH_WATER], P->ws_high_water);
-    out->pool_total_allocated_bytes = P->arena.total_allocated;
+    out->pool_total_allocated_bytes = P->total_allocated;
     out->raw_alloc_count = P->raw_count;
     out->raw_alloc_bytes = P->raw_bytes;
+    out->live_leaves_max = (int64_t)c[CNT_LIVE_MAX];
     return STARMM_OK;
 }
+
+}  // extern "C"
+
+// ============================================================================
+// execute: path choice, packing, protocol state, tile kernel, co3 merge
+// ============================================================================
+namespace {
+
+// Geometry of one kernel path on this plan's problem: tiles, occupancy, k-split.
+struct Geom {
+    int path = 0;
+    bool is_dmma = false;
+    PathShape shape{};
+    int BK = 0, TBM = 0, TBN = 0, per_sm = 1, gpu_workers = 0, s_log2 = 0, S = 1, tar_levels = 0;
+    bool balanced = false;
+    long long tiles_m = 0, tiles_n = 0, tiles = 0, Mp = 0, Np = 0, Kp = 0, kslice = 0, ntasks = 0;
+    TaskGrid g{};
+};
+
+int plan_geometry(const starmm_plan* P, int path, Geom& G) {
+    G = Geom();
+    G.path = path;
+    G.is_dmma = (path == PATH_DMMA_F64);
+    G.shape = path_shape(path);
+    G.BK = G.shape.bk; G.TBM = G.shape.bm; G.TBN = G.shape.bn; G.per_sm = G.shape.per_sm;
+    G.tiles_m = (P->m + G.TBM - 1) / G.TBM; G.tiles_n = (P->n + G.TBN - 1) / G.TBN;
+    G.tiles = G.tiles_m * G.tiles_n;
+    G.gpu_workers = P->sms * G.per_sm;                 // persistent CTAs (the GPU workers)
+    if (path == PATH_MIN_ORDERED) {                    // k-serial, one CTA per output tile
+        G.Mp = G.tiles_m * G.TBM; G.Np = G.tiles_n * G.TBN; G.Kp = P->k; G.kslice = P->k;
+        G.ntasks = G.tiles;
+        G.g.tiles_m = (int)G.tiles_m; G.g.tiles_n = (int)G.tiles_n; G.g.S = 1; G.g.num_tasks = (int)G.tiles;
+        return G.tiles_m > 65535 ? STARMM_TOO_LARGE : STARMM_OK;
+    }
+    const bool is_dmma = G.is_dmma;
+    const int BK = G.BK;
+    const long long tiles = G.tiles;
+    const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
+    const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
+    int per_sm = G.per_sm, s_log2 = 0;
+    bool balanced = false;
+    if ((simt_path || is_dmma) && (P->ksplit_req < 0 || !may_split)) {
+        // Pick (CTAs per SM, split depth) by a wave cost model
+        //   time ~ ceil(tasks / CTAs) * (stages per task + overhead) / per-CTA rate
+        // overhead = 4.5 stages of prologue/epilogue per task, plus the split write-back.
+        // The CUDA-core kernels are compiled for two CTAs per SM; launched at one per SM
+        // they run at 0.89 of a full SM, 0.97 for the policies with a one-CTA-per-SM build
+        // (tools/ksplit_ab.py, profiles/r01i_ksplit_c2.json).  co2 never splits
+        // (classic.py:125-128).  The split write-back's cost depends on the schedule's
+        // protocol (tools/ksplit_ab.py, profiles/r01k_ksplit_*.json): TAR atomic-madd 2
+        // stages (20 for the CAS of float minima), CO3 workspace + merge 3, SAR pair states
+        // + locks + lazy temporaries 60 on DMMA (the sibling folds serialise under the tile
+        // lock; measured on the round-1 two-CTA 64x128 DMMA kernel, kept for the one-CTA
+        // 256x64 kernel whose longer stages make the same write-back relatively cheaper)
+        // and 16 on the CUDA-core paths (int64 n=1024: S=2 cost +23%); STAR levels above
+        // switch_depth are TAR, deeper ones SAR.  The DMMA path runs one CTA per SM.
+        const bool cas_min = P->sr == STARMM_SR_TROPICAL_F32 || P->sr == STARMM_SR_TROPICAL_F64;
+        const double pen_tar = cas_min ? 20.0 : 2.0, pen_sar = is_dmma ? 60.0 : 16.0;
+        // (the SAR folds of one tile serialise under its lock: cost grows with the 2^sl
+        // slices per tile -- tropical n=1024, S=8: -27% vs co2 with a flat penalty)
+        auto split_pen = [&](int sl) -> double {
+            if (sl == 0) return 0.0;
+            const double sar = pen_sar * (double)(1 << sl) / 2.0;
+            switch (P->algo) {
+            case STARMM_TAR: return pen_tar;
+            case STARMM_CO3: return 3.0;
+            case STARMM_SAR: return sar;
+            default: return sl <= switch_depth(P->workers) ? pen_tar : sar;   // star
+            }
+        };
+        const double kst = (double)round_up(P->k, BK) / BK;
+        int smax = 0;
+        if (may_split)
+            while (smax < 6 && (P->k >> (smax + 1)) >= std::max(P->base_dim, BK) &&
+                   (tiles << smax) < 8LL * G.gpu_workers)
+                ++smax;
+        double best = 0;
+        int best_occ = per_sm, best_s = 0;
+        for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
+            const bool occ1_build = path == PATH_SIMT_I64_DP4A || path == PATH_SIMT_F32_PAIR ||
+                                    path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER ||
+                                    path == PATH_SIMT_F32_S16X2 || path == PATH_SIMT_I32_S16X2 ||
+                                    path == PATH_SIMT_F64T_S16X2;                // has_occ1_build
+            const double rate1 = occ1_build ? 0.97 : 0.89;
+            const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
+            for (int sl = 0; sl <= smax; ++sl) {
+                const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
+                const double ovh = 4.5 + split_pen(sl);
+                const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
+                if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
+            }
+        }
+        // Balanced slices (TAR with uneven k-slices, "stream-K"): every worker gets the
+        // same share of the flattened (tile, k-stage) space, pieces of shared tiles merge
+        // with the atomic-madd.  Only for tar/star (their split write-back IS the
+        // atomic-madd) and exact, cheap atomics (int64 red.add, int32 red.min).
+        const char* benv = getenv("STARMM_NO_BALANCED");
+        if (simt_path && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
+            (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32) &&
+            P->remote_parts == 0 && !(benv && benv[0] == '1')) {
+            const double Gw = (double)P->sms * per_sm;
+            const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw * per_sm;
+            if (c < 0.97 * best) { balanced = true; best_occ = per_sm; best_s = 0; }
+        }
+        per_sm = best_occ;
+        s_log2 = best_s;
+    } else if (!may_split) {
+        s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
+                               // (the opt-in tensor path keeps whole-K tiles too)
+    } else if (P->ksplit_req >= 0) {
+        s_log2 = P->ksplit_req;
+    }
+    // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels
+    // than the recursion has (log2(k / b))
+    while (s_log2 > 0 && ((P->k >> s_log2) < std::max(P->base_dim, BK) || (P->k >> s_log2) < 1))
+        --s_log2;
+    G.per_sm = per_sm;
+    G.gpu_workers = P->sms * per_sm;
+    G.s_log2 = s_log2;
+    G.S = 1 << s_log2;
+    G.balanced = balanced;
+    G.tar_levels = 0;
+    if (P->algo == STARMM_TAR) G.tar_levels = s_log2;
+    if (P->algo == STARMM_STAR) G.tar_levels = std::min(switch_depth(P->workers), s_log2);
+    G.Mp = G.tiles_m * G.TBM; G.Np = G.tiles_n * G.TBN;
+    G.Kp = round_up(P->k, std::max<long long>(32, (long long)BK * G.S));
+    G.kslice = G.Kp / G.S;
+    TaskGrid& g = G.g;
+    g.tiles_m = (int)G.tiles_m; g.tiles_n = (int)G.tiles_n; g.S = G.S; g.log2S = s_log2;
+    g.tar_levels = G.tar_levels; g.kslice = G.kslice;
+    // raster groups sized so one wave of resident CTAs covers a near-square block of
+    // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
+    g.group_m = is_dmma ? 4 : 12;   // DMMA: 4 x 256 rows (58 GB vs 61 GB at 6), SIMT 12 x 128
+    g.balanced = balanced ? 1 : 0;
+    g.kstages = G.Kp / std::max(1, BK);
+    G.ntasks = tiles * G.S;
+    if (G.ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
+    g.num_tasks = (int)G.ntasks;
+    return STARMM_OK;
+}
+
+// DMMA reads A and B in place when the tiles divide the problem and rows are 16-byte
+// aligned; otherwise from zero-padded staging copies
+bool dmma_direct(const starmm_plan* P, const Geom& G, const void* A, long long lda, const void* B,
+                 long long ldb) {
+    return (P->m % G.TBM == 0) && (P->n % G.TBN == 0) && (P->k == G.Kp) &&
+           (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
+}
+
+// staging bytes of the packed operands of a path (0: read in place)
+void packed_bytes(const starmm_plan* P, const Geom& G, const void* A, long long lda, const void* B,
+                  long long ldb, size_t* ab, size_t* bb) {
+    *ab = *bb = 0;
+    if (G.path == PATH_MIN_ORDERED) return;
+    if (G.is_dmma) {
+        if (dmma_direct(P, G, A, lda, B, ldb)) return;
+        *ab = (size_t)(G.Mp * G.Kp * 8);
+        *bb = (size_t)(G.Kp * G.Np * 8);
+        return;
+    }
+    *ab = (size_t)(G.Mp * G.Kp * G.shape.a_bytes_per_km / 1000);
+    *bb = (size_t)(G.Kp * G.Np * G.shape.b_bytes_per_kn / 1000);
+}
+
+struct Exec {
+    starmm_plan* P;
+    cudaStream_t s;
+    std::vector<Block> staged;
+    int launches = 0;
+    unsigned long long* oz_rowmax = nullptr;
+    unsigned long long* oz_colmax = nullptr;
+    int acquire(size_t bytes, void** p) {
+        TRY(plan_acquire(P, bytes, s, p, false));
+        staged.push_back({*p, bytes});
+        return STARMM_OK;
+    }
+};
+
+// Pack (or pad-copy) the operands of `G.path` into pa / pb.  rng: fold the range guard
+// into the same pass.  Returns the operands the tile kernel reads.
+int pack_operands(Exec& x, const Geom& G, const void* A, long long lda, const void* B, long long ldb,
+                  void* pa, void* pb, unsigned long long* rng, Pred pr, const void** opA, long long* olda,
+                  const void** opB, long long* oldb) {
+    starmm_plan* P = x.P;
+    cudaStream_t s = x.s;
+    const long long Mp = G.Mp, Np = G.Np, Kp = G.Kp;
+    *opA = A; *opB = B; *olda = lda; *oldb = ldb;
+    int rc = STARMM_OK;
+    if (G.path == PATH_MIN_ORDERED) return STARMM_OK;
+    if (G.is_dmma) {
+        if (dmma_direct(P, G, A, lda, B, ldb)) return STARMM_OK;
+        pad_copy_kernel<double><<<grid2d(Mp, Kp), 256, 0, s>>>((const double*)A, P->m, P->k, lda,
+                                                                (double*)pa, Mp, Kp, pr);
+        pad_copy_kernel<double><<<grid2d(Kp, Np), 256, 0, s>>>((const double*)B, P->k, P->n, ldb,
+                                                                (double*)pb, Kp, Np, pr);
+        CK(cudaGetLastError());
+        x.launches += 2;
+        *opA = pa; *opB = pb; *olda = Kp; *oldb = Np;
+        return STARMM_OK;
+    }
+    const float finf = std::numeric_limits<float>::infinity();
+    const unsigned s16pad = 16383u | (16383u << 16);
+    switch (G.path) {
+    case PATH_SIMT_F32_PAIR:
+        rc = launch_pack<float, float, 2, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                         Mp, Np, Kp, finf, s, rng, pr); break;
+    case PATH_SIMT_I32_CARRIER:
+        rc = launch_pack<int, float, 2, ConvI32ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                       Mp, Np, Kp, finf, s, rng, pr); break;
+    case PATH_SIMT_I32_VMIN:
+        rc = launch_pack<int, int, 1, ConvI32Vmin>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
+                                                    Np, Kp, (1 << 30) - 1, s, rng, pr); break;
+    case PATH_SIMT_I32_SAT:
+        rc = launch_pack<int, int, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
+                                                     Np, Kp, 0x7fffffff, s, rng, pr); break;
+    case PATH_SIMT_I64:
+        rc = launch_pack<long long, long long, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k,
+                                                                 pa, pb, Mp, Np, Kp, 0LL, s, rng, pr); break;
+    case PATH_SIMT_I64_NARROW:
+        rc = launch_pack<long long, int, 1, ConvI64ToI32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                           Mp, Np, Kp, 0, s, rng, pr); break;
+    case PATH_SIMT_F64_MIN: {
+        const double dinf = std::numeric_limits<double>::infinity();
+        rc = launch_pack<double, double, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa,
+                                                           pb, Mp, Np, Kp, dinf, s, rng, pr); break;
+    }
+    case PATH_SIMT_F64T_CARRIER:
+        rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
+                                                          Mp, Np, Kp, finf, s, rng, pr); break;
+    // the narrow encodings below only ever run as a plan's first guess (never behind a
+    // device-side verdict), so they take no predicate
+    case PATH_SIMT_I64_DP4A:
+        pack_a_s8x4_kernel<<<dim3((unsigned)((Kp / 4 + 31) / 32), (unsigned)(Mp / 32)), dim3(32, 8), 0, s>>>(
+            (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
+        pack_b_s8x4_kernel<<<grid2d(Kp / 4, Np / 2), 256, 0, s>>>(
+            (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
+        rc = cuda_status(cudaGetLastError());
+        break;
+    case PATH_TC_I8:
+        pack_i8_rows_kernel<<<dim3((unsigned)((Kp / 8 + 255) / 256), (unsigned)std::min<long long>(Mp, 4096)), 256, 0, s>>>(
+            (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, Kp, rng);
+        pack_i8_transpose_kernel<<<dim3((unsigned)(Np / 32), (unsigned)((Kp + 127) / 128)), dim3(32, 8), 0, s>>>(
+            (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, Kp, rng);
+        rc = cuda_status(cudaGetLastError());
+        break;
+    case PATH_OZAKI_F64: {
+        // scale pass (and the finiteness guard); residues are packed after the verdict
+        TRY(x.acquire((size_t)Mp * 8, (void**)&x.oz_rowmax));
+        TRY(x.acquire((size_t)Np * 8, (void**)&x.oz_colmax));
+        CK(cudaMemsetAsync(x.oz_colmax, 0, (size_t)Np * 8, s));
+        const int wpb = 8;
+        oz_amax_rows_kernel<<<(unsigned)std::min<long long>((P->m + wpb - 1) / wpb, 148LL * 16), 32 * wpb, 0, s>>>(
+            (const double*)A, P->m, P->k, lda, x.oz_rowmax, rng ? rng + 1 : nullptr);
+        oz_amax_cols_kernel<<<dim3((unsigned)((P->n + 31) / 32), (unsigned)((P->k + 255) / 256)), dim3(32, 8), 0, s>>>(
+            (const double*)B, P->k, P->n, ldb, x.oz_colmax, rng ? rng + 1 : nullptr);
+        rc = cuda_status(cudaGetLastError());
+        break;
+    }
+    case PATH_SIMT_F32_S16X2:
+    case PATH_SIMT_I32_S16X2:
+    case PATH_SIMT_F64T_S16X2: {
+        dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
+        if (G.path == PATH_SIMT_F64T_S16X2) {
+            pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
+            pack_b_s16x2_kernel<double><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+                (const double*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
+        } else if (G.path == PATH_SIMT_F32_S16X2) {
+            pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
+            pack_b_s16x2_kernel<float><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+                (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
+        } else {
+            pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
+                (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
+            pack_b_s16x2_kernel<int><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+                (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
+        }
+        rc = cuda_status(cudaGetLastError());
+        break;
+    }
+    }
+    if (rc) return rc;
+    x.launches += 2;
+    *opA = pa; *opB = pb;
+    return STARMM_OK;
+}
+
+template <class Sr>
+int launch_ordered(const OrderedParams& op, long long tiles_m, long long tiles_n, cudaStream_t s) {
+    minplus_ordered_kernel<Sr><<<dim3((unsigned)tiles_n, (unsigned)tiles_m), ordered::THREADS, 0, s>>>(op);
+    CK(cudaGetLastError());
+    return STARMM_OK;
+}
+
+// Everything after packing for one candidate path: Ozaki residues, protocol state
+// (TileExclusionTable slots, pair states, lazy scratch, co3 workspace), identity fill,
+// the tile kernel and the co3 merge -- every launch behind `pr`.  `ci` receives the
+// candidate's stats.  ev: the candidate's timing pair (nullptr: untimed).
+int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void* A, long long lda,
+                     const void* B, long long ldb, const void* opA, long long olda, const void* opB,
+                     long long oldb, Pred pr, cudaEvent_t* ev, CandInfo& ci) {
+    starmm_plan* P = x.P;
+    cudaStream_t s = x.s;
+    const int eb = elem_bytes(P->sr);
+    const bool init_identity = (P->flags & STARMM_F_INIT_IDENTITY) != 0;
+    const int S = G.S, s_log2 = G.s_log2;
+    const long long tiles = G.tiles, Mp = G.Mp, Np = G.Np, Kp = G.Kp;
+    ci = CandInfo();
+    ci.path = G.path;
+    ci.tasks = G.ntasks;
+    ci.S = S;
+    ci.s_log2 = s_log2;
+    ci.tar_levels = G.tar_levels;
+    int rc = STARMM_OK;
+    if (G.path == PATH_MIN_ORDERED) {
+        OrderedParams op;
+        op.A = A; op.lda = lda; op.B = B; op.ldb = ldb; op.C = C; op.ldc = ldc;
+        op.M = P->m; op.N = P->n; op.K = P->k;
+        op.blk = P->base_dim; op.kofs = P->kofs;
+        op.init_identity = init_identity ? 1 : 0;
+        op.pr = pr;
+        if (ev && (rc = cuda_status(cudaEventRecord(ev[0], s)))) return rc;
+        rc = P->sr == STARMM_SR_TROPICAL_F32 ? launch_ordered<SrTropF32>(op, G.tiles_m, G.tiles_n, s)
+                                             : launch_ordered<SrTropF64>(op, G.tiles_m, G.tiles_n, s);
+        if (rc) return rc;
+        if (ev && (rc = cuda_status(cudaEventRecord(ev[1], s)))) return rc;
+        ++x.launches;
+        ci.workers = std::min<long long>(G.ntasks, (long long)P->sms * 8);
+        return STARMM_OK;
+    }
+    if (G.path == PATH_OZAKI_F64) {   // residue planes for the scales the guard pass found
+        const int t = ozaki_bits(P->k);
+        oz_pack_rows_kernel<<<dim3((unsigned)((Kp / 4 + 255) / 256), (unsigned)std::min<long long>(Mp, 65535)), 256, 0, s>>>(
+            (const double*)A, P->m, P->k, lda, x.oz_rowmax, t, (signed char*)opA, Mp, Kp, pr);
+        oz_pack_cols_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 64)), dim3(32, 8), 0, s>>>(
+            (const double*)B, P->k, P->n, ldb, x.oz_colmax, t, (signed char*)opB, Np, Kp, pr);
+        CK(cudaGetLastError());
+        x.launches += 2;
+    }
+    // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
+    const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
+    void* pstate = nullptr;
+    const size_t state_bytes = need_slots ? (size_t)(tiles + tiles * (S / 2)) * 4 : 0;
+    if (need_slots) {
+        TRY(x.acquire(state_bytes, &pstate));
+        CK(cudaMemsetAsync(pstate, 0, state_bytes, s));
+    }
+    // per-worker lazy-temp blocks (tile sized, for SAR/STAR pairs)
+    void* wscratch = nullptr;
+    const long long tile_elems = (long long)G.TBM * G.TBN;
+    if (need_slots) TRY(x.acquire((size_t)(G.gpu_workers * tile_elems * eb), &wscratch));
+    // co3 workspace D_1..D_{S-1}: pooled (the device pool, reused) or raw (fresh per call)
+    void* W = nullptr;
+    size_t wbytes = 0;
+    if (P->algo == STARMM_CO3 && S > 1) {
+        wbytes = (size_t)(S - 1) * (size_t)P->m * (size_t)P->n * eb;
+        if (P->alloc == STARMM_POOLED) {
+            TRY(plan_acquire(P, wbytes, s, &W, true));
+            x.staged.push_back({W, wbytes});
+        } else {
+            CK(cudaMallocAsync(&W, wbytes, s));
+            ci.raw_count = 1;
+            ci.raw_bytes = (long long)wbytes;
+        }
+        P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
+    }
+    if (init_identity && (S > 1 || G.balanced) && P->algo != STARMM_CO3 && P->remote_parts == 0) {
+        TRY(fill_dispatch(P->sr, C, P->m, P->n, ldc, s, pr));
+        ++x.launches;
+    }
+
+    WbParams w;
+    w.mode_base = P->algo; w.init_identity = init_identity ? 1 : 0;
+    w.C = C; w.ldc = ldc; w.M = P->m; w.N = P->n;
+    w.W = W; w.ldw = P->n; w.wstride = P->m * P->n;
+    w.slots = (int*)pstate;
+    w.pairs = pstate ? (int*)pstate + tiles : nullptr;
+    w.counters = P->d_counters; w.worker_used = P->d_worker_used;
+    w.scratch = wscratch; w.scratch_elems = tile_elems;
+    w.remote_parts = P->remote_parts; w.remote_rows = P->remote_rows; w.remote_ld = P->remote_ld;
+    for (int i = 0; i < 8; ++i) w.remote_base[i] = P->remote_base[i];
+
+    const int grid = occupancy_grid(P, G.per_sm, G.balanced ? G.ntasks * G.g.kstages : G.ntasks);
+    if (ev && (rc = cuda_status(cudaEventRecord(ev[0], s)))) return rc;
+    if (G.path == PATH_TC_I8) {
+        EpiFoldI64 e;
+        e.o = tcg_out(P, C, ldc, init_identity);
+        TRY(launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s,
+                       [&](size_t b, void** p) { return x.acquire(b, p); }, pr));
+    } else if (G.path == PATH_OZAKI_F64) {
+        void* planes = nullptr;
+        TRY(x.acquire((size_t)oz::P * Mp * Np, &planes));
+        EpiOzakiResidues e;
+        e.R = (unsigned char*)planes; e.Mp = Mp; e.Np = Np;
+        TRY(launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s,
+                       [&](size_t b, void** p) { return x.acquire(b, p); }, pr));
+        if (ev && (rc = cuda_status(cudaEventRecord(ev[1], s)))) return rc;
+        const long long groups = (P->n + OZ_CRT_W - 1) / OZ_CRT_W;
+        oz_crt_kernel<<<dim3((unsigned)((groups + 127) / 128), (unsigned)std::min<long long>(P->m, 65535)), 128, 0, s>>>(
+            (const unsigned char*)planes, Mp, Np, x.oz_rowmax, x.oz_colmax, ozaki_bits(P->k), ozaki_crt(),
+            tcg_out(P, C, ldc, init_identity), pr);
+        CK(cudaGetLastError());
+        ++x.launches;
+    } else if (G.is_dmma) {
+        DmmaParams dp;
+        dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
+        dp.g = G.g; dp.w = w;
+        dp.gate = P->d_gate;
+        dp.pr = pr;
+        // Wave gate: off by default since the one-CTA-per-SM 256x64 kernel keeps its
+        // persistent CTAs close enough on its own (58 GB of DRAM reads per n=16384
+        // launch without, 53 GB with, at -0.1..0.3%; the two-CTA 64x128 kernel needed
+        // it: 250 -> 51 GB).  STARMM_DMMA_GATE=1 turns it on; it needs the whole grid
+        // co-resident and pays only over several waves, and the host path's
+        // overlapping launches never use it.
+        const char* genv = getenv("STARMM_DMMA_GATE");
+        const bool gate = genv && genv[0] == '1' && P->dmma_gate && G.ntasks >= 4LL * grid;
+        TRY(launch_dmma(dp, grid, gate, s));
+    } else {
+        SimtParams sp;
+        sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = G.g; sp.w = w;
+        sp.pr = pr;
+        // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
+        CK((cudaError_t)starmm_simt_launch(G.path, sp, grid, P->sms, s));
+    }
+    ++x.launches;
+    if (ev && G.path != PATH_OZAKI_F64 && (rc = cuda_status(cudaEventRecord(ev[1], s)))) return rc;
+
+    // ---- co3: merge the workspace bottom-up (merge_tasks, ops.py:108-155) ----
+    if (P->algo == STARMM_CO3 && S > 1) {
+        const long long slab = P->m * P->n;
+        for (int lvl = s_log2; lvl >= 1; --lvl) {
+            const int step = 1 << (s_log2 - lvl);
+            for (int xx = step; xx < S; xx += 2 * step) {
+                char* src = (char*)W + (size_t)(xx - 1) * slab * eb;
+                const int tgt = xx - step;
+                if (tgt == 0) rc = madd_dispatch(P->sr, C, ldc, src, P->n, P->m, P->n, 0, s, 0, pr);
+                else rc = madd_dispatch(P->sr, (char*)W + (size_t)(tgt - 1) * slab * eb, P->n, src,
+                                        P->n, P->m, P->n, 0, s, 0, pr);
+                if (rc) return rc;
+                ++x.launches;
+            }
+        }
+        if (P->alloc == STARMM_RAW) CK(cudaFreeAsync(W, s));
+    }
+    ci.workers = std::min<long long>(G.ntasks, (long long)P->sms * G.per_sm);
+    ci.balanced_workers = G.balanced ? std::min<long long>(G.ntasks * G.g.kstages, (long long)P->sms * G.per_sm) : 0;
+    if (S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && G.tar_levels < s_log2)
+        ci.pair_count = tiles * (S / 2);
+    return STARMM_OK;
+}
+
+// widest exact path of the semiring (no range condition), and the fastest one to try first
+int general_path(const starmm_plan* P) {
+    switch (P->sr) {
+    case STARMM_SR_FP64: return PATH_DMMA_F64;
+    case STARMM_SR_INT64: return PATH_SIMT_I64;
+    case STARMM_SR_TROPICAL_F64: return PATH_SIMT_F64_MIN;
+    case STARMM_SR_TROPICAL_F32: return PATH_SIMT_F32_PAIR;
+    default: return PATH_SIMT_I32_SAT;
+    }
+}
+int fastest_path(const starmm_plan* P) {
+    const bool fast = !(P->flags & STARMM_F_NO_FASTPATH);
+    if (!fast) return general_path(P);
+    switch (P->sr) {
+    case STARMM_SR_FP64: return (P->flags & STARMM_F_FP64_EMU) && P->k < (1LL << 17) ? PATH_OZAKI_F64 : PATH_DMMA_F64;
+    case STARMM_SR_INT64: return (P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A;
+    case STARMM_SR_TROPICAL_F64: return PATH_SIMT_F64T_S16X2;
+    case STARMM_SR_TROPICAL_F32: return PATH_SIMT_F32_S16X2;
+    default: return PATH_SIMT_I32_S16X2;
+    }
+}
+bool float_min(const starmm_plan* P) {
+    return P->sr == STARMM_SR_TROPICAL_F64 || P->sr == STARMM_SR_TROPICAL_F32;
+}
+// does this call need the range guard?  (a fast path to confirm, or -0.0 to detect)
+bool needs_guard(const starmm_plan* P) {
+    if (fastest_path(P) != general_path(P)) return true;
+    return float_min(P) && P->remote_parts == 0;
+}
+
+}  // namespace
 
 static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
                         const void* B, int64_t ldb, void* stream, bool force_async) {
@@ -540,479 +1115,167 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
     const int eb = elem_bytes(P->sr);
     if (((uintptr_t)C | (uintptr_t)A | (uintptr_t)B) % eb) return STARMM_ALIGNMENT_ERROR;
-    int prev_dev = 0;
-    CK(cudaGetDevice(&prev_dev));
-    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
+    DeviceGuard dg;
+    TRY(dg.set(P->device));
     cudaStream_t s = (cudaStream_t)stream;
-    TRY(ensure_bookkeeping(P));
-    const bool init_identity = (P->flags & STARMM_F_INIT_IDENTITY) != 0;
-    const bool fast_ok = !(P->flags & STARMM_F_NO_FASTPATH);
-    int launches = 0;
+    TRY(ensure_bookkeeping(P, s));
+    const bool async = (P->flags & STARMM_F_ASYNC) || force_async;
+    const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
+    if (timed && !P->tev[0])
+        for (auto& e : P->tev) CK(cudaEventCreate(&e));
+    // an earlier call's device-side verdict (mapped host word; stale is fine: a hint)
+    if (P->spec_used && P->hs[3]) P->hint = (int)P->hs[3];
+    const bool ordered_ok = P->remote_parts == 0;
 
-    // ---- path selection -------------------------------------------------------
+    // ---- path selection ------------------------------------------
     // Range-guarded exact narrow paths are chosen optimistically: the operands are
-    // packed for the fastest kernel while the packers reduce max|x| (and float
-    // integrality) in the same pass; if the guard fails they are re-packed for the
-    // path the observed range allows.
-    int path = 0;
-    bool guard_pending = false;
-    if (P->sr == STARMM_SR_FP64) {
-        // opt-in Ozaki-II emulation on the int8 tensor cores; the guard
-        // (finite inputs) runs in the same pass that finds the per-row/column scales
-        if (fast_ok && (P->flags & STARMM_F_FP64_EMU) && P->k < (1LL << 17)) {
-            path = PATH_OZAKI_F64;
-            guard_pending = true;
-        } else {
-            path = PATH_DMMA_F64;
-        }
-    }
-    else if (P->sr == STARMM_SR_TROPICAL_F64) { path = fast_ok ? PATH_SIMT_F64T_S16X2 : PATH_SIMT_F64_MIN; guard_pending = fast_ok; }
-    else if (P->sr == STARMM_SR_TROPICAL_F32) { path = fast_ok ? PATH_SIMT_F32_S16X2 : PATH_SIMT_F32_PAIR; guard_pending = fast_ok; }
-    else if (P->sr == STARMM_SR_INT64) {
-        path = fast_ok ? ((P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A) : PATH_SIMT_I64;
-        guard_pending = fast_ok;
-    }
-    else { path = fast_ok ? PATH_SIMT_I32_S16X2 : PATH_SIMT_I32_SAT; guard_pending = fast_ok; }
-    // the previous execute's guard outcome is the better first guess (data ranges are
-    // usually stable across calls); the guard itself still runs on every call
-    if (guard_pending && P->last_guarded_path && P->sr != STARMM_SR_FP64) path = P->last_guarded_path;
-
-    // geometry of the chosen path (re-derived if the guard changes the path)
-    bool is_dmma = false;
-    PathShape shape;
-    int BK = 0, TBM = 0, TBN = 0, per_sm = 1, gpu_workers = 0, s_log2 = 0, S = 1, tar_levels = 0;
-    bool balanced = false;
-    long long tiles_m = 0, tiles_n = 0, tiles = 0, Mp = 0, Np = 0, Kp = 0, kslice = 0, ntasks = 0;
-    TaskGrid g;
-    auto plan_geometry = [&]() -> int {
-        is_dmma = (path == PATH_DMMA_F64);
-        shape = path_shape(path);
-        BK = shape.bk; TBM = shape.bm; TBN = shape.bn; per_sm = shape.per_sm;
-        tiles_m = (P->m + TBM - 1) / TBM; tiles_n = (P->n + TBN - 1) / TBN;
-        tiles = tiles_m * tiles_n;
-        gpu_workers = P->sms * per_sm;                  // persistent CTAs (the GPU workers)
-        balanced = false;
-        const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
-        const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
-        if ((simt_path || is_dmma) && (P->ksplit_req < 0 || !may_split)) {
-            // CUDA-core paths: pick (CTAs per SM, split depth) by a wave cost model
-            //   time ~ ceil(tasks / CTAs) * (stages per task + overhead) / per-CTA rate
-            // overhead = 4.5 stages of prologue/epilogue per task, plus the split write-back
-            // (atomics: 2 stages; the CAS loop of the float minima: 20).  The kernels are
-            // compiled for two CTAs per SM; launched at one per SM they run at 0.89 of a
-            // full SM (tools/ksplit_ab.py, profiles/r01i_ksplit_c2.json).  Small problems
-            // such as config 2 (1024 tiles = 3.46 waves of 296 CTAs) then prefer one CTA
-            // per SM (co2: +5.5%) or a split to two.  co2 never splits (classic.py:125-128).
-            // The split write-back's cost depends on the schedule's protocol (tools/ksplit_ab.py,
-            // profiles/r01k_ksplit_*.json; DMMA n=2048: S=2/4 cost +6%/+1.6% for tar -- which the
-            // model reproduces -- and +30%/+48% for sar): TAR atomic-madd 2 stages (20 for the CAS
-            // of float minima), CO3 workspace + merge 3, SAR pair states + locks + lazy
-            // temporaries 60 on DMMA (the sibling folds serialise under the tile lock; n=1024:
-            // +40% at S=2) and 16 on the CUDA-core paths (2-4x longer stages, batched folds;
-            // int64 n=1024: S=2 cost +23%);
-            // STAR levels above switch_depth are TAR, deeper ones SAR.  The DMMA path always
-            // runs two CTAs per SM.
-            const bool cas_min = P->sr == STARMM_SR_TROPICAL_F32 || P->sr == STARMM_SR_TROPICAL_F64;
-            const double pen_tar = cas_min ? 20.0 : 2.0, pen_sar = is_dmma ? 60.0 : 16.0;
-            // (the SAR folds of one tile serialise under its lock: cost grows with the 2^sl
-            // slices per tile -- tropical n=1024, S=8: -27% vs co2 with a flat penalty)
-            auto split_pen = [&](int sl) -> double {
-                if (sl == 0) return 0.0;
-                const double sar = pen_sar * (double)(1 << sl) / 2.0;
-                switch (P->algo) {
-                case STARMM_TAR: return pen_tar;
-                case STARMM_CO3: return 3.0;
-                case STARMM_SAR: return sar;
-                default: return sl <= switch_depth(P->workers) ? pen_tar : sar;   // star
-                }
-            };
-            const double kst = (double)round_up(P->k, BK) / BK;
-            int smax = 0;
-            if (may_split)
-                while (smax < 6 && (P->k >> (smax + 1)) >= std::max(P->base_dim, BK) &&
-                       (tiles << smax) < 8LL * gpu_workers)
-                    ++smax;
-            double best = 0;
-            int best_occ = per_sm, best_s = 0;
-            for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
-                const bool occ1_build = path == PATH_SIMT_I64_DP4A || path == PATH_SIMT_F32_PAIR ||
-                                        path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER ||
-                                        path == PATH_SIMT_F32_S16X2 || path == PATH_SIMT_I32_S16X2 ||
-                                        path == PATH_SIMT_F64T_S16X2;                // has_occ1_build
-                const double rate1 = occ1_build ? 0.97 : 0.89;
-                const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
-                for (int sl = 0; sl <= smax; ++sl) {
-                    const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
-                    const double ovh = 4.5 + split_pen(sl);
-                    const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
-                    if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
-                }
-            }
-            // Balanced slices (TAR with uneven k-slices, "stream-K"): every worker gets the
-            // same share of the flattened (tile, k-stage) space, pieces of shared tiles merge
-            // with the atomic-madd.  Only for tar/star (their split write-back IS the
-            // atomic-madd) and exact, cheap atomics (int64 red.add, int32 red.min).
-            const char* benv = getenv("STARMM_NO_BALANCED");
-            if (simt_path && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
-                (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32) &&
-                P->remote_parts == 0 && !(benv && benv[0] == '1')) {
-                const double Gw = (double)P->sms * per_sm;
-                const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw * per_sm;
-                if (c < 0.97 * best) { balanced = true; best_occ = per_sm; best_s = 0; }
-            }
-            per_sm = best_occ;
-            gpu_workers = P->sms * per_sm;
-            s_log2 = best_s;
-        } else if (!may_split) {
-            s_log2 = 0;            // k-halves serialised (classic.py:125-128): never split
-                                   // (the opt-in tensor path keeps whole-K tiles too)
-        } else if (P->ksplit_req >= 0) {
-            s_log2 = P->ksplit_req;
-        } else {
-            // (the opt-in tcgen05 paths never reach here: they keep whole-K tiles)
-            s_log2 = 0;
-        }
-        // a k-slice is at least one leaf (base_dim) and one k-stage; never more levels
-        // than the recursion has (log2(k / b))
-        while (s_log2 > 0 && ((P->k >> s_log2) < std::max(P->base_dim, BK) || (P->k >> s_log2) < 1))
-            --s_log2;
-        S = 1 << s_log2;
-        tar_levels = 0;
-        if (P->algo == STARMM_TAR) tar_levels = s_log2;
-        if (P->algo == STARMM_STAR) tar_levels = std::min(switch_depth(P->workers), s_log2);
-        Mp = tiles_m * TBM; Np = tiles_n * TBN;
-        Kp = round_up(P->k, std::max<long long>(32, (long long)BK * S));
-        kslice = Kp / S;
-        g.tiles_m = (int)tiles_m; g.tiles_n = (int)tiles_n; g.S = S; g.log2S = s_log2;
-        g.tar_levels = tar_levels; g.kslice = kslice;
-        // raster groups sized so one wave of resident CTAs covers a near-square block of
-        // tiles (minimises the A+B panels live in L2; tools/gsweep.sh: -42% DRAM bytes)
-        g.group_m = is_dmma ? 4 : 12;   // DMMA: 4 x 256 rows (58 GB vs 61 GB at 6), SIMT 12 x 128
-        g.balanced = balanced ? 1 : 0;
-        g.kstages = Kp / std::max(1, BK);
-        ntasks = tiles * S;
-        if (ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
-        g.num_tasks = (int)ntasks;
-        return STARMM_OK;
-    };
-
-    // ---- staging buffers from the arena (not counted as algorithm temps) ----
-    std::vector<Block> staged;
-    auto stage_acquire = [&](size_t bytes, void** p) -> int {
-        long long fr = 0, ru = 0;
-        TRY(P->arena.acquire(bytes, p, false, &fr, &ru));
-        staged.push_back({*p, bytes});
-        return STARMM_OK;
-    };
+    // packed for the fastest path (or the one the last verdict allowed) while the
+    // packers reduce max|x| (and float integrality / -0.0) in the same pass.  The
+    // verdict is then taken ON THE DEVICE (select_path_kernel) and the exact fallback
+    // candidates -- the semiring's general kernel, and for the float (min,+) semirings
+    // the ordered kernel -- are queued behind it with a predicate; exactly one runs.
+    // Only a plan's first blocking call (no verdict to go on yet) reads the guard on
+    // the host, so that it picks the narrowest path at once.
+    Exec x{P, s};
     int rc = STARMM_OK;
-    unsigned long long *oz_rowmax = nullptr, *oz_colmax = nullptr;
-    const void* opA = A; const void* opB = B;
-    long long olda = lda, oldb = ldb;
+    CandInfo info[3];
+    int ncand = 0;
+    bool host_decided = true;
+    const char* genv = getenv("STARMM_GUARD_SYNC");      // 1: always host-side, 0: never
     do {
-      for (;;) {
-        if ((rc = plan_geometry())) break;
-        opA = A; opB = B; olda = lda; oldb = ldb;     // a re-plan starts from the caller's operands
-        unsigned long long* rng = guard_pending ? P->d_range : nullptr;
-        if (rng && (rc = cuda_status(cudaMemsetAsync(rng, 0, 2 * sizeof(unsigned long long), s)))) break;
-        if (is_dmma) {
-            bool direct = (P->m % TBM == 0) && (P->n % TBN == 0) && (P->k == Kp) &&
-                          (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
-            if (!direct) {
-                void *pa, *pb;
-                if ((rc = stage_acquire((size_t)(Mp * Kp * 8), &pa))) break;
-                if ((rc = stage_acquire((size_t)(Kp * Np * 8), &pb))) break;
-                pad_copy_kernel<double><<<grid2d(Mp, Kp), 256, 0, s>>>((const double*)A, P->m, P->k,
-                                                                            lda, (double*)pa, Mp, Kp);
-                pad_copy_kernel<double><<<grid2d(Kp, Np), 256, 0, s>>>((const double*)B, P->k, P->n,
-                                                                            ldb, (double*)pb, Kp, Np);
-                if ((rc = cuda_status(cudaGetLastError()))) break;
-                launches += 2;
-                opA = pa; opB = pb; olda = Kp; oldb = Np;
-            }
-        } else {
-            void *pa, *pb;
-            if ((rc = stage_acquire((size_t)(Mp * Kp * shape.a_bytes_per_km / 1000), &pa))) break;
-            if ((rc = stage_acquire((size_t)(Kp * Np * shape.b_bytes_per_kn / 1000), &pb))) break;
-            const float finf = std::numeric_limits<float>::infinity();
-            const unsigned s16pad = 16383u | (16383u << 16);
-            switch (path) {
-            case PATH_SIMT_F32_PAIR:
-                rc = launch_pack<float, float, 2, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                 Mp, Np, Kp, finf, s, rng); break;
-            case PATH_SIMT_I32_CARRIER:
-                rc = launch_pack<int, float, 2, ConvI32ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                               Mp, Np, Kp, finf, s, rng); break;
-            case PATH_SIMT_I32_VMIN:
-                rc = launch_pack<int, int, 1, ConvI32Vmin>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
-                                                            Np, Kp, (1 << 30) - 1, s, rng); break;
-            case PATH_SIMT_I32_SAT:
-                rc = launch_pack<int, int, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb, Mp,
-                                                             Np, Kp, 0x7fffffff, s, rng); break;
-            case PATH_SIMT_I64:
-                rc = launch_pack<long long, long long, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k,
-                                                                         pa, pb, Mp, Np, Kp, 0LL, s, rng); break;
-            case PATH_SIMT_I64_NARROW:
-                rc = launch_pack<long long, int, 1, ConvI64ToI32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                   Mp, Np, Kp, 0, s, rng); break;
-            case PATH_SIMT_F64_MIN: {
-                const double dinf = std::numeric_limits<double>::infinity();
-                rc = launch_pack<double, double, 1, ConvIdentity>(A, lda, B, ldb, P->m, P->n, P->k, pa,
-                                                                   pb, Mp, Np, Kp, dinf, s, rng); break;
-            }
-            case PATH_SIMT_I64_DP4A:
-                pack_a_s8x4_kernel<<<dim3((unsigned)((Kp / 4 + 31) / 32), (unsigned)(Mp / 32)), dim3(32, 8), 0, s>>>(
-                    (const long long*)A, P->m, P->k, lda, (int*)pa, Mp, Kp, rng);
-                pack_b_s8x4_kernel<<<grid2d(Kp / 4, Np / 2), 256, 0, s>>>(
-                    (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
-                rc = cuda_status(cudaGetLastError());
-                break;
-            case PATH_TC_I8:
-                pack_i8_rows_kernel<<<dim3((unsigned)((Kp / 8 + 255) / 256), (unsigned)std::min<long long>(Mp, 4096)), 256, 0, s>>>(
-                    (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, Kp, rng);
-                pack_i8_transpose_kernel<<<dim3((unsigned)(Np / 32), (unsigned)((Kp + 127) / 128)), dim3(32, 8), 0, s>>>(
-                    (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, Kp, rng);
-                rc = cuda_status(cudaGetLastError());
-                break;
-            case PATH_OZAKI_F64: {
-                // scale pass (and the finiteness guard); residues are packed after it
-                if ((rc = stage_acquire((size_t)Mp * 8, (void**)&oz_rowmax))) break;
-                if ((rc = stage_acquire((size_t)Np * 8, (void**)&oz_colmax))) break;
-                if ((rc = cuda_status(cudaMemsetAsync(oz_colmax, 0, (size_t)Np * 8, s)))) break;
-                const int wpb = 8;
-                oz_amax_rows_kernel<<<(unsigned)std::min<long long>((P->m + wpb - 1) / wpb, 148LL * 16), 32 * wpb, 0, s>>>(
-                    (const double*)A, P->m, P->k, lda, oz_rowmax, rng + 1);
-                oz_amax_cols_kernel<<<dim3((unsigned)((P->n + 31) / 32), (unsigned)((P->k + 255) / 256)), dim3(32, 8), 0, s>>>(
-                    (const double*)B, P->k, P->n, ldb, oz_colmax, rng + 1);
-                rc = cuda_status(cudaGetLastError());
-                break;
-            }
-            case PATH_SIMT_F64T_CARRIER:
-                rc = launch_pack<double, float, 2, ConvF64ToF32>(A, lda, B, ldb, P->m, P->n, P->k, pa, pb,
-                                                                  Mp, Np, Kp, finf, s, rng); break;
-            case PATH_SIMT_F32_S16X2:
-            case PATH_SIMT_I32_S16X2:
-            case PATH_SIMT_F64T_S16X2: {
-                dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
-                if (path == PATH_SIMT_F64T_S16X2) {
-                    pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
-                        (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<double><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
-                        (const double*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
-                } else if (path == PATH_SIMT_F32_S16X2) {
-                    pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
-                        (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<float><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
-                        (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
-                } else {
-                    pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
-                        (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-                    pack_b_s16x2_kernel<int><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
-                        (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
+        if (!needs_guard(P)) {
+            Geom G;
+            if ((rc = plan_geometry(P, general_path(P), G))) break;
+            size_t ab, bb;
+            packed_bytes(P, G, A, lda, B, ldb, &ab, &bb);
+            void *pa = nullptr, *pb = nullptr;
+            if (ab && (rc = x.acquire(ab, &pa))) break;
+            if (bb && (rc = x.acquire(bb, &pb))) break;
+            const void *opA, *opB;
+            long long olda, oldb;
+            if ((rc = pack_operands(x, G, A, lda, B, ldb, pa, pb, nullptr, Pred(), &opA, &olda, &opB, &oldb))) break;
+            rc = launch_candidate(x, G, C, ldc, A, lda, B, ldb, opA, olda, opB, oldb, Pred(),
+                                  timed ? &P->tev[0] : nullptr, info[0]);
+            ncand = 1;
+            break;
+        }
+        int first = (P->hint && P->hint != PATH_MIN_ORDERED) ? P->hint : fastest_path(P);
+        const bool host_sync = genv ? genv[0] == '1' : (!async && P->hint == 0);
+        if (host_sync) {
+            // ---- host-side verdict: pack, read the guard, re-pack if it disallows ----
+            bool guard_pending = true;
+            for (;;) {
+                Geom G;
+                if ((rc = plan_geometry(P, first, G))) break;
+                size_t ab, bb;
+                packed_bytes(P, G, A, lda, B, ldb, &ab, &bb);
+                void *pa = nullptr, *pb = nullptr;
+                if (ab && (rc = x.acquire(ab, &pa))) break;
+                if (bb && (rc = x.acquire(bb, &pb))) break;
+                unsigned long long* rng = guard_pending ? P->d_range : nullptr;
+                if (rng && (rc = cuda_status(cudaMemsetAsync(rng, 0, 2 * sizeof(unsigned long long), s)))) break;
+                const void *opA, *opB;
+                long long olda, oldb;
+                if ((rc = pack_operands(x, G, A, lda, B, ldb, pa, pb, rng, Pred(), &opA, &olda, &opB, &oldb))) break;
+                if (guard_pending) {
+                    publish_range_kernel<<<1, 32, 0, s>>>(P->d_range, P->hs_dev);
+                    if ((rc = cuda_status(cudaGetLastError()))) break;
+                    if ((rc = cuda_status(cudaStreamSynchronize(s)))) break;
+                    ++x.launches;
+                    ++P->st.guard_syncs;
+                    guard_pending = false;
+                    const int nar = guard_narrowest(P->sr, P->flags, P->k, P->hs[0], P->hs[1], ordered_ok);
+                    P->hint = nar;
+                    if (nar != first) { first = nar; continue; }   // re-pack for the allowed path
                 }
-                rc = cuda_status(cudaGetLastError());
+                rc = launch_candidate(x, G, C, ldc, A, lda, B, ldb, opA, olda, opB, oldb, Pred(),
+                                      timed ? &P->tev[0] : nullptr, info[0]);
+                ncand = 1;
                 break;
             }
-            }
-            if (rc) break;
-            launches += 2;
-            opA = pa; opB = pb;
+            break;
         }
-        if (!guard_pending) break;
-        // ---- the fused guard: decide the exact path the observed range allows ----
-        unsigned long long h[2];
-        publish_range_kernel<<<1, 32, 0, s>>>(P->d_range, P->h_range_dev);
-        if ((rc = cuda_status(cudaGetLastError()))) break;
-        if ((rc = cuda_status(cudaStreamSynchronize(s)))) break;
-        h[0] = P->h_range[0];
-        h[1] = P->h_range[1];
-        ++launches;
-        guard_pending = false;
-        const unsigned long long mx = h[0];
-        const bool bad = h[1] != 0;
-        int actual = path;
-        if (P->sr == STARMM_SR_FP64) {
-            actual = bad ? PATH_DMMA_F64 : PATH_OZAKI_F64;   // NaN / inf: IEEE semantics via DMMA
-        } else if (P->sr == STARMM_SR_INT64) {
-            // exact iff every int32 partial sum fits: K * max|a| * max|b| < 2^31
-            long double bound = (long double)P->k * (long double)mx * (long double)mx;
-            if (mx <= 127 && bound < 2147483648.0L)
-                actual = (P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A;
-            else if (mx < (1ull << 31) && bound < 2147483648.0L) actual = PATH_SIMT_I64_NARROW;
-            else actual = PATH_SIMT_I64;
-        } else if (P->sr == STARMM_SR_TROPICAL_F64) {
-            // integer-valued float64: int16 when |x| <= 4096, else fp32 carrier while all
-            // sums stay below 2^24 (exact), else the float64 kernel
-            if (!bad && mx <= (unsigned long long)S16_FINITE_MAX) actual = PATH_SIMT_F64T_S16X2;
-            else if (!bad && mx <= (1ull << 23)) actual = PATH_SIMT_F64T_CARRIER;
-            else actual = PATH_SIMT_F64_MIN;
-        } else if (P->sr == STARMM_SR_TROPICAL_F32) {
-            // integer-valued with |x| <= 4096: int16 sums cannot overflow, exact
-            actual = (!bad && mx <= (unsigned long long)S16_FINITE_MAX) ? PATH_SIMT_F32_S16X2
-                                                                         : PATH_SIMT_F32_PAIR;
-        } else {
-            if (mx <= (unsigned long long)S16_FINITE_MAX) actual = PATH_SIMT_I32_S16X2;   // int16 exact
-            else if (mx <= (1ull << 23)) actual = PATH_SIMT_I32_CARRIER;                 // fp32-exact sums
-            else if (mx < (1ull << 28)) actual = PATH_SIMT_I32_VMIN;                     // no overflow
-            else actual = PATH_SIMT_I32_SAT;
-        }
-        P->last_guarded_path = actual;
-        if (actual == path) break;
-        path = actual;                  // re-pack for the path the range allows
-      }
-      if (rc) break;
-        if (path == PATH_OZAKI_F64) {   // residue planes for the scales the guard pass found
-            const int t = ozaki_bits(P->k);
-            oz_pack_rows_kernel<<<dim3((unsigned)((Kp / 4 + 255) / 256), (unsigned)std::min<long long>(Mp, 65535)), 256, 0, s>>>(
-                (const double*)A, P->m, P->k, lda, oz_rowmax, t, (signed char*)opA, Mp, Kp);
-            oz_pack_cols_kernel<<<dim3((unsigned)(Np / 32), (unsigned)(Kp / 64)), dim3(32, 8), 0, s>>>(
-                (const double*)B, P->k, P->n, ldb, oz_colmax, t, (signed char*)opB, Np, Kp);
-            if ((rc = cuda_status(cudaGetLastError()))) break;
-            launches += 2;
-        }
-
-        // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
-        const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
-        void* pstate = nullptr;
-        size_t state_bytes = need_slots ? (size_t)(tiles + tiles * (S / 2)) * 4 : 0;
-        if (need_slots) {
-            if ((rc = stage_acquire(state_bytes, &pstate))) break;
-            if ((rc = cuda_status(cudaMemsetAsync(pstate, 0, state_bytes, s)))) break;
-        }
-        // per-worker lazy-temp blocks (tile sized, for SAR/STAR pairs)
-        void* wscratch = nullptr;
-        const long long tile_elems = (long long)TBM * TBN;
-        if (need_slots) {
-            if ((rc = stage_acquire((size_t)(gpu_workers * tile_elems * eb), &wscratch))) break;
-        }
-        // co3 workspace D_1..D_{S-1}: pooled (arena, reused) or raw (fresh per call)
-        void* W = nullptr;
-        size_t wbytes = 0;
-        if (P->algo == STARMM_CO3 && S > 1) {
-            wbytes = (size_t)(S - 1) * (size_t)P->m * (size_t)P->n * eb;
-            if (P->alloc == STARMM_POOLED) {
-                if ((rc = P->arena.acquire(wbytes, &W, true, &P->ws_fresh, &P->ws_reuse))) break;
-                staged.push_back({W, wbytes});
-            } else {
-                if ((rc = cuda_status(cudaMallocAsync(&W, wbytes, s)))) break;
-                ++P->raw_count;
-                P->raw_bytes += (long long)wbytes;
-            }
-            P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
-        }
-        if (init_identity && (S > 1 || balanced) && P->algo != STARMM_CO3 && P->remote_parts == 0) {
-            if ((rc = fill_dispatch(P->sr, C, P->m, P->n, ldc, s))) break;
-            ++launches;
-        }
-
-        WbParams w;
-        w.mode_base = P->algo; w.init_identity = init_identity ? 1 : 0;
-        w.C = C; w.ldc = ldc; w.M = P->m; w.N = P->n;
-        w.W = W; w.ldw = P->n; w.wstride = P->m * P->n;
-        w.slots = (int*)pstate;
-        w.pairs = pstate ? (int*)pstate + tiles : nullptr;
-        w.counters = P->d_counters; w.worker_used = P->d_worker_used;
-        w.scratch = wscratch; w.scratch_elems = tile_elems;
-        w.remote_parts = P->remote_parts; w.remote_rows = P->remote_rows; w.remote_ld = P->remote_ld;
-        for (int i = 0; i < 8; ++i) w.remote_base[i] = P->remote_base[i];
-
-        int grid = occupancy_grid(P, per_sm, balanced ? ntasks * g.kstages : ntasks);
-        const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
-        if (timed) {
-            if (!P->ev0) {
-                if ((rc = cuda_status(cudaEventCreate(&P->ev0)))) break;
-                if ((rc = cuda_status(cudaEventCreate(&P->ev1)))) break;
-            }
-            if ((rc = cuda_status(cudaEventRecord(P->ev0, s)))) break;
-        }
-        if (path == PATH_TC_I8) {
-            EpiFoldI64 e;
-            e.o = tcg_out(P, C, ldc, init_identity);
-            rc = launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s, stage_acquire);
-        } else if (path == PATH_OZAKI_F64) {
-            void* planes = nullptr;
-            if ((rc = stage_acquire((size_t)oz::P * Mp * Np, &planes))) break;
-            EpiOzakiResidues e;
-            e.R = (unsigned char*)planes; e.Mp = Mp; e.Np = Np;
-            if ((rc = launch_tcg(opA, opB, Mp, Np, Kp, oz::P, e, P->sms, s, stage_acquire))) break;
-            if (timed && (rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
-            const long long groups = (P->n + OZ_CRT_W - 1) / OZ_CRT_W;
-            oz_crt_kernel<<<dim3((unsigned)((groups + 127) / 128), (unsigned)std::min<long long>(P->m, 65535)), 128, 0, s>>>(
-                (const unsigned char*)planes, Mp, Np, oz_rowmax, oz_colmax, ozaki_bits(P->k), ozaki_crt(),
-                tcg_out(P, C, ldc, init_identity));
-            rc = cuda_status(cudaGetLastError());
-            ++launches;
-        } else if (is_dmma) {
-            DmmaParams dp;
-            dp.A = (const double*)opA; dp.lda = olda; dp.B = (const double*)opB; dp.ldb = oldb;
-            dp.g = g; dp.w = w;
-            dp.gate = P->d_gate;
-            // Wave gate: off by default since the one-CTA-per-SM 256x64 kernel keeps its
-            // persistent CTAs close enough on its own (58 GB of DRAM reads per n=16384
-            // launch without, 53 GB with, at -0.1..0.3%; the two-CTA 64x128 kernel needed
-            // it: 250 -> 51 GB).  STARMM_DMMA_GATE=1 turns it on; it needs the whole grid
-            // co-resident and pays only over several waves, and the host path's
-            // overlapping launches never use it.
-            const char* genv = getenv("STARMM_DMMA_GATE");
-            const bool gate = genv && genv[0] == '1' && P->dmma_gate && ntasks >= 4LL * grid;
-            rc = launch_dmma(dp, grid, gate, s);
-        } else {
-            SimtParams sp;
-            sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = g; sp.w = w;
-            // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
-            rc = cuda_status((cudaError_t)starmm_simt_launch(path, sp, grid, P->sms, s));
+        // ---- device-side verdict: first guess + predicated exact fallbacks ----
+        host_decided = false;
+        int cands[3] = {first, 0, 0};
+        ncand = 1;
+        const int general = general_path(P);
+        if (general != first) cands[ncand++] = general;
+        if (float_min(P) && ordered_ok) cands[ncand++] = PATH_MIN_ORDERED;
+        Geom G[3];
+        size_t abmax = 0, bbmax = 0;
+        for (int c = 0; c < ncand && !rc; ++c) {
+            rc = plan_geometry(P, cands[c], G[c]);
+            size_t ab, bb;
+            packed_bytes(P, G[c], A, lda, B, ldb, &ab, &bb);
+            abmax = std::max(abmax, ab);
+            bbmax = std::max(bbmax, bb);
         }
         if (rc) break;
-        ++launches;
-        if (timed && path != PATH_OZAKI_F64) {   // (the Ozaki path records it after its GEMM)
-            if ((rc = cuda_status(cudaEventRecord(P->ev1, s)))) break;
-        }
-
-        // ---- co3: merge the workspace bottom-up (merge_tasks, ops.py:108-155) ----
-        if (P->algo == STARMM_CO3 && S > 1) {
-            const long long slab = P->m * P->n;
-            for (int lvl = s_log2; lvl >= 1 && !rc; --lvl) {
-                int step = 1 << (s_log2 - lvl);
-                for (int x = step; x < S && !rc; x += 2 * step) {
-                    char* src = (char*)W + (size_t)(x - 1) * slab * eb;
-                    int tgt = x - step;
-                    if (tgt == 0) rc = madd_dispatch(P->sr, C, ldc, src, P->n, P->m, P->n, 0, s);
-                    else rc = madd_dispatch(P->sr, (char*)W + (size_t)(tgt - 1) * slab * eb, P->n, src,
-                                            P->n, P->m, P->n, 0, s);
-                    ++launches;
-                }
-            }
-            if (rc) break;
-            if (P->alloc == STARMM_RAW) {
-                if ((rc = cuda_status(cudaFreeAsync(W, s)))) break;
-            }
+        // every candidate packs into the same staging: a fallback's packers only run when
+        // the first guess's kernel does not
+        void *pa = nullptr, *pb = nullptr;
+        if (abmax && (rc = x.acquire(abmax, &pa))) break;
+        if (bbmax && (rc = x.acquire(bbmax, &pb))) break;
+        if ((rc = cuda_status(cudaMemsetAsync(P->d_range, 0, 2 * sizeof(unsigned long long), s)))) break;
+        const void *opA[3], *opB[3];
+        long long olda[3], oldb[3];
+        if ((rc = pack_operands(x, G[0], A, lda, B, ldb, pa, pb, P->d_range, Pred(), &opA[0], &olda[0],
+                                &opB[0], &oldb[0]))) break;
+        select_path_kernel<<<1, 32, 0, s>>>(P->d_range, P->sr, P->flags, P->k, first, general,
+                                            ordered_ok ? 1 : 0, P->d_sel, P->hs_dev);
+        if ((rc = cuda_status(cudaGetLastError()))) break;
+        ++x.launches;
+        P->spec_used = true;
+        for (int c = 0; c < ncand && !rc; ++c) {
+            const Pred pr{P->d_sel, (unsigned)cands[c]};
+            if (c > 0 && (rc = pack_operands(x, G[c], A, lda, B, ldb, pa, pb, nullptr, pr, &opA[c], &olda[c],
+                                             &opB[c], &oldb[c]))) break;
+            rc = launch_candidate(x, G[c], C, ldc, A, lda, B, ldb, opA[c], olda[c], opB[c], oldb[c], pr,
+                                  timed ? &P->tev[2 * c] : nullptr, info[c]);
         }
     } while (0);
 
-    // staging buffers go back to their LIFO stacks; stream order protects reuse
-    for (auto it = staged.rbegin(); it != staged.rend(); ++it) P->arena.release(it->p, it->bytes);
+    // staging blocks go back to the device pool, fenced by the work queued so far
+    FenceRef fence = P->ctx->arena.fence(s);
+    for (auto it = x.staged.rbegin(); it != x.staged.rend(); ++it) P->ctx->arena.release(it->p, fence);
+    plan_note_fence(P, fence);
     if (rc) return rc;
-    if (!(P->flags & STARMM_F_ASYNC) && !force_async) CK(cudaStreamSynchronize(s));
-    if (P->flags & STARMM_F_TIME_MAIN) {
-        CK(cudaEventSynchronize(P->ev1));
+    if (!async) CK(cudaStreamSynchronize(s));
+    // which candidate ran: known now if the host decided or the call was blocking
+    int ran = 0;
+    if (!host_decided && !async) {
+        const int sel = (int)P->hs[2];
+        for (int c = 0; c < ncand; ++c)
+            if (info[c].path == sel) ran = c;
+        if (P->hs[3]) P->hint = (int)P->hs[3];
+    }
+    const CandInfo& ci = info[ran];
+    if (timed) {
+        CK(cudaEventSynchronize(P->tev[2 * ran + 1]));
         float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, P->ev0, P->ev1));
+        CK(cudaEventElapsedTime(&ms, P->tev[2 * ran], P->tev[2 * ran + 1]));
         P->st.main_kernel_ns += (int64_t)((double)ms * 1e6);
         P->st.main_kernel_launches += 1;
     }
-
-    P->st.tasks = ntasks;
-    P->st.workers = std::min<long long>(ntasks, (long long)P->sms * per_sm);
-    P->st.ksplit = S;
-    P->st.balanced_workers = balanced ? std::min<long long>(ntasks * g.kstages, (long long)P->sms * per_sm) : 0;
-    P->st.tar_levels = tar_levels;
-    P->st.kernel_launches = launches;
-    P->st.path = path;
+    P->raw_count += ci.raw_count;
+    P->raw_bytes += ci.raw_bytes;
+    P->st.tasks = ci.tasks;
+    P->st.workers = ci.workers;
+    P->st.ksplit = ci.S;
+    P->st.balanced_workers = ci.balanced_workers;
+    P->st.tar_levels = ci.tar_levels;
+    P->st.kernel_launches = x.launches;
+    P->st.path = ci.path;
     P->st.executes += 1;
-    if (S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && tar_levels < s_log2)
-        P->st.pair_count += tiles * (S / 2);
-    if (prev_dev != P->device) cudaSetDevice(prev_dev);
+    P->st.pair_count += ci.pair_count;
+    P->st.candidates = ncand;
     return STARMM_OK;
 }
+
+extern "C" {
+
+// ============================================================================
 
 // ============================================================================
 // The Strassen family (strassen.py:1-235): C <- A (x) B over a ring, overwriting C.
@@ -1072,7 +1335,7 @@ int str_acquire(StrCtx& x, long long n, void** out) {
         ++x.P->raw_count;
         x.P->raw_bytes += (long long)bytes;
     } else {
-        TRY(x.P->arena.acquire(bytes, out, true, &x.P->ws_fresh, &x.P->ws_reuse));
+        TRY(plan_acquire(x.P, bytes, x.s, out, true));
     }
     x.P->str_issued += (long long)bytes;
     x.P->ws_high_water = std::max(x.P->ws_high_water, x.P->str_issued);
@@ -1082,7 +1345,8 @@ int str_acquire(StrCtx& x, long long n, void** out) {
 void str_release(StrCtx& x, void* p, long long n) {
     size_t bytes = (size_t)(n * n) * x.eb;
     if (x.P->alloc == STARMM_RAW) cudaFreeAsync(p, x.s);
-    else x.P->arena.release(p, bytes);   // LIFO: the next same-size acquire gets it back
+    else x.P->ctx->arena.release(p, nullptr);   // LIFO: the next same-size acquire gets it back
+                                                // (same stream: stream order protects it)
     x.P->str_issued -= (long long)bytes;
 }
 
@@ -1229,17 +1493,16 @@ int strassen_execute(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
     if (P->m != P->n || P->n != P->k) return STARMM_DIM_MISMATCH;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
-    int prev_dev = 0;
-    CK(cudaGetDevice(&prev_dev));
-    if (prev_dev != P->device) CK(cudaSetDevice(P->device));
-    TRY(ensure_bookkeeping(P));
+    DeviceGuard dg;
+    TRY(dg.set(P->device));
+    TRY(ensure_bookkeeping(P, (cudaStream_t)stream));
     StrCtx x{P, (cudaStream_t)stream, (size_t)elem_bytes(P->sr),
              std::max<long long>(P->base_dim, P->strassen_leaf), switch_depth(P->workers), 0};
     int rc = str_mm(x, 0, MM_STORE, C, ldc, A, lda, B, ldb, P->n);
     if (!rc && !(P->flags & STARMM_F_ASYNC)) rc = cuda_status(cudaStreamSynchronize(x.s));
     P->st.kernel_launches = x.launches;
     P->st.executes += 1;
-    if (prev_dev != P->device) cudaSetDevice(prev_dev);
+    plan_note_fence(P, P->ctx->arena.fence(x.s));
     return rc;
 }
 
@@ -1350,7 +1613,7 @@ static double host_nominal_ops(int sr) {
 }
 
 static int host_phase1_chunks(long long m, long long n, long long k, int sr, double h2d_bytes,
-                              std::vector<long long>& kb) {
+                              long long base_dim, std::vector<long long>& kb) {
     kb.assign(1, 0);
     const char* env = getenv("STARMM_HOST_PHASE1");
     if ((env && env[0] == '0') || m < 512 || k < 512) return 0;
@@ -1358,7 +1621,10 @@ static int host_phase1_chunks(long long m, long long n, long long k, int sr, dou
     if (!(env && env[0] == '1') && t_mm < h2d_bytes / 50e9) return 0;
     // first chunk k/64 (k >= 8192) or k/32: its upload is the exposed head of the schedule
     const long long div = (k >= 8192 && sr == STARMM_SR_FP64) ? 64 : 32;   // DMMA calls have no packing / guard
-    long long w = std::max<long long>(128, round_up((k + div - 1) / div, 128)), sum = 0;
+    // widths are multiples of the leaf size (and of 128): a leaf never straddles two
+    // calls, so the ordered kernel's per-leaf minima are the reference's
+    const long long cq = std::max<long long>(128, base_dim);
+    long long w = std::max<long long>(cq, round_up((k + div - 1) / div, cq)), sum = 0;
     while (sum + w <= k / 2) {
         sum += w;
         kb.push_back(sum);
@@ -1381,21 +1647,28 @@ static int execute_host_remote(starmm_plan* P, const void* A, int64_t lda, const
     const size_t eb = (size_t)elem_bytes(P->sr);
     const long long m = P->m, n = P->n, k = P->k;
     std::vector<long long> kb(1, 0);
-    for (long long w = std::max<long long>(128, round_up((k + 31) / 32, 128)); kb.back() < k; w *= 2)
+    // chunk widths are multiples of the leaf size, so leaves never straddle two calls
+    const long long cq = std::max<long long>(128, P->base_dim);
+    for (long long w = std::max<long long>(cq, round_up((k + 31) / 32, cq)); kb.back() < k; w *= 2)
         kb.push_back(std::min(k, kb.back() + w));
     const int nq = (int)kb.size() - 1;
     cudaStream_t cs = (cudaStream_t)stream, up = nullptr;
     TRY(res.stream(&up));
     std::vector<cudaEvent_t> ev(nq);
     for (auto& e : ev) TRY(res.event(&e));
+    // the uploads are ordered after everything already queued on the caller's stream
+    // (it may still be producing the pinned inputs)
+    cudaEvent_t ev_entry = nullptr;
+    TRY(res.event(&ev_entry));
+    CK(cudaEventRecord(ev_entry, cs));
+    CK(cudaStreamWaitEvent(up, ev_entry, 0));
     void *dA = nullptr, *dB = nullptr;
-    long long fr = 0, ru = 0;
     const size_t a_bytes = (size_t)m * k * eb, b_bytes = (size_t)k * n * eb;
     int rc = STARMM_OK;
     const int saved_flags = P->flags;
     do {
-        if ((rc = P->arena.acquire(a_bytes, &dA, false, &fr, &ru))) break;
-        if ((rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
+        if ((rc = plan_acquire(P, a_bytes, up, &dA, false))) break;
+        if ((rc = plan_acquire(P, b_bytes, up, &dB, false))) break;
         for (int c = 0; c < nq && !rc; ++c) {
             const long long k0 = kb[c], kc = kb[c + 1] - kb[c];
             rc = cuda_status(cudaMemcpy2DAsync((char*)dB + k0 * n * eb, n * eb, (const char*)B + k0 * ldb * eb,
@@ -1410,18 +1683,20 @@ static int execute_host_remote(starmm_plan* P, const void* A, int64_t lda, const
             const long long k0 = kb[c];
             if ((rc = cuda_status(cudaStreamWaitEvent(cs, ev[c], 0)))) break;
             P->k = kb[c + 1] - k0;
+            P->kofs = k0;
             // (C is not touched: every write-back goes to the peers)
             rc = execute_impl(P, dA, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true);
             P->k = k;
+            P->kofs = 0;
         }
         if (rc) break;
         rc = cuda_status(cudaStreamSynchronize(cs));
     } while (0);
-    P->k = k; P->flags = saved_flags;
+    P->k = k; P->kofs = 0; P->flags = saved_flags;
     cudaStreamSynchronize(up);
     cudaStreamSynchronize(cs);
-    if (dB) P->arena.release(dB, b_bytes);
-    if (dA) P->arena.release(dA, a_bytes);
+    if (dB) P->ctx->arena.release(dB, nullptr);
+    if (dA) P->ctx->arena.release(dA, nullptr);
     return rc;
 }
 
@@ -1445,7 +1720,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     const bool same_ab = (A == B) && (m == k) && (n == k) && (lda == ldb);
     const double h2d = (double)eb * ((double)m * k + (same_ab ? 0.0 : (double)k * n) +
                                      ((saved_flags & STARMM_F_INIT_IDENTITY) ? 0.0 : (double)m * n));
-    const int nq = host_phase1_chunks(m, n, k, P->sr, h2d, kb);
+    const int nq = host_phase1_chunks(m, n, k, P->sr, h2d, P->base_dim, kb);
     const long long kq = kb.back();
     // phase-2 row blocks: ~2.5e11 semiring ops each (>= ~7 ms of B200 work, so per-block
     // guards / packing stay negligible), at most 16, and at least 8 (m >= 1024) or 4
@@ -1513,12 +1788,14 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         trace.push_back({label, e});
     };
     mark("start", cs);
-    if (tracing) {
-        cudaStreamWaitEvent(up, trace[0].second, 0);
-        cudaStreamWaitEvent(down, trace[0].second, 0);
-    }
+    // the copy streams start after everything already queued on the caller's stream
+    // (it may still be producing the pinned inputs or reading C)
+    cudaEvent_t ev_entry = nullptr;
+    TRY(res.event(&ev_entry));
+    CK(cudaEventRecord(ev_entry, cs));
+    CK(cudaStreamWaitEvent(up, ev_entry, 0));
+    CK(cudaStreamWaitEvent(down, ev_entry, 0));
     void *dA = nullptr, *dB = nullptr, *dC = nullptr, *dC0 = nullptr;
-    long long fr = 0, ru = 0;
     const size_t a_bytes = (size_t)m * k * eb, b_bytes = (size_t)k * n * eb, c_bytes = (size_t)m * n * eb;
     int rc = STARMM_OK;
     // host (src, ld_src) -> device (dst, ld_dst): the rows x cols block at (r0, c0)
@@ -1535,21 +1812,22 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     auto run = [&](starmm_plan* Q, cudaStream_t st, void* Cd, const void* Ad, const void* Bd, long long rows,
                    long long kk, bool store) {
         Q->m = rows; Q->k = kk;
+        Q->kofs = (long long)((const char*)Bd - (const char*)dB) / (long long)(n * eb);   // leaf alignment
         if (kk == k - kq && ks2 >= -1) Q->ksplit_req = ks2;   // phase-2 split override (tuning)
         // (STARMM_F_TIME_MAIN would synchronise the host after every launch and serialise the
         // schedule, so the host path never times its kernels)
         const int f = saved_flags & ~STARMM_F_TIME_MAIN;
         Q->flags = store ? (f | STARMM_F_INIT_IDENTITY) : (f & ~STARMM_F_INIT_IDENTITY);
         int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true);
-        Q->m = m; Q->k = k; Q->flags = saved_flags; Q->ksplit_req = saved_ks;
+        Q->m = m; Q->k = k; Q->kofs = 0; Q->flags = saved_flags; Q->ksplit_req = saved_ks;
         return r;
     };
     do {
-        if ((rc = P->arena.acquire(a_bytes, &dA, false, &fr, &ru))) break;
-        if (!same_ab && (rc = P->arena.acquire(b_bytes, &dB, false, &fr, &ru))) break;
+        if ((rc = plan_acquire(P, a_bytes, up, &dA, false))) break;
+        if (!same_ab && (rc = plan_acquire(P, b_bytes, up, &dB, false))) break;
         if (same_ab) dB = dA;
-        if ((rc = P->arena.acquire(c_bytes, &dC, false, &fr, &ru))) break;
-        if (staged_c0 && (rc = P->arena.acquire(c_bytes, &dC0, false, &fr, &ru))) break;
+        if ((rc = plan_acquire(P, c_bytes, up, &dC, false))) break;
+        if (staged_c0 && (rc = plan_acquire(P, c_bytes, up, &dC0, false))) break;
         void* dCin = staged_c0 ? dC0 : dC;   // where C0's rows land
         // ---- uploads, in consumption order, all on `up` ----
         for (int c = 0; c < nq && !rc; ++c) {
@@ -1602,7 +1880,8 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             // persistent launch on the other stream would wait for that launch to end
             if (staged_c0) {
                 if ((rc = cuda_status(cudaStreamWaitEvent(sb, ev_c[b], 0)))) break;
-                if ((rc = madd_dispatch(P->sr, Cb, n, (char*)dC0 + r0 * n * eb, n, rows, n, 0, sb))) break;
+                // C0 comes first in the reference's fold sequence: Cb <- C0 (+) Cb
+                if ((rc = madd_dispatch(P->sr, Cb, n, (char*)dC0 + r0 * n * eb, n, rows, n, 0, sb, 1))) break;
             }
             if (kq < k) {
                 if ((rc = cuda_status(cudaStreamWaitEvent(sb, ev_a[b], 0)))) break;
@@ -1641,22 +1920,51 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         fprintf(stderr, "{\"host_trace\": \"%s\", \"ms\": %.3f}\n", t.first.c_str(), ms);
     }
     for (auto& t : trace) cudaEventDestroy(t.second);
-    if (dC0) P->arena.release(dC0, c_bytes);
-    if (dC) P->arena.release(dC, c_bytes);
-    if (dB && !same_ab) P->arena.release(dB, b_bytes);
-    if (dA) P->arena.release(dA, a_bytes);
+    // (every stream was synchronised above: the blocks are free on the device)
+    if (dC0) P->ctx->arena.release(dC0, nullptr);
+    if (dC) P->ctx->arena.release(dC, nullptr);
+    if (dB && !same_ab) P->ctx->arena.release(dB, nullptr);
+    if (dA) P->ctx->arena.release(dA, nullptr);
     return rc;
 }
 
+// Semiring.matmul (semiring.py:92-94): out <- A (x) B from the additive identity, one
+// product over the whole K (the reference's numba kernel is one leaf: its first minimum
+// over k wins, so the plan's leaf size is K rounded up to a power of two).  Plans are
+// cached per device by shape and flags -- a call costs launches, not plan setup, and
+// the range guard's verdict carries over from call to call.  A cached plan is taken out
+// of the cache while a thread uses it.
 int starmm_matmul(int semiring, void* out, int64_t ldo, const void* A, int64_t lda, const void* B,
                   int64_t ldb, int64_t m, int64_t n, int64_t k, void* stream, int flags) {
     int dev = 0;
     CK(cudaGetDevice(&dev));
+    if (dev < 0 || dev >= starmm_host::MAX_DEVICES) return STARMM_CONTRACT_VIOLATION;
+    const int pf = flags | STARMM_F_INIT_IDENTITY | STARMM_F_ALLOW_NONPOW2;
+    int leaf = 1;
+    while (leaf < k && leaf < (1 << 30)) leaf <<= 1;
     starmm_plan* P = nullptr;
-    TRY(starmm_plan_create(&P, semiring, STARMM_CO2, STARMM_POOLED, m, n, k, 1, 1, 0, dev,
-                           (flags | STARMM_F_INIT_IDENTITY | STARMM_F_ALLOW_NONPOW2)));
-    int rc = starmm_execute(P, out, ldo, A, lda, B, ldb, stream);
-    starmm_plan_destroy(P);
+    {
+        std::lock_guard<std::mutex> g(g_mm_mu);
+        auto& c = g_mm_cache[dev];
+        for (size_t i = c.size(); i-- > 0;) {
+            starmm_plan* q = c[i];
+            if (q->sr == semiring && q->m == m && q->n == n && q->k == k && q->flags == pf) {
+                P = q;
+                c.erase(c.begin() + (long)i);
+                break;
+            }
+        }
+    }
+    if (!P) TRY(starmm_plan_create(&P, semiring, STARMM_CO2, STARMM_POOLED, m, n, k, leaf, 1, 0, dev, pf));
+    const int rc = starmm_execute(P, out, ldo, A, lda, B, ldb, stream);
+    starmm_plan* evict = nullptr;
+    {
+        std::lock_guard<std::mutex> g(g_mm_mu);
+        auto& c = g_mm_cache[dev];
+        c.push_back(P);                                   // most recently used last
+        if (c.size() > 32) { evict = c.front(); c.erase(c.begin()); }
+    }
+    if (evict) starmm_plan_destroy(evict);
     return rc;
 }
 
@@ -1677,6 +1985,65 @@ int starmm_atomic_accumulate(int semiring, void* C, int64_t ldc, const void* P_,
     cudaStream_t s = (cudaStream_t)stream;
     TRY(madd_dispatch(semiring, C, ldc, P_, ldp, rows, cols, 1, s));
     if (!(flags & STARMM_F_ASYNC)) CK(cudaStreamSynchronize(s));
+    return STARMM_OK;
+}
+
+// ---- the device block pool (pool.py:67-167) --------------------------------
+int starmm_pool_acquire(int device, int64_t bytes, void* stream, void** out, int* fresh) {
+    if (!out || bytes <= 0) return STARMM_CONTRACT_VIOLATION;
+    *out = nullptr;
+    DeviceCtx* c = device_ctx(device);
+    if (!c) return STARMM_CONTRACT_VIOLATION;
+    DeviceGuard dg;
+    TRY(dg.set(device));
+    bool f = false;
+    CK(c->arena.acquire((size_t)bytes, (cudaStream_t)stream, out, &f));
+    if (fresh) *fresh = f ? 1 : 0;
+    return STARMM_OK;
+}
+
+int starmm_pool_release(int device, void* block, void* stream) {
+    DeviceCtx* c = device_ctx(device);
+    if (!c || !block) return STARMM_CONTRACT_VIOLATION;
+    if (!c->arena.owns(block)) return STARMM_CONTRACT_VIOLATION;   // pool.py:120-127
+    DeviceGuard dg;
+    TRY(dg.set(device));
+    c->arena.release(block, c->arena.fence((cudaStream_t)stream));
+    return STARMM_OK;
+}
+
+int starmm_pool_counts_get(int device, starmm_pool_counts* out) {
+    DeviceCtx* c = device_ctx(device);
+    if (!c || !out) return STARMM_CONTRACT_VIOLATION;
+    std::lock_guard<std::mutex> g(c->arena.mu);
+    const starmm_host::PoolCounts& k = c->arena.c;
+    out->allocated_bytes = k.allocated; out->cached_bytes = k.cached; out->issued_bytes = k.issued;
+    out->high_water_bytes = k.high_water; out->fresh_count = k.fresh; out->reuse_count = k.reuse;
+    out->cross_stream_waits = k.waits; out->trims = k.trims;
+    return STARMM_OK;
+}
+
+int starmm_pool_reset(int device) {
+    DeviceCtx* c = device_ctx(device);
+    if (!c) return STARMM_CONTRACT_VIOLATION;
+    DeviceGuard dg;
+    TRY(dg.set(device));
+    // cached one-shot matmul plans hold pool blocks: drop them first
+    std::vector<starmm_plan*> drop;
+    {
+        std::lock_guard<std::mutex> g(g_mm_mu);
+        drop.swap(g_mm_cache[device]);
+    }
+    for (auto* p : drop) starmm_plan_destroy(p);
+    c->arena.reset();
+    return STARMM_OK;
+}
+
+int starmm_pool_set_discipline(int device, int fifo) {
+    DeviceCtx* c = device_ctx(device);
+    if (!c || (fifo != 0 && fifo != 1)) return STARMM_CONTRACT_VIOLATION;
+    std::lock_guard<std::mutex> g(c->arena.mu);
+    c->arena.fifo = fifo;
     return STARMM_OK;
 }
 

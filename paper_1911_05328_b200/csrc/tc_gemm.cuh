@@ -64,6 +64,7 @@ struct TcgShape {
     // after 2 ms, so a partly resident grid is slower but cannot deadlock.
     unsigned* gate;                             // passes * rounds counters, zeroed; or null
     int gate_depth, rounds;
+    Pred pr;                                    // device-side path predicate (common.cuh)
 };
 
 // ---------------------------------------------------------------------------
@@ -184,6 +185,7 @@ tcg_kernel(const __grid_constant__ CUtensorMap tmap_a, const __grid_constant__ C
            TcgShape sh, Epi epi) {
     using namespace tcg;
     using namespace tcgx;
+    if (sh.pr.off()) return;   // uniform over the cluster: both CTAs leave before any sync
     extern __shared__ __align__(128) unsigned char smem_raw[];
     unsigned char* tiles = reinterpret_cast<unsigned char*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));

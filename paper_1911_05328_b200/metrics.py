@@ -1,11 +1,16 @@
 """Run metrics (reference metrics.py:19-153), filled from the device counters.
 
-The reference measures per-depth concurrency of Python tasks; on the GPU the
-concurrent units are persistent CTAs executing leaf tasks, so the snapshot
-reports: base_case_max = CTAs that ran leaves concurrently (<= SMs, the
-busy-leaves bound of SPEC.md:566 with p = workers), the tile-slot
-serialisations (atomic-madd merges), SAR pair states / transitions and lazy
-temporary acquisitions, and the pool counters.
+The reference measures per-depth concurrency of Python tasks (task_enter /
+base_enter, metrics.py:63-95); on the GPU the concurrent units are persistent
+CTAs executing leaf tasks (output tile x k-slice), and the same quantity is
+MEASURED by a device gauge: thread 0 of a CTA counts its leaf in and out with
+atomics and the maximum in flight is kept (csrc/common.cuh leaf_enter /
+leaf_exit).  base_case_max is that observed maximum (the busy-leaves bound of
+SPEC.md:566 asks it to stay <= p, here the persistent workers); per_depth_max
+keys it by the split depth the leaves ran at.  Also reported: the tile-slot
+serialisations (atomic-madd merges), SAR pair states / transitions, lazy
+temporary acquisitions and the pool counters.  The opt-in tcgen05 paths and the
+ordered (min,+) kernel carry no gauge and report 0.
 """
 from __future__ import annotations
 
@@ -62,16 +67,16 @@ class Metrics:
 
     def absorb_device(self, st: dict, elem_bytes: int) -> None:
         with self._lock:
-            self.base_case_max = max(self.base_case_max, min(st["workers"], st["tasks"]))
+            live = st.get("live_leaves_max", 0)
+            self.base_case_max = max(self.base_case_max, live)
             self.tile_serializations += st["tile_serializations"]
             self.pair_count += st["pair_count"]
             self.pair_transitions += st["pair_transitions"]
             self.lazy_temp_acquires += st["lazy_temp_acquires"]
             self.raw_alloc_count += st["raw_alloc_count"]
             self.raw_alloc_elements += st["raw_alloc_bytes"] // max(1, elem_bytes)
-            self.per_depth_max[st["ksplit"].bit_length() - 1] = max(
-                self.per_depth_max.get(st["ksplit"].bit_length() - 1, 0),
-                min(st["workers"], st["tasks"]))
+            depth = st["ksplit"].bit_length() - 1
+            self.per_depth_max[depth] = max(self.per_depth_max.get(depth, 0), live)
             self.last = dict(st)
 
     def count_serialization(self, n=1):

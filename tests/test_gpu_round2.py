@@ -1,0 +1,367 @@
+"""GPU tests of the round-2 boundary work (all through the C ABI / drop-in API):
+
+* signed zeros: the reference's tropical results, sign of zero included, bit for bit
+  (tests/golden/ref_signed_zero.npz was computed by the reference itself), on every
+  schedule, through the fast paths (C0 holds -0.0) and the ordered kernel (A or B does);
+* the device-side range-guard verdict: a plan's later calls never wait for the guard on
+  the host, stay exact when the data range changes under them, and STARMM_F_ASYNC holds;
+* the per-device block pool: LIFO re-issue, FIFO sabotage, cross-stream ordering, plan
+  create/destroy without device-wide synchronisation or cudaFree, Semiring.matmul cost;
+* instrumentation: the live leaf gauge, STAR's space bound.
+"""
+import ctypes
+import os
+import time
+
+import numpy as np
+import pytest
+import torch
+
+import paper_1911_05328_b200 as sm
+from paper_1911_05328_b200 import _lib
+from _bits import same_bits, diff_count
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+SZ = np.load(os.path.join(GOLD, "ref_signed_zero.npz"))
+SZ_CASES = [(1, 4), (2, 8), (4, 16), (8, 32), (16, 32), (32, 32)]
+ALGOS = {"co2": sm.co2, "co3": sm.co3, "tar": sm.tar_mm, "sar": sm.sar_mm, "star": sm.star_mm}
+
+
+def _run(algo, s, C0, A, B, cfg):
+    C = sm.Matrix(C0, s)
+    with sm.Executor(cfg) as ex:
+        sm.run_algorithm(ex, algo, C, sm.Matrix(A, s), sm.Matrix(B, s), s)
+        st = ex.last_stats
+    return C.numpy(), st
+
+
+# ---- signed zeros ------------------------------------------------------------------
+@pytest.mark.parametrize("algo", list(ALGOS))
+@pytest.mark.parametrize("b,n", SZ_CASES)
+@pytest.mark.parametrize("workers", [1, 148])
+def test_signed_zero_schedules_vs_reference_golden(algo, b, n, workers):
+    """+-0.0-heavy operands: every schedule equals the reference bit for bit (the
+    guard sees -0.0 and runs the ordered kernel at the plan's leaf size)."""
+    key = f"n{n}_b{b}"
+    got, st = _run(algo, sm.TROPICAL, SZ[key + "_C0"], SZ[key + "_A"], SZ[key + "_B"],
+                   sm.Config(base_dim=b, workers=workers))
+    assert st["path_name"] == "minplus_ordered_leaf_order"
+    assert same_bits(got, SZ[f"{key}_{algo}"]), diff_count(got, SZ[f"{key}_{algo}"])
+
+
+@pytest.mark.parametrize("b,n", SZ_CASES)
+def test_signed_zero_naive_matmul_and_madd_vs_reference_golden(b, n):
+    key = f"n{n}_b{b}"
+    s = sm.TROPICAL
+    got = sm.naive_mm(sm.Matrix(SZ[key + "_A"], s), sm.Matrix(SZ[key + "_B"], s), s).numpy()
+    assert same_bits(got, SZ[key + "_naive"])
+    assert same_bits(s.matmul(SZ[key + "_A"], SZ[key + "_B"]), SZ[key + "_naive"])
+    C = SZ[key + "_C0"].copy()
+    s.fold_add(C, SZ[key + "_A"])
+    assert same_bits(C, SZ[key + "_madd"])
+
+
+@pytest.mark.parametrize("sid", ["tropical", "tropical_f32"])
+@pytest.mark.parametrize("algo", ["co2", "co3", "sar", "star"])
+@pytest.mark.parametrize("b", [16, 64, 256])
+def test_signed_zero_operands_take_ordered_kernel(sid, algo, b):
+    """Integer-valued data (the s16x2 fast path's range) with -0.0 sprinkled into A and
+    B: the ordered kernel runs and equals the oracle's serial schedule (leaf order of
+    the reference) bit for bit."""
+    n = 256
+    s = sm.get_semiring(sid)
+    dt = s.dtype
+    rng = np.random.default_rng(b + len(algo))
+    A = rng.integers(0, 4, (n, n)).astype(dt)       # minima are mostly zeros of either sign
+    B = rng.integers(0, 4, (n, n)).astype(dt)
+    for M in (A, B):
+        z = rng.random(M.shape) < 0.3
+        M[z] = np.where(rng.random(z.sum()) < 0.5, dt.type(0.0), dt.type(-0.0))
+        M[rng.random(M.shape) < 0.05] = np.inf
+    C0 = rng.integers(0, 2, (n, n)).astype(dt)
+    C0[C0 == 0] = np.where(rng.random((C0 == 0).sum()) < 0.5, dt.type(0.0), dt.type(-0.0))
+    want = C0.copy()
+    O.schedule_mm(O.SR_BY_NAME[sid], algo, want, A, B, b)
+    got, st = _run(algo, s, C0, A, B, sm.Config(base_dim=b, workers=148))
+    assert st["path_name"] == "minplus_ordered_leaf_order"
+    assert same_bits(got, want), diff_count(got, want)
+    assert np.any(np.signbit(got) & (got == 0)) and np.any(~np.signbit(got) & (got == 0))
+
+
+@pytest.mark.parametrize("sid,expect", [("tropical", "simt_f64trop_s16x2_viaddmnmx"),
+                                        ("tropical_f32", "simt_f32_s16x2_viaddmnmx")])
+def test_signed_zero_in_C0_only_keeps_fast_path(sid, expect):
+    """-0.0 only in C0: the packed fast kernels never see it, and the fold keeps
+    np.minimum's tie rule (C0 = -0.0 folded with a +0.0 product gives +0.0)."""
+    n = 256
+    s = sm.get_semiring(sid)
+    dt = s.dtype
+    rng = np.random.default_rng(3)
+    A = rng.integers(-2, 3, (n, n)).astype(dt)
+    B = rng.integers(0, 3, (n, n)).astype(dt)
+    A[rng.random(A.shape) < 0.3] = np.inf
+    C0 = np.where(rng.random((n, n)) < 0.5, dt.type(-0.0), dt.type(0.0)).astype(dt)
+    want = C0.copy()
+    O.schedule_mm(O.SR_BY_NAME[sid], "co2", want, A, B, 64)
+    got, st = _run("co2", s, C0, A, B, sm.Config(base_dim=64, workers=148))
+    assert st["path_name"] == expect
+    assert same_bits(got, want), diff_count(got, want)
+
+
+def test_signed_zero_host_path_matches_device_path():
+    """The host-buffer schedule (k-chunks, C0 folded between them) keeps the
+    reference's fold order: C0 first (madd in reverse order)."""
+    n = 1024
+    s = sm.TROPICAL_F32
+    rng = np.random.default_rng(11)
+    A = rng.integers(-2, 3, (n, n)).astype(np.float32)
+    B = rng.integers(-2, 3, (n, n)).astype(np.float32)
+    for M in (A, B):
+        M[rng.random(M.shape) < 0.4] = np.float32(-0.0)
+    C0 = np.where(rng.random((n, n)) < 0.5, np.float32(-0.0), np.float32(0.0))
+    want = C0.copy()
+    O.schedule_mm(O.SR_TROP_F32, "star", want, A, B, 64)
+    for phase1 in ("1", "0"):
+        os.environ["STARMM_HOST_PHASE1"] = phase1
+        try:
+            Ct = torch.from_numpy(C0.copy()).pin_memory()
+            with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
+                ex.execute_host("star", Ct, torch.from_numpy(A).pin_memory(),
+                                torch.from_numpy(B).pin_memory(), s)
+        finally:
+            del os.environ["STARMM_HOST_PHASE1"]
+        assert same_bits(Ct.numpy(), want), (phase1, diff_count(Ct.numpy(), want))
+
+
+# ---- the device-side guard verdict ---------------------------------------------------
+def _plan(sr, n, flags=0, algo="star", b=64):
+    return _lib.Plan(sr, algo, "pooled", n, n, n, b, 148, -1, torch.cuda.current_device(), flags)
+
+
+def _exec(p, C, A, B):
+    p.reset_stats()
+    p.execute(C.data_ptr(), C.stride(0), A.data_ptr(), A.stride(0), B.data_ptr(), B.stride(0),
+              torch.cuda.current_stream().cuda_stream)
+    return p.stats()
+
+
+def test_guard_verdict_moves_to_the_device_and_tracks_the_data():
+    """1st call: host reads the guard (narrowest path).  Later calls: no host wait,
+    the device picks the first guess or the exact fallback -- results stay bit-exact
+    when the data range changes under the plan, and the next call adapts."""
+    n = 512
+    p = _plan(_lib.SR_INT64, n)
+    rng = np.random.default_rng(0)
+    small = [torch.from_numpy(rng.integers(-9, 10, (n, n))).cuda() for _ in range(2)]
+    big = [torch.from_numpy(rng.integers(-2 ** 40, 2 ** 40, (n, n))).cuda() for _ in range(2)]
+    seq = [(small, "simt_i64_dp4a", 1), (small, "simt_i64_dp4a", 0),
+           (big, "simt_i64", 0),          # guess dp4a is wrong: the device runs the general kernel
+           (big, "simt_i64", 0),          # the hint moved: the general kernel is the first guess
+           (small, "simt_i64", 0)]        # a wider path is always exact (narrows next call)
+    try:
+        for i, (ops, path, syncs) in enumerate(seq):
+            A, B = ops
+            C = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+            st = _exec(p, C, A, B)
+            want = np.zeros((n, n), np.int64)
+            O.gemm_fold(O.SR_INT64, want, A.cpu().numpy(), B.cpu().numpy(), par=True)
+            assert same_bits(C.cpu().numpy(), want), i
+            assert st["guard_syncs"] == syncs, (i, st)
+            assert st["path_name"] == path, (i, st["path_name"])
+        assert st["candidates"] >= 1
+        C = torch.zeros((n, n), dtype=torch.int64, device="cuda")
+        st = _exec(p, C, *small)                       # narrowed again
+        assert st["path_name"] == "simt_i64_dp4a" and st["guard_syncs"] == 0
+    finally:
+        p.close()
+
+
+@pytest.mark.parametrize("sid", ["tropical_i32", "tropical_f32", "tropical"])
+def test_guard_device_fallbacks_exact_for_minplus(sid):
+    """(min,+) chains: a plan primed on small integers meets -0.0 (float) or huge values
+    (int32) -- the device verdict picks the ordered / saturating kernel, bit-exact."""
+    n = 512
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(5)
+    p = _plan(s.sr_id, n, flags=_lib.F_ALLOW_NONPOW2, algo="co2", b=128)
+    try:
+        for it in range(3):
+            A = rng.integers(0, 50, (n, n)).astype(s.dtype)
+            B = rng.integers(0, 50, (n, n)).astype(s.dtype)
+            if it == 1:
+                if sid == "tropical_i32":
+                    A[0, 0] = 2 ** 30
+                else:
+                    A[rng.random(A.shape) < 0.3] = -0.0
+                    B[rng.random(B.shape) < 0.3] = -0.0
+            C0 = rng.integers(0, 80, (n, n)).astype(s.dtype)
+            want = C0.copy()
+            O.schedule_mm(O.SR_BY_NAME[sid], "co2", want, A, B, 128)
+            C = torch.from_numpy(C0.copy()).cuda()
+            st = _exec(p, C, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+            assert same_bits(C.cpu().numpy(), want), (it, st["path_name"])
+            if it == 1:
+                assert st["path_name"] in ("minplus_ordered_leaf_order", "simt_i32_saturating")
+                assert st["guard_syncs"] == 0
+    finally:
+        p.close()
+
+
+def test_async_flag_never_waits_for_the_guard():
+    n = 1024
+    rng = np.random.default_rng(1)
+    A = torch.from_numpy(rng.integers(-100, 100, (n, n)).astype(np.int32)).cuda()
+    C0 = A.clone()
+    p = _plan(_lib.SR_TROPICAL_I32, n, flags=_lib.F_ASYNC)
+    try:
+        C = C0.clone()
+        st = _exec(p, C, A, A)                 # first call of the plan, asynchronous
+        assert st["guard_syncs"] == 0 and st["candidates"] >= 2
+        torch.cuda.synchronize()
+        want = C0.cpu().numpy().copy()
+        O.gemm_fold(O.SR_TROP_I32, want, A.cpu().numpy(), A.cpu().numpy(), par=True)
+        assert same_bits(C.cpu().numpy(), want)
+    finally:
+        p.close()
+
+
+# ---- the device block pool ---------------------------------------------------------
+def test_device_pool_lifo_reissue_and_contracts():
+    p = sm.Pool(2, device="cuda")
+    h1 = p.acquire(0, 1 << 17)
+    p.release(h1)
+    h2 = p.acquire(0, 1 << 17)
+    assert h2 is h1                                 # LIFO reuse (pool.py:97)
+    c = p.snapshot_counts()
+    assert c["reuse_count"] >= 1 and c["fresh_count"] <= 1
+    with pytest.raises(sm.ContractViolation):
+        p.release(h2, worker=1)
+    m = h2.as_matrix(64, sm.FLOAT_RING)
+    m.data.fill_(2.5)
+    assert float(m.data.sum()) == 2.5 * 64 * 64
+    p.release(h2)
+    with pytest.raises(sm.ContractViolation):
+        p.release(h2)                               # double release
+    a, b = p.acquire(0, 1 << 16), p.acquire(1, 1 << 16)
+    p.release(a)
+    p.release(b)
+    assert p.acquire(0, 1 << 16) is b               # newest first
+    p.close()
+
+
+def test_fifo_sabotage_reaches_the_device_pool_and_verify_fails(capsys):
+    from paper_1911_05328_b200.cli import main
+    f = sm.Pool(1, discipline="fifo", device="cuda")
+    try:
+        w = 12345                                   # a size class nothing else uses
+        a, b = f.acquire(0, w), f.acquire(0, w)
+        f.release(a)
+        f.release(b)
+        assert f.acquire(0, w) is a                 # the oldest: FIFO on the device pool
+    finally:
+        f.close()
+    assert main(["verify", "--suite", "pool"]) == 0
+    assert main(["verify", "--suite", "pool", "--sabotage-lifo"]) == 1
+    capsys.readouterr()
+
+
+def test_pool_reuse_across_streams_is_ordered_on_the_device():
+    dev = torch.cuda.current_device()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    before = _lib.pool_counts(dev)["cross_stream_waits"]
+    nb = (64 << 20) + 1792                          # a size class nothing else uses
+    ptr, _ = _lib.pool_acquire(dev, nb, s1.cuda_stream)
+    buf = torch.as_tensor(sm.pool._DeviceBytes(ptr, nb), device="cuda").view(torch.float32)
+    with torch.cuda.stream(s1):
+        torch.cuda._sleep(20_000_000)               # s1 still busy when the block is freed
+        buf.fill_(1.0)
+    _lib.pool_release(dev, ptr, s1.cuda_stream)
+    ptr2, fresh = _lib.pool_acquire(dev, nb, s2.cuda_stream)
+    assert ptr2 == ptr and not fresh
+    buf2 = torch.as_tensor(sm.pool._DeviceBytes(ptr2, nb), device="cuda").view(torch.float32)
+    with torch.cuda.stream(s2):
+        buf2.fill_(2.0)                             # must run after s1's fill
+    torch.cuda.synchronize()
+    assert float(buf2.min()) == 2.0
+    assert _lib.pool_counts(dev)["cross_stream_waits"] == before + 1
+    _lib.pool_release(dev, ptr2, s2.cuda_stream)
+
+
+def test_plan_lifecycle_reuses_the_device_pool():
+    """Creating, running and destroying plans allocates once: later plans of the same
+    shape reuse the pool's blocks (no cudaMalloc / cudaFree per plan)."""
+    dev = torch.cuda.current_device()
+    n = 512
+    A = torch.randn(n, n, dtype=torch.float64, device="cuda")
+    _exec_once = lambda: sm.star_mm(sm.Matrix(torch.zeros_like(A), sm.FLOAT_RING),
+                                    sm.Matrix(A, sm.FLOAT_RING), sm.Matrix(A, sm.FLOAT_RING),
+                                    sm.FLOAT_RING, sm.Config(base_dim=64, workers=148))
+    _exec_once()
+    before = _lib.pool_counts(dev)
+    for _ in range(20):
+        _exec_once()                                # an Executor + plan per call
+    after = _lib.pool_counts(dev)
+    assert after["fresh_count"] == before["fresh_count"]
+    assert after["allocated_bytes"] == before["allocated_bytes"]
+    assert after["trims"] == before["trims"]
+
+
+def test_semiring_matmul_per_call_cost_is_microseconds(capsys):
+    """10k Semiring.matmul calls at 64x64 (the reference's numba kernel is called per
+    leaf): cached plans, pooled staging, device-side guard -- per-call cost in us."""
+    s = sm.INT_RING
+    A = torch.randint(-5, 5, (64, 64), dtype=torch.int64, device="cuda")
+    B = torch.randint(-5, 5, (64, 64), dtype=torch.int64, device="cuda")
+    want = (A.cpu() @ B.cpu()).numpy()
+    for _ in range(50):
+        s.matmul(A, B)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    calls = 10_000
+    for _ in range(calls):
+        out = s.matmul(A, B)
+    torch.cuda.synchronize()
+    us = (time.perf_counter() - t0) / calls * 1e6
+    assert same_bits(out.cpu().numpy(), want)
+    with capsys.disabled():
+        print(f"\n[Semiring.matmul 64x64 int64] {us:.1f} us per call over {calls} calls")
+    assert us < 500.0
+
+
+# ---- instrumentation -------------------------------------------------------------
+@pytest.mark.parametrize("algo", ["tar", "star", "sar", "co2"])
+def test_live_leaf_gauge_is_measured_and_bounded(algo):
+    """Busy-leaves: the leaves observed in flight at once never exceed
+    the persistent workers, over repeated runs; and the gauge is an observation
+    (>= 1), not the grid formula."""
+    n = 1024
+    rng = np.random.default_rng(2)
+    A = rng.integers(-20, 20, (n, n)).astype(np.int64)
+    for rep in range(10):
+        _, st = _run(algo, sm.INT_RING, np.zeros((n, n), np.int64), A, A,
+                     sm.Config(base_dim=64, workers=148, ksplit=None if rep % 2 else 2))
+        assert 1 <= st["live_leaves_max"] <= st["workers"], st
+    with sm.Executor(sm.Config(base_dim=64, workers=148)) as ex:
+        C = sm.Matrix(np.zeros((n, n), np.int64), sm.INT_RING)
+        sm.run_algorithm(ex, "star", C, sm.Matrix(A, sm.INT_RING), sm.Matrix(A, sm.INT_RING), sm.INT_RING)
+        snap = ex.metrics.snapshot()
+        assert snap.base_case_max == ex.last_stats["live_leaves_max"]
+
+
+@pytest.mark.parametrize("p", [1, 4, 16])
+def test_star_space_bound(p):
+    """STAR temp high-water <= ceil(n^2/3) + p*b^2 elements, n = 16b, with
+    the GPU's leaf (the output tile a CTA owns) as b^2 and p the persistent workers."""
+    b = 32
+    n = 16 * b
+    rng = np.random.default_rng(p)
+    A = rng.integers(-20, 20, (n, n)).astype(np.int64)
+    for ks in (None, 1, 2, 3):
+        _, st = _run("star", sm.INT_RING, np.zeros((n, n), np.int64), A, A,
+                     sm.Config(base_dim=b, workers=p, ksplit=ks))
+        tile = 128 * 128                            # CUDA-core leaf tile (int64 path)
+        bound = (-(-n * n // 3) + st["workers"] * tile) * 8
+        assert st["pool_high_water_bytes"] <= bound, (ks, st)

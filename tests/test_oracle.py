@@ -130,3 +130,32 @@ def test_i32_tropical_saturation():
     A = np.array([[-2 ** 31 + 3]], np.int32)
     B = np.array([[-10]], np.int32)
     assert O.matmul(O.SR_TROP_I32, A, B).tolist() == [[-2 ** 31]]
+
+
+SZ = np.load(os.path.join(GOLD, "ref_signed_zero.npz"))
+SZ_CASES = [(1, 4), (2, 8), (4, 16), (8, 32), (16, 32), (32, 32)]
+
+
+@pytest.mark.parametrize("algo", ["co2", "co3", "tar", "sar", "star"])
+@pytest.mark.parametrize("b,n", SZ_CASES)
+def test_signed_zero_schedules_bitwise(algo, b, n):
+    """+-0.0-heavy tropical operands: the oracle's leaf order (first minimum inside a
+    b-leaf, semiring.py:56-58) and np.minimum's second-operand tie (semiring.py:126-127)
+    reproduce the reference bit for bit, sign of zero included."""
+    from _bits import same_bits
+    key = f"n{n}_b{b}"
+    C = SZ[key + "_C0"].copy()
+    O.schedule_mm(O.SR_TROP_F64, algo, C, SZ[key + "_A"], SZ[key + "_B"], b)
+    assert same_bits(C, SZ[f"{key}_{algo}"])
+
+
+@pytest.mark.parametrize("b,n", SZ_CASES)
+def test_signed_zero_naive_and_madd_bitwise(b, n):
+    from _bits import same_bits
+    key = f"n{n}_b{b}"
+    assert same_bits(O.naive_mm(O.SR_TROP_F64, SZ[key + "_A"], SZ[key + "_B"]), SZ[key + "_naive"])
+    C = SZ[key + "_C0"].copy()
+    O.fold(O.SR_TROP_F64, C, SZ[key + "_A"])
+    assert same_bits(C, SZ[key + "_madd"])
+    # the golden really exercises both signs of zero
+    assert np.any(np.signbit(SZ[key + "_star"]) & (SZ[key + "_star"] == 0))
