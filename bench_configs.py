@@ -103,3 +103,33 @@ def from_reference(cid: int, y: np.ndarray) -> np.ndarray:
         x = np.where(np.isinf(y), float(I32_INF), y)
         return x.astype(np.int32)
     return y.astype(cfg["dtype"])
+
+
+# ---- the device generator's spec of each config (csrc/generate.cuh) -------------------
+# Same distributions as make_inputs, drawn from the counter-based device generator
+# (Philox4x32-10 keyed by the config's seed; stream id 0 = A, 1 = B, 2 = C) so that any
+# rank can generate its panels and the oracle can regenerate any sampled tile's panels.
+# None: the matrix is a copy of another ("A" for C = A) or all zeros.
+DEVICE_GEN = {
+    1: {"A": dict(dist="uniform_real", stream_id=0, a=-1.0, b=1.0),
+        "B": dict(dist="uniform_real", stream_id=1, a=-1.0, b=1.0), "C": "zeros"},
+    2: {"A": dict(dist="uniform_int", stream_id=0, a=-16, b=16),
+        "B": dict(dist="uniform_int", stream_id=1, a=-16, b=16), "C": "zeros"},
+    3: {"A": dict(dist="graph", stream_id=0, a=1, b=100, p=0.1, zero_diag=True),
+        "B": "A", "C": "A"},
+    4: {"A": dict(dist="normal", stream_id=0, a=0.0, b=1.0),
+        "B": dict(dist="normal", stream_id=1, a=0.0, b=1.0),
+        "C": dict(dist="uniform_real", stream_id=2, a=-1.0, b=1.0)},
+    5: {"A": dict(dist="uniform_int", stream_id=0, a=1, b=10 ** 6, zero_diag=True),
+        "B": "A", "C": "A"},
+}
+
+
+def device_gen_spec(cid: int, which: str):
+    """Resolve DEVICE_GEN[cid][which] to the generator kwargs (or "zeros")."""
+    spec = DEVICE_GEN[cid][which]
+    while isinstance(spec, str) and spec in ("A", "B", "C"):
+        spec = DEVICE_GEN[cid][spec]
+    if isinstance(spec, dict):
+        return dict(spec, seed=CONFIGS[cid]["seed"])
+    return spec

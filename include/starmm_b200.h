@@ -213,6 +213,27 @@ int  starmm_pool_counts_get(int device, starmm_pool_counts* out);
 int  starmm_pool_reset(int device);
 int  starmm_pool_set_discipline(int device, int fifo);
 
+/* ---- input generation -----------------------------------
+ * Counter-based: element (i, j) of a matrix is a pure function of (seed, stream_id,
+ * GLOBAL row i, GLOBAL column j) -- Philox4x32-10 on (j, i, stream_id, 0), key = seed --
+ * so a rank generates exactly its own panel [row0, row0+rows) x [col0, col0+cols) with
+ * no collective, and any panel can be regenerated on the host (the oracle restates it
+ * bit for bit).  Stream-ordered on `stream`, does not block.  The reference's fixture
+ * generator (matrix.py:196-214, numpy) is what the parity tests keep using; this is
+ * the generator for inputs too large to ship (the BASELINE configs at full size).
+ *   UNIFORM_REAL  a + (b - a) * u, u in [0, 1) (53 bits)       float semirings
+ *   NORMAL        a + b * z, z ~ N(0, 1) (Box-Muller, + - * / and sqrt only)
+ *   UNIFORM_INT   integer in [a, b]                            any semiring
+ *   GRAPH         edge with probability p: weight UNIFORM_INT[a, b], else the
+ *                 additive identity (+inf / INT32_MAX)
+ * STARMM_GEN_ZERO_DIAG sets element (i, i) to 0. */
+enum starmm_dist { STARMM_DIST_UNIFORM_REAL = 0, STARMM_DIST_NORMAL = 1, STARMM_DIST_UNIFORM_INT = 2,
+                   STARMM_DIST_GRAPH = 3 };
+#define STARMM_GEN_ZERO_DIAG 0x1
+int  starmm_generate(int semiring, int dist, void* out, int64_t ld, int64_t rows, int64_t cols,
+                     int64_t row0, int64_t col0, uint64_t seed, uint32_t stream_id, double a,
+                     double b, double p, int gen_flags, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -53,8 +53,13 @@ def lib():
         L.oracle_co3_mm.argtypes = [ci, vp, vp, vp, i64, i64]
         L.oracle_num_threads.restype = ci
         L.oracle_set_threads.argtypes = [ci]
+        L.oracle_generate.argtypes = [ci, ci, vp, i64, i64, i64, i64, i64, ctypes.c_uint64,
+                                      ctypes.c_uint32, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ci]
+        L.oracle_philox4x32_10.argtypes = [ctypes.POINTER(ctypes.c_uint32)] * 3
+        L.oracle_philox4x32_10.restype = None
         for f in (L.oracle_matmul, L.oracle_fold, L.oracle_gemm_fold,
-                  L.oracle_serial_mm, L.oracle_co3_mm):
+                  L.oracle_serial_mm, L.oracle_co3_mm, L.oracle_generate):
             f.restype = ci
         _lib = L
     return _lib
@@ -131,3 +136,29 @@ def num_threads() -> int:
 
 def set_threads(t: int) -> None:
     lib().oracle_set_threads(int(t))
+
+
+# ---- the input generator's restatement (csrc/generate.cuh) ---------------------
+DIST_IDS = {"uniform_real": 0, "normal": 1, "uniform_int": 2, "graph": 3}
+
+
+def philox4x32_10(ctr, key):
+    """Philox4x32-10 block: 4 x uint32 counter, 2 x uint32 key -> 4 x uint32."""
+    c = (ctypes.c_uint32 * 4)(*[int(x) & 0xffffffff for x in ctr])
+    k = (ctypes.c_uint32 * 2)(*[int(x) & 0xffffffff for x in key])
+    o = (ctypes.c_uint32 * 4)()
+    lib().oracle_philox4x32_10(c, k, o)
+    return [int(x) for x in o]
+
+
+def generate(sr: int, dist: str, rows: int, cols: int, row0: int = 0, col0: int = 0, seed: int = 0,
+             stream: int = 0, a: float = 0.0, b: float = 1.0, p: float = 0.0,
+             zero_diag: bool = False) -> np.ndarray:
+    """Host regeneration of a device-generated panel (bit for bit)."""
+    out = np.empty((rows, cols), dtype=DTYPES[sr])
+    rc = lib().oracle_generate(sr, DIST_IDS[dist], _ptr(out), cols, rows, cols, row0, col0,
+                               ctypes.c_uint64(seed), ctypes.c_uint32(stream), ctypes.c_double(a),
+                               ctypes.c_double(b), ctypes.c_double(p), 1 if zero_diag else 0)
+    if rc:
+        raise RuntimeError(f"oracle_generate rc={rc}")
+    return out

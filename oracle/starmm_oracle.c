@@ -407,3 +407,124 @@ int oracle_co3_mm(int sr, void* C, const void* A, const void* B, int64_t n, int6
     free(x.tmp);
     return 0;
 }
+
+/* ==========================================================================
+ * Input generator restatement (paper_1911_05328_b200/csrc/generate.cuh): the
+ * counter-based panels the device generates, regenerated on the host so that
+ * sampled output tiles of full-size runs can be checked.  Philox4x32-10 (Salmon
+ * et al., SC'11; pinned by its published known-answer vectors in
+ * tests/test_oracle.py), then + - * / and sqrt only, no FMA contraction (this file
+ * is compiled with -ffp-contract=off), with the same correctly rounded constants.
+ * ========================================================================== */
+void oracle_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c0 = ctr[0], c1 = ctr[1], c2 = ctr[2], c3 = ctr[3], k0 = key[0], k1 = key[1];
+    for (int r = 0; r < 10; ++r) {
+        uint64_t p0 = (uint64_t)0xD2511F53u * c0, p1 = (uint64_t)0xCD9E8D57u * c2;
+        uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+        uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+        uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+    out[0] = c0; out[1] = c1; out[2] = c2; out[3] = c3;
+}
+
+static const double G_INV_ODD[12] = {
+    0x1.0000000000000p+0, 0x1.5555555555555p-2, 0x1.999999999999ap-3, 0x1.2492492492492p-3,
+    0x1.c71c71c71c71cp-4, 0x1.745d1745d1746p-4, 0x1.3b13b13b13b14p-4, 0x1.1111111111111p-4,
+    0x1.e1e1e1e1e1e1ep-5, 0x1.af286bca1af28p-5, 0x1.8618618618618p-5, 0x1.642c8590b2164p-5};
+static const double G_IFE[14] = {
+    0x1.0000000000000p+0, 0x1.0000000000000p-1, 0x1.5555555555555p-5, 0x1.6c16c16c16c17p-10,
+    0x1.a01a01a01a01ap-16, 0x1.27e4fb7789f5cp-22, 0x1.1eed8eff8d898p-29, 0x1.93974a8c07c9dp-37,
+    0x1.ae7f3e733b81fp-45, 0x1.6827863b97d97p-53, 0x1.e542ba4020225p-62, 0x1.0ce396db7f853p-70,
+    0x1.f2cf01972f578p-80, 0x1.88e85fc6a4e5ap-89};
+static const double G_IFO[14] = {
+    0x1.0000000000000p+0, 0x1.5555555555555p-3, 0x1.1111111111111p-7, 0x1.a01a01a01a01ap-13,
+    0x1.71de3a556c734p-19, 0x1.ae64567f544e4p-26, 0x1.6124613a86d09p-33, 0x1.ae7f3e733b81fp-41,
+    0x1.952c77030ad4ap-49, 0x1.2f49b46814157p-57, 0x1.71b8ef6dcf572p-66, 0x1.761b41316381ap-75,
+    0x1.3f3ccdd165fa9p-84, 0x1.d1ab1c2dccea3p-94};
+
+static double g_log(double x) {
+    uint64_t bits;
+    memcpy(&bits, &x, 8);
+    int e = (int)((bits >> 52) & 0x7ff) - 1023;
+    bits = (bits & 0x000fffffffffffffULL) | 0x3ff0000000000000ULL;
+    double m;
+    memcpy(&m, &bits, 8);
+    if (m > 0x1.6a09e667f3bcdp+0) { m = m * 0.5; e += 1; }
+    const double s = (m - 1.0) / (m + 1.0);
+    const double s2 = s * s;
+    double t = G_INV_ODD[11];
+    for (int k = 10; k >= 0; --k) t = t * s2 + G_INV_ODD[k];
+    const double lm = (2.0 * s) * t;
+    return (double)e * 0x1.62e42fee00000p-1 + ((double)e * 0x1.a39ef35793c76p-33 + lm);
+}
+
+static double g_cos2pi(double u) {
+    const double t = u * 4.0;
+    const int q = (int)t;
+    const double f = t - (double)q;
+    const double a = f * 0x1.921fb54442d18p+0;
+    const double a2 = a * a;
+    double c = -G_IFE[13], sn = -G_IFO[13];
+    for (int k = 12; k >= 0; --k) {
+        const double ce = (k & 1) ? -G_IFE[k] : G_IFE[k];
+        const double so = (k & 1) ? -G_IFO[k] : G_IFO[k];
+        c = c * a2 + ce;
+        sn = sn * a2 + so;
+    }
+    sn = sn * a;
+    switch (q & 3) {
+    case 0: return c;
+    case 1: return -sn;
+    case 2: return -c;
+    default: return sn;
+    }
+}
+
+/* value of element (i, j); *absent for a GRAPH non-edge */
+static double g_value(int dist, double a, double b, double p, uint64_t seed, uint32_t stream,
+                      int64_t i, int64_t j, int* absent) {
+    uint32_t ctr[4] = {(uint32_t)j, (uint32_t)i, stream, 0u}, key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    uint32_t x[4];
+    oracle_philox4x32_10(ctr, key, x);
+    *absent = 0;
+    const double two_m53 = 1.1102230246251565e-16;
+    if (dist == 0) {
+        const uint64_t u53 = ((uint64_t)x[0] << 21) | (x[1] >> 11);
+        return a + (b - a) * ((double)u53 * two_m53);
+    }
+    if (dist == 1) {
+        const uint64_t ua = ((uint64_t)x[0] << 21) | (x[1] >> 11);
+        const uint64_t ub = ((uint64_t)x[2] << 21) | (x[3] >> 11);
+        const double u1 = (double)(ua + 1) * two_m53, u2 = (double)ub * two_m53;
+        const double rad = sqrt(-2.0 * g_log(u1));
+        return a + b * (rad * g_cos2pi(u2));
+    }
+    if (dist == 3) {
+        const uint32_t thr = (uint32_t)(p * 4294967296.0);
+        if (!(x[1] < thr)) { *absent = 1; return 0.0; }
+    }
+    const uint64_t span = (uint64_t)((int64_t)b - (int64_t)a + 1);
+    return (double)((int64_t)a + (int64_t)(((uint64_t)x[0] * span) >> 32));
+}
+
+int oracle_generate(int sr, int dist, void* out, int64_t ld, int64_t rows, int64_t cols, int64_t row0,
+                    int64_t col0, uint64_t seed, uint32_t stream, double a, double b, double p, int flags) {
+    for (int64_t r = 0; r < rows; ++r)
+        for (int64_t c = 0; c < cols; ++c) {
+            const int64_t i = row0 + r, j = col0 + c;
+            int absent;
+            const double v = g_value(dist, a, b, p, seed, stream, i, j, &absent);
+            const int diag = (flags & 1) && i == j;
+            switch (sr) {
+            case SR_INT64: ((int64_t*)out)[r * ld + c] = diag ? 0 : (absent ? 0 : (int64_t)v); break;
+            case SR_FP64: ((double*)out)[r * ld + c] = diag ? 0.0 : (absent ? 0.0 : v); break;
+            case SR_TROP_F64: ((double*)out)[r * ld + c] = diag ? 0.0 : (absent ? INFINITY : v); break;
+            case SR_TROP_F32: ((float*)out)[r * ld + c] = diag ? 0.0f : (absent ? INFINITY : (float)v); break;
+            case SR_TROP_I32: ((int32_t*)out)[r * ld + c] = diag ? 0 : (absent ? I32_INF : (int32_t)v); break;
+            default: return 1;
+            }
+        }
+    return 0;
+}

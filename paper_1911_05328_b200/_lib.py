@@ -119,6 +119,10 @@ def lib():
         L.starmm_madd.restype = ci
         L.starmm_atomic_accumulate.argtypes = [ci, vp, i64, vp, i64, i64, i64, vp, ci]
         L.starmm_atomic_accumulate.restype = ci
+        L.starmm_generate.argtypes = [ci, ci, vp, i64, i64, i64, i64, i64, ctypes.c_uint64,
+                                      ctypes.c_uint32, ctypes.c_double, ctypes.c_double,
+                                      ctypes.c_double, ci, vp]
+        L.starmm_generate.restype = ci
         L.starmm_pool_acquire.argtypes = [ci, i64, vp, ctypes.POINTER(vp), ctypes.POINTER(ci)]
         L.starmm_pool_acquire.restype = ci
         L.starmm_pool_release.argtypes = [ci, vp, vp]

@@ -18,16 +18,26 @@ template <class Pol> constexpr bool has_occ1_build() {
            std::is_same<Pol, PolS16x2Min>::value;
 }
 
+// The >48 KB dynamic-smem opt-in is an attribute of the function in the CURRENT
+// device's context: remembered per device, not per process.
+constexpr int SL_MAX_DEV = 64;
+inline int sl_device() {
+    int d = 0;
+    if (cudaGetDevice(&d) != cudaSuccess) { cudaGetLastError(); return 0; }
+    return d < SL_MAX_DEV ? d : SL_MAX_DEV - 1;
+}
+
 template <class Pol, class Sr>
 int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
     constexpr int smem = simt::smem_bytes<Pol>();
+    const int dev = sl_device();
     if constexpr (has_occ1_build<Pol>() && Pol::OCC > 1) {
         if (grid <= sms) {
             auto k1 = simt_mm_kernel<Pol, Sr, 1>;
-            static bool attr1 = false;
-            if (!attr1) {
+            static bool attr1[SL_MAX_DEV] = {};
+            if (!attr1[dev]) {
                 SL_CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-                attr1 = true;
+                attr1[dev] = true;
             }
             k1<<<grid, simt::THREADS, smem, s>>>(p);
             SL_CK(cudaGetLastError());
@@ -35,10 +45,10 @@ int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
         }
     }
     auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
-    static bool attr_done = false;
-    if (!attr_done) {
+    static bool attr_done[SL_MAX_DEV] = {};
+    if (!attr_done[dev]) {
         SL_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-        attr_done = true;
+        attr_done[dev] = true;
     }
     kern<<<grid, simt::THREADS, smem, s>>>(p);
     SL_CK(cudaGetLastError());

@@ -33,6 +33,7 @@
 #include "tc_gemm.cuh"
 #include "ozaki.cuh"
 #include "ordered_kernel.cuh"
+#include "generate.cuh"
 #include "simt_launch.h"
 #include "guard.h"
 #include "arena.h"
@@ -1109,8 +1110,15 @@ bool needs_guard(const starmm_plan* P) {
 
 }  // namespace
 
+// force_async: the caller synchronises (host path, Strassen leaves).  host_guard: read
+// the range guard on the host every call -- the host-buffer schedule, whose row blocks
+// alternate between two compute streams: a predicated-off fallback TILE kernel still
+// needs SM slots to start and exit, so queued behind the other stream's persistent
+// kernel it would hold back this stream's downloads (config 3 e2e 54 -> 49.5 Tops/s);
+// that schedule is a blocking call anyway.
 static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int64_t lda,
-                        const void* B, int64_t ldb, void* stream, bool force_async) {
+                        const void* B, int64_t ldb, void* stream, bool force_async,
+                        bool host_guard = false) {
     if (!P || !C || !A || !B) return STARMM_CONTRACT_VIOLATION;
     if (ldc < P->n || lda < P->k || ldb < P->n) return STARMM_DIM_MISMATCH;
     const int eb = elem_bytes(P->sr);
@@ -1160,7 +1168,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             break;
         }
         int first = (P->hint && P->hint != PATH_MIN_ORDERED) ? P->hint : fastest_path(P);
-        const bool host_sync = genv ? genv[0] == '1' : (!async && P->hint == 0);
+        const bool host_sync = genv ? genv[0] == '1' : (host_guard || (!async && P->hint == 0));
         if (host_sync) {
             // ---- host-side verdict: pack, read the guard, re-pack if it disallows ----
             bool guard_pending = true;
@@ -1685,7 +1693,7 @@ static int execute_host_remote(starmm_plan* P, const void* A, int64_t lda, const
             P->k = kb[c + 1] - k0;
             P->kofs = k0;
             // (C is not touched: every write-back goes to the peers)
-            rc = execute_impl(P, dA, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true);
+            rc = execute_impl(P, dA, n, (char*)dA + k0 * eb, k, (char*)dB + k0 * n * eb, n, cs, true, true);
             P->k = k;
             P->kofs = 0;
         }
@@ -1818,7 +1826,7 @@ int starmm_execute_host(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         // schedule, so the host path never times its kernels)
         const int f = saved_flags & ~STARMM_F_TIME_MAIN;
         Q->flags = store ? (f | STARMM_F_INIT_IDENTITY) : (f & ~STARMM_F_INIT_IDENTITY);
-        int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true);
+        int r = execute_impl(Q, Cd, n, Ad, k, Bd, n, st, true, true);
         Q->m = m; Q->k = k; Q->kofs = 0; Q->flags = saved_flags; Q->ksplit_req = saved_ks;
         return r;
     };
@@ -2036,6 +2044,41 @@ int starmm_pool_reset(int device) {
     }
     for (auto* p : drop) starmm_plan_destroy(p);
     c->arena.reset();
+    return STARMM_OK;
+}
+
+// ---- input generation (generate.cuh) ----------------------------------------
+int starmm_generate(int semiring, int dist, void* out, int64_t ld, int64_t rows, int64_t cols,
+                    int64_t row0, int64_t col0, uint64_t seed, uint32_t stream_id, double a,
+                    double b, double p, int gen_flags, void* stream) {
+    if (!out || rows < 0 || cols < 0 || ld < cols || row0 < 0 || col0 < 0) return STARMM_CONTRACT_VIOLATION;
+    if (dist < STARMM_DIST_UNIFORM_REAL || dist > STARMM_DIST_GRAPH) return STARMM_CONTRACT_VIOLATION;
+    if (row0 + rows > (1LL << 31) || col0 + cols > (1LL << 31)) return STARMM_TOO_LARGE;
+    const bool fl = semiring == STARMM_SR_FP64 || semiring == STARMM_SR_TROPICAL_F64 ||
+                    semiring == STARMM_SR_TROPICAL_F32;
+    if ((dist == STARMM_DIST_UNIFORM_REAL || dist == STARMM_DIST_NORMAL) && !fl) return STARMM_CONTRACT_VIOLATION;
+    if ((dist == STARMM_DIST_UNIFORM_INT || dist == STARMM_DIST_GRAPH) &&
+        !(b >= a && b - a < 4294967296.0 && a == std::floor(a) && b == std::floor(b)))
+        return STARMM_CONTRACT_VIOLATION;
+    if (rows == 0 || cols == 0) return STARMM_OK;
+    gen::Params g;
+    g.dist = dist; g.flags = gen_flags; g.a = a; g.b = b; g.p = p; g.seed = seed; g.stream = stream_id;
+    const dim3 grid = grid2d(rows, cols);
+    cudaStream_t s = (cudaStream_t)stream;
+    switch (semiring) {
+    case STARMM_SR_INT64:
+        gen::generate_kernel<SrInt64><<<grid, 256, 0, s>>>((long long*)out, ld, rows, cols, row0, col0, g); break;
+    case STARMM_SR_FP64:
+        gen::generate_kernel<SrFp64><<<grid, 256, 0, s>>>((double*)out, ld, rows, cols, row0, col0, g); break;
+    case STARMM_SR_TROPICAL_F64:
+        gen::generate_kernel<SrTropF64><<<grid, 256, 0, s>>>((double*)out, ld, rows, cols, row0, col0, g); break;
+    case STARMM_SR_TROPICAL_F32:
+        gen::generate_kernel<SrTropF32><<<grid, 256, 0, s>>>((float*)out, ld, rows, cols, row0, col0, g); break;
+    case STARMM_SR_TROPICAL_I32:
+        gen::generate_kernel<SrTropI32><<<grid, 256, 0, s>>>((int*)out, ld, rows, cols, row0, col0, g); break;
+    default: return STARMM_CONTRACT_VIOLATION;
+    }
+    CK(cudaGetLastError());
     return STARMM_OK;
 }
 

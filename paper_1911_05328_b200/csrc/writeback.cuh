@@ -58,8 +58,9 @@ STARMM_DEV void fold_batched(Each each, Addr addr, bool cg) {
 }
 
 // FOLD_CH: elements per batched read-fold-write chunk; 0 = element by element (the DMMA
-// kernel: its epilogue is hidden by the co-resident CTA, and any change to this code
-// shifted its register allocation and cost 1-3% -- profiles/r01k_epilogue_ab.md)
+// kernel, whose full aligned FOLD tiles take its own vectorised epilogue (EPI=1,
+// dmma_kernel.cuh) -- this generic path only sees its ragged / protocol tiles; changes
+// here shifted its register allocation and cost 1-3%, profiles/r01k_epilogue_ab.md)
 template <class Sr, int BM, int BN, int NTHREADS, int FOLD_CH, class Each>
 STARMM_DEV void writeback(const WbParams& w, const TaskGrid& g, int tm, int tn, int s, int tile,
                           int worker, int mode, int pair_seen, Each each) {

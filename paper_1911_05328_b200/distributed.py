@@ -89,7 +89,7 @@ class DistributedMM:
                  base_dim: int = 64, workers: int = 1, group_ks=None,
                  local_mm: Optional[Callable] = None, device: Optional[int] = None,
                  time_kernel: bool = False, combine: str = "nccl", int_tensor: bool = False,
-                 fp64_emu: bool = False):
+                 fp64_emu: bool = False, fastpath: bool = True):
         self.n, self.s, self.grid, self.rank = n, semiring, grid, rank
         self.I, self.J, self.K = grid.coords(rank)
         self.r0, self.r1 = block_bounds(n, grid.pr, self.I)
@@ -100,6 +100,15 @@ class DistributedMM:
         self.init_identity = self.K > 0
         self.local_mm = local_mm
         self.plan = None
+        self.combine_requested = combine
+        self.peer_verdicts = None
+        if local_mm is None and combine == "fused" and grid.ks > 1:
+            # the fused combine writes into the owners' rows over NVLink peer memory: every
+            # member of the k-split group must reach every other member's device, else the
+            # group falls back to the NCCL reduce-scatter (all members decide alike)
+            dev = device if device is not None else torch.cuda.current_device()
+            self.peer_verdicts = gather_peer_access(dev, group_ks)
+            combine = decide_combine(combine, self.peer_verdicts)
         if local_mm is None:
             fused = combine == "fused" and grid.ks > 1
             # the fused combine folds every partial into the owners' rows, so no rank
@@ -112,6 +121,8 @@ class DistributedMM:
                 flags |= _lib.F_INT_TENSOR
             if fp64_emu:
                 flags |= _lib.F_FP64_EMU
+            if not fastpath:
+                flags |= _lib.F_NO_FASTPATH
             self.plan = _lib.Plan(semiring.sr_id, algo, "pooled", self.m, self.nn, self.k,
                                   base_dim, workers, -1,
                                   device if device is not None else torch.cuda.current_device(),
@@ -259,6 +270,30 @@ class DistributedMM:
         if self.plan is not None:
             self.plan.close()
             self.plan = None
+
+
+def peer_access_local(device: int, peer_devices) -> bool:
+    """Can `device` map every peer's memory (CUDA IPC + peer access over NVLink)?  The
+    same device (ranks sharing a GPU) always can."""
+    return all(d == device or torch.cuda.can_device_access_peer(device, d) for d in peer_devices)
+
+
+def gather_peer_access(device: int, group=None):
+    """Every group member's peer-access verdict towards all the others."""
+    devs = [None] * dist.get_world_size(group)
+    dist.all_gather_object(devs, int(device), group=group)
+    ok = peer_access_local(device, devs)
+    verdicts = [None] * len(devs)
+    dist.all_gather_object(verdicts, bool(ok), group=group)
+    return verdicts
+
+
+def decide_combine(requested: str, verdicts) -> str:
+    """The k-split combine a group runs: the fused peer-memory one only if every member
+    can reach every other; otherwise the NCCL reduce-scatter."""
+    if requested == "fused" and verdicts is not None and not all(verdicts):
+        return "nccl"
+    return requested
 
 
 def ks_groups(grid: Grid):

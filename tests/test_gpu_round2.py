@@ -365,3 +365,40 @@ def test_star_space_bound(p):
         tile = 128 * 128                            # CUDA-core leaf tile (int64 path)
         bound = (-(-n * n // 3) + st["workers"] * tile) * 8
         assert st["pool_high_water_bytes"] <= bound, (ks, st)
+
+
+# ---- counter-based input generation ---------------------------
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+@pytest.mark.parametrize("what", ["A", "B", "C"])
+def test_device_generator_matches_oracle_regeneration(cid, what):
+    """generate_panel on the GPU equals the oracle's host restatement bit for bit, for
+    every config's matrices, at panel offsets (so the bench's sampled-tile check can
+    regenerate any rank's panels)."""
+    from bench_configs import CONFIGS, device_gen_spec
+    spec = device_gen_spec(cid, what)
+    if spec == "zeros":
+        pytest.skip("all-zero matrix")
+    s = sm.get_semiring(CONFIGS[cid]["semiring"])
+    dev = sm.generate_panel(s, rows=300, cols=260, row0=4093, col0=4000, **spec).cpu().numpy()
+    spec = dict(spec)
+    spec["stream"] = spec.pop("stream_id")
+    host = O.generate(O.SR_BY_NAME[CONFIGS[cid]["semiring"]], rows=300, cols=260, row0=4093,
+                      col0=4000, **spec)
+    assert same_bits(dev, host), diff_count(dev, host)
+
+
+def test_generated_config_panel_product_vs_oracle():
+    """End to end on generated inputs: a config-4-distributed 1024^3 STAR product's
+    sampled tiles vs the oracle on host-regenerated panels."""
+    from bench_configs import device_gen_spec
+    n = 1024
+    s = sm.FLOAT_RING
+    A = sm.generate_panel(s, rows=n, cols=n, **device_gen_spec(4, "A"))
+    B = sm.generate_panel(s, rows=n, cols=n, **device_gen_spec(4, "B"))
+    C = sm.generate_panel(s, rows=n, cols=n, **device_gen_spec(4, "C"))
+    C0 = C.cpu().numpy()
+    sm.star_mm(sm.Matrix(C, s), sm.Matrix(A, s), sm.Matrix(B, s), s, sm.Config(base_dim=64, workers=148))
+    want = C0.copy()
+    O.gemm_fold(O.SR_FP64, want, A.cpu().numpy(), B.cpu().numpy(), par=True)
+    got = C.cpu().numpy()
+    assert np.all(np.abs(got - want) <= 1e-10 * np.sqrt(n) * np.maximum(1, np.abs(want)))

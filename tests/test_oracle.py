@@ -159,3 +159,54 @@ def test_signed_zero_naive_and_madd_bitwise(b, n):
     assert same_bits(C, SZ[key + "_madd"])
     # the golden really exercises both signs of zero
     assert np.any(np.signbit(SZ[key + "_star"]) & (SZ[key + "_star"] == 0))
+
+
+# ---- the input generator's restatement (csrc/generate.cuh) --------------------------
+def test_philox4x32_10_known_answers():
+    """Random123's published Philox4x32-10 known-answer vectors."""
+    assert O.philox4x32_10([0, 0, 0, 0], [0, 0]) == [0x6627e8d5, 0xe169c58d, 0xbc57ac4c, 0x9b00dbd8]
+    assert O.philox4x32_10([0xffffffff] * 4, [0xffffffff] * 2) == \
+        [0x408f276d, 0x41c83b0e, 0xa20bc7c6, 0x6d5451fd]
+    assert O.philox4x32_10([0x243f6a88, 0x85a308d3, 0x13198a2e, 0x03707344], [0xa4093822, 0x299f31d0]) == \
+        [0xd16cfe09, 0x94fdcceb, 0x5001e420, 0x24126ea1]
+
+
+@pytest.mark.parametrize("cid", [1, 2, 3, 4, 5])
+def test_generator_is_panel_invariant_and_matches_the_config_distribution(cid):
+    """Element (i, j) depends only on (seed, stream, i, j): a panel cut anywhere equals
+    the same window of a larger panel; moments match BASELINE's distributions."""
+    from bench_configs import device_gen_spec
+    sr = O.SR_BY_NAME[CONFIGS[cid]["semiring"]]
+    spec = dict(device_gen_spec(cid, "A"))
+    spec["stream"] = spec.pop("stream_id")
+    big = O.generate(sr, rows=200, cols=300, row0=1000, col0=2000, **spec)
+    sub = O.generate(sr, rows=37, cols=51, row0=1100, col0=2222, **spec)
+    assert np.array_equal(big[100:137, 222:273], sub)
+    x = big.astype(np.float64)
+    if cid == 4:
+        assert abs(x.mean()) < 0.02 and abs(x.std() - 1.0) < 0.02
+    if cid == 1:
+        assert x.min() >= -1 and x.max() < 1 and abs(x.mean()) < 0.02
+    if cid == 2:
+        assert x.min() == -16 and x.max() == 16 and abs(x.mean()) < 0.2
+    if cid == 3:
+        fin = np.isfinite(x)
+        assert abs(fin.mean() - 0.1) < 0.01 and x[fin].min() >= 1 and x[fin].max() <= 100
+    if cid == 5:
+        assert x.min() >= 1 and x.max() <= 10 ** 6
+        d = O.generate(sr, rows=64, cols=64, row0=0, col0=0, **spec)
+        assert np.all(np.diag(d) == 0)                  # 0 on the diagonal
+
+
+def test_generator_normal_is_accurate_box_muller():
+    """The + - * / log and cos of the normal transform agree with libm to ~1e-15."""
+    import math
+    seed, stream = 3, 0
+    z = O.generate(O.SR_FP64, "normal", 4, 64, seed=seed, stream=stream)
+    for j in range(64):
+        x = O.philox4x32_10([j, 0, stream, 0], [seed, 0])
+        ua = (x[0] << 21) | (x[1] >> 11)
+        ub = (x[2] << 21) | (x[3] >> 11)
+        u1, u2 = (ua + 1) * 2.0 ** -53, ub * 2.0 ** -53
+        want = math.sqrt(-2.0 * math.log(u1)) * math.cos(2 * math.pi * u2)
+        assert abs(z[0, j] - want) <= 1e-13 * max(1.0, abs(want)), (j, z[0, j], want)
