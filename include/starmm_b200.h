@@ -212,6 +212,10 @@ int  starmm_pool_release(int device, void* block, void* stream);
 int  starmm_pool_counts_get(int device, starmm_pool_counts* out);
 int  starmm_pool_reset(int device);
 int  starmm_pool_set_discipline(int device, int fifo);
+/* bytes the pool may own before it reuses a block that is still in use on another
+ * stream (ordered by an event wait) or returns cached blocks to the driver; default
+ * 3/4 of the device memory (env STARMM_POOL_LIMIT_MB); returns the previous limit in *old */
+int  starmm_pool_set_limit(int device, int64_t bytes, int64_t* old);
 
 /* ---- input generation -----------------------------------
  * Counter-based: element (i, j) of a matrix is a pure function of (seed, stream_id,

@@ -131,6 +131,8 @@ def lib():
         L.starmm_pool_counts_get.restype = ci
         L.starmm_pool_reset.argtypes = [ci]
         L.starmm_pool_reset.restype = ci
+        L.starmm_pool_set_limit.argtypes = [ci, i64, ctypes.POINTER(i64)]
+        L.starmm_pool_set_limit.restype = ci
         L.starmm_pool_set_discipline.argtypes = [ci, ci]
         L.starmm_pool_set_discipline.restype = ci
         if L.starmm_abi_version() != ABI_VERSION:
@@ -246,3 +248,10 @@ def pool_reset(device: int) -> None:
 
 def pool_set_discipline(device: int, fifo: bool) -> None:
     check(lib().starmm_pool_set_discipline(device, 1 if fifo else 0), "starmm_pool_set_discipline")
+
+
+def pool_set_limit(device: int, nbytes: int) -> int:
+    """Set the pool's owned-bytes limit; returns the previous one."""
+    old = ctypes.c_int64(0)
+    check(lib().starmm_pool_set_limit(device, nbytes, ctypes.byref(old)), "starmm_pool_set_limit")
+    return int(old.value)

@@ -100,13 +100,35 @@ struct DevArena {
         const size_t b = size_class(bytes);
         std::unique_lock<std::mutex> g(mu);
         auto it = free_.find(b);
+        // Which free block: in discipline order (LIFO: newest first), the first one that is
+        // ready for `s` without a wait -- released on `s` itself, unfenced, or its fence
+        // already passed.  Only when none is ready and the pool is at its limit does `s`
+        // wait on another stream's fence: two streams alternating launches (the host
+        // path's twin compute streams) must not be chained through their staging blocks.
+        long pick = -1;
+        bool must_wait = false;
         if (it != free_.end() && !it->second.empty()) {
-            Blk blk = fifo ? it->second.front() : it->second.back();   // LIFO pop (pool.py:97)
-            if (fifo) it->second.pop_front(); else it->second.pop_back();
+            auto& dq = it->second;
+            const long nb = (long)dq.size();
+            for (long q = 0; q < nb && pick < 0; ++q) {
+                const long idx = fifo ? q : nb - 1 - q;
+                const Blk& x = dq[(size_t)idx];
+                if (!x.fence || x.fence->st == s || cudaEventQuery(x.fence->ev) == cudaSuccess) pick = idx;
+            }
+            if (pick < 0) cudaGetLastError();                    // (cudaErrorNotReady)
+            if (pick < 0 && limit > 0 && c.allocated + (long long)b > limit) {
+                pick = fifo ? 0 : nb - 1;
+                must_wait = true;
+            }
+        }
+        if (pick >= 0) {
+            auto& dq = it->second;
+            Blk blk = dq[(size_t)pick];
+            dq.erase(dq.begin() + pick);
             c.cached -= (long long)b;
-            if (blk.fence && blk.fence->st != s) {
+            if (must_wait) {
                 cudaError_t e = cudaStreamWaitEvent(s, blk.fence->ev, 0);
-                if (e != cudaSuccess) { it->second.push_back(blk); c.cached += (long long)b; return e; }
+                if (e != cudaSuccess) { dq.push_back(blk); c.cached += (long long)b; return e; }
                 ++c.waits;
             }
             *out = blk.p;

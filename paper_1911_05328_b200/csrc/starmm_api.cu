@@ -2082,6 +2082,15 @@ int starmm_generate(int semiring, int dist, void* out, int64_t ld, int64_t rows,
     return STARMM_OK;
 }
 
+int starmm_pool_set_limit(int device, int64_t bytes, int64_t* old) {
+    DeviceCtx* c = device_ctx(device);
+    if (!c || bytes < 0) return STARMM_CONTRACT_VIOLATION;
+    std::lock_guard<std::mutex> g(c->arena.mu);
+    if (old) *old = c->arena.limit;
+    c->arena.limit = bytes;
+    return STARMM_OK;
+}
+
 int starmm_pool_set_discipline(int device, int fifo) {
     DeviceCtx* c = device_ctx(device);
     if (!c || (fifo != 0 && fifo != 1)) return STARMM_CONTRACT_VIOLATION;

@@ -269,25 +269,49 @@ def test_fifo_sabotage_reaches_the_device_pool_and_verify_fails(capsys):
 
 
 def test_pool_reuse_across_streams_is_ordered_on_the_device():
+    """A block released on a busy stream is not handed to another stream while the pool
+    has room (a fresh block instead: streams are not chained through the pool); at its
+    limit the pool reuses it, ordered by an event wait on the device."""
     dev = torch.cuda.current_device()
     s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
-    before = _lib.pool_counts(dev)["cross_stream_waits"]
     nb = (64 << 20) + 1792                          # a size class nothing else uses
     ptr, _ = _lib.pool_acquire(dev, nb, s1.cuda_stream)
     buf = torch.as_tensor(sm.pool._DeviceBytes(ptr, nb), device="cuda").view(torch.float32)
     with torch.cuda.stream(s1):
-        torch.cuda._sleep(20_000_000)               # s1 still busy when the block is freed
+        torch.cuda._sleep(50_000_000)               # s1 still busy when the block is freed
         buf.fill_(1.0)
     _lib.pool_release(dev, ptr, s1.cuda_stream)
-    ptr2, fresh = _lib.pool_acquire(dev, nb, s2.cuda_stream)
-    assert ptr2 == ptr and not fresh
-    buf2 = torch.as_tensor(sm.pool._DeviceBytes(ptr2, nb), device="cuda").view(torch.float32)
-    with torch.cuda.stream(s2):
-        buf2.fill_(2.0)                             # must run after s1's fill
+    other, fresh = _lib.pool_acquire(dev, nb, s2.cuda_stream)
+    assert other != ptr and fresh                   # room left: no cross-stream chaining
+    _lib.pool_release(dev, other, s2.cuda_stream)
     torch.cuda.synchronize()
-    assert float(buf2.min()) == 2.0
-    assert _lib.pool_counts(dev)["cross_stream_waits"] == before + 1
-    _lib.pool_release(dev, ptr2, s2.cuda_stream)
+    # at the limit: a block still in use on s1 is reused by s2 behind an event wait
+    x, _ = _lib.pool_acquire(dev, nb, s1.cuda_stream)
+    bx = torch.as_tensor(sm.pool._DeviceBytes(x, nb), device="cuda").view(torch.float32)
+    with torch.cuda.stream(s1):
+        torch.cuda._sleep(50_000_000)
+        bx.fill_(1.0)
+    _lib.pool_release(dev, x, s1.cuda_stream)
+    before = _lib.pool_counts(dev)
+    old = _lib.pool_set_limit(dev, before["allocated_bytes"])
+    got = []
+    try:
+        for _ in range(4):                          # ready blocks first, then x
+            p2, fresh = _lib.pool_acquire(dev, nb, s2.cuda_stream)
+            assert not fresh
+            got.append(p2)
+            if p2 == x:
+                break
+        assert got[-1] == x
+        with torch.cuda.stream(s2):
+            bx.fill_(2.0)                           # must run after s1's fill
+        torch.cuda.synchronize()
+        assert float(bx.min()) == 2.0
+        assert _lib.pool_counts(dev)["cross_stream_waits"] == before["cross_stream_waits"] + 1
+    finally:
+        for p2 in got:
+            _lib.pool_release(dev, p2, s2.cuda_stream)
+        _lib.pool_set_limit(dev, old)
 
 
 def test_plan_lifecycle_reuses_the_device_pool():

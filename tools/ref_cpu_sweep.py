@@ -1,0 +1,95 @@
+"""The reference's own CPU path, swept on the GPU box's host cores:
+star_mm (classic.py:314-316) from the UNMODIFIED package in baseline/_ref under
+Config(base_dim=b, workers=W) for W in {1, os.cpu_count()}, n = 256, 512, ... doubling
+after a small-n JIT warm-up, stopping at the first run over the cap (600 s) -- a run
+whose predicted time (8x the previous) exceeds 1.5x the cap is recorded as skipped
+rather than burnt.  Writes profiles/r02_ref_cpu_sweep.json (largest n completed per
+semiring and W, Gop/s at every n).
+
+  python tools/ref_cpu_sweep.py [--cap 600] [--semirings float,int,tropical]
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import time
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+CHILD = r"""
+import os, sys, time, json
+sys.dont_write_bytecode = True
+sys.path.insert(0, os.path.join(%(repo)r, "baseline", "_ref"))
+sys.path.insert(0, %(repo)r)
+import numpy as np
+import starmm as ref
+from bench_configs import make_inputs, to_reference
+cid, n, W, b = %(cid)d, %(n)d, %(W)d, %(b)d
+s = ref.get_semiring(%(sid)r)
+A, B, C = make_inputs(cid, n)
+Am = ref.Matrix(to_reference(cid, A), s)
+Bm = Am if B is A else ref.Matrix(to_reference(cid, B), s)
+Cm = ref.Matrix(to_reference(cid, C).copy(), s)
+t0 = time.perf_counter()
+ref.star_mm(Cm, Am, Bm, s, ref.Config(base_dim=b, workers=W))
+print(json.dumps({"seconds": time.perf_counter() - t0}))
+"""
+
+CID_OF = {"float": 4, "int": 2, "tropical": 5}
+
+
+def run_one(sid, n, W, b, cap):
+    code = CHILD % {"repo": REPO, "cid": CID_OF[sid], "n": n, "W": W, "b": b, "sid": sid}
+    env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/starmm_ref_numba_cache")
+    t0 = time.perf_counter()
+    try:
+        p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=cap,
+                           env=env)
+    except subprocess.TimeoutExpired:
+        return {"n": n, "status": f"over {cap:.0f} s (killed)", "seconds": time.perf_counter() - t0}
+    if p.returncode != 0:
+        return {"n": n, "status": "error", "stderr": p.stderr[-400:]}
+    sec = json.loads(p.stdout.strip().splitlines()[-1])["seconds"]
+    return {"n": n, "status": "ok", "seconds": sec, "gops": 2.0 * n ** 3 / sec / 1e9}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--cap", type=float, default=600.0)
+    ap.add_argument("--semirings", default="float,int,tropical")
+    ap.add_argument("--workers", default="")
+    args = ap.parse_args()
+    cores = os.cpu_count() or 1
+    Ws = [int(x) for x in args.workers.split(",")] if args.workers else sorted({1, cores})
+    out = {"host_cores": cores, "cap_seconds": args.cap, "series": [], "largest_n": {},
+           "how": "reference star_mm (baseline/_ref, unmodified), Config(base_dim=b, workers=W); "
+                  "b = 32 up to n = 512, else 64; inputs = the BASELINE config distributions "
+                  "(bench_configs.make_inputs: float -> config 4, int -> config 2, tropical -> "
+                  "config 5's weights up-cast to float64)"}
+    for sid in args.semirings.split(","):
+        run_one(sid, 64, 1, 32, args.cap)                       # numba JIT into the cache
+        for W in Ws:
+            rows, n, prev = [], 256, None
+            while True:
+                b = 32 if n <= 512 else 64
+                if prev is not None and prev * 8 > 1.5 * args.cap:
+                    rows.append({"n": n, "status": f"skipped: predicted {prev * 8:.0f} s > 1.5 x cap"})
+                    break
+                r = run_one(sid, n, W, b, args.cap)
+                rows.append(r)
+                print(sid, W, r, flush=True)
+                if r["status"] != "ok" or r["seconds"] > args.cap:
+                    break
+                prev = r["seconds"]
+                n *= 2
+            done = [r for r in rows if r["status"] == "ok" and r["seconds"] <= args.cap]
+            out["series"].append({"semiring": sid, "workers": W, "runs": rows})
+            out["largest_n"][f"{sid}:W{W}"] = max((r["n"] for r in done), default=None)
+    path = os.path.join(REPO, "profiles", "r02_ref_cpu_sweep.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print(json.dumps(out["largest_n"]))
+
+
+if __name__ == "__main__":
+    main()
