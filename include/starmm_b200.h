@@ -128,6 +128,8 @@ typedef struct {
     int64_t guard_syncs;             /* host waits on the range guard (0 once a plan has a
                                         verdict: the device decides)        */
     int64_t candidates;              /* paths queued behind the device-side verdict (1: none) */
+    int64_t cluster_size;            /* > 0: the k-slices of a tile ran on one thread-block
+                                        cluster and merged through DSMEM (DMMA path)      */
 } starmm_stats;
 
 /* The device's block pool (pool.py:67-167): one per device, shared by every plan and

@@ -107,14 +107,27 @@ __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long
     RangeAcc acc;
     const long long r0 = (long long)blockIdx.y * 32, w0 = (long long)blockIdx.x * 32;   // words
     const int tx = threadIdx.x, ty = threadIdx.y;                                       // 32 x 8
+    // a thread's 4 int64 (32 B) as two 16-byte loads when the row allows it (4 separate
+    // 8-byte loads per thread left each load instruction a quarter of its sectors)
+    const bool vec = ((reinterpret_cast<uintptr_t>(A) | (uintptr_t)(lda * 8)) & 15) == 0;
     for (int i = ty; i < 32; i += 8) {
         const long long r = r0 + i, k = (w0 + tx) * 4;
+        long long v[4] = {0, 0, 0, 0};
+        if (r < rows) {
+            if (vec && k + 3 < kdim) {
+                const longlong2 x0 = *reinterpret_cast<const longlong2*>(A + r * lda + k);
+                const longlong2 x1 = *reinterpret_cast<const longlong2*>(A + r * lda + k + 2);
+                v[0] = x0.x; v[1] = x0.y; v[2] = x1.x; v[3] = x1.y;
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) v[q] = k + q < kdim ? A[r * lda + k + q] : 0;
+            }
+        }
         unsigned w = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            long long v = (r < rows && k + q < kdim) ? A[r * lda + k + q] : 0;
-            acc.add(v);
-            w |= ((unsigned)(v & 0xff)) << (8 * q);
+            acc.add(v[q]);
+            w |= ((unsigned)(v[q] & 0xff)) << (8 * q);
         }
         tile[i][tx] = (int)w;
     }

@@ -134,6 +134,7 @@ struct CandInfo {
     long long tasks = 0, workers = 0, S = 1, tar_levels = 0, balanced_workers = 0, pair_count = 0;
     long long raw_count = 0, raw_bytes = 0;
     int s_log2 = 0;
+    int cluster = 0;         // > 0: DMMA split-k merged on a cluster of this many CTAs
 };
 
 }  // namespace
@@ -217,7 +218,7 @@ PathShape path_shape(int path) {
         PathShape sh{DmmaProd::BM, DmmaProd::BN, DmmaProd::BK, DmmaProd::MIN_BLOCKS, 8000, 8000};
         return sh;
     }
-    case PATH_SIMT_I64: return simt_shape<PolI64>();
+    case PATH_SIMT_I64: return simt_shape<PolI64Lo>();
     case PATH_SIMT_I64_NARROW: return simt_shape<PolI64Narrow>();
     case PATH_SIMT_F32_PAIR: return simt_shape<PolF32Pair>();
     case PATH_SIMT_I32_CARRIER: return simt_shape<PolF32Pair>();
@@ -271,6 +272,91 @@ int launch_dmma(const DmmaParams& p, int grid, bool gate, cudaStream_t s) {
     return STARMM_OK;
 }
 
+
+// ---- DMMA split-k on clusters (dmma_fp64_cluster_kernel) ------------------------------
+// Cluster mode runs the S k-slices of a tile on the S CTAs of one cluster and merges
+// them through DSMEM: for tar / sar / star on the DMMA path with S in {2, 4, 8}, local
+// write-back.  STARMM_DMMA_CLUSTER=0 keeps the global-memory protocols (A/B evidence).
+bool dmma_cluster_mode(const starmm_plan* P, int S) {
+    if (S < 2 || S > 8 || P->remote_parts > 0) return false;
+    if (!(P->algo == STARMM_TAR || P->algo == STARMM_SAR || P->algo == STARMM_STAR)) return false;
+    const char* e = getenv("STARMM_DMMA_CLUSTER");
+    return !(e && e[0] == '0');
+}
+
+template <int CS>
+cudaError_t dmma_cluster_config(cudaLaunchConfig_t& lc, cudaLaunchAttribute* at, int* slots) {
+    using K = DmmaProd;
+    static bool attr_done[starmm_host::MAX_DEVICES] = {};
+    static int cached[starmm_host::MAX_DEVICES] = {};
+    const int dev = current_device();
+    auto kern = dmma_fp64_cluster_kernel<K, CS>;
+    if (!attr_done[dev]) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, K::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        int sms = 0;
+        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+        cudaLaunchConfig_t q = {};
+        q.gridDim = dim3((unsigned)(sms / CS * CS)); q.blockDim = dim3(K::THREADS);
+        q.dynamicSmemBytes = K::SMEM_BYTES;
+        cudaLaunchAttribute qa[1];
+        qa[0].id = cudaLaunchAttributeClusterDimension;
+        qa[0].val.clusterDim.x = CS; qa[0].val.clusterDim.y = 1; qa[0].val.clusterDim.z = 1;
+        q.attrs = qa; q.numAttrs = 1;
+        int c = 0;
+        if (cudaOccupancyMaxActiveClusters(&c, kern, &q) != cudaSuccess || c < 1) {
+            cudaGetLastError();
+            c = std::max(1, sms / CS);
+        }
+        cached[dev] = c;
+        attr_done[dev] = true;
+    }
+    *slots = cached[dev];
+    lc.blockDim = dim3(K::THREADS);
+    lc.dynamicSmemBytes = K::SMEM_BYTES;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+    lc.attrs = at; lc.numAttrs = 1;
+    return cudaSuccess;
+}
+
+// co-resident clusters of size S (the cluster mode's persistent slots)
+int dmma_cluster_slots(int S) {
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    int slots = 0;
+    cudaError_t e = cudaSuccess;
+    switch (S) {
+    case 2: e = dmma_cluster_config<2>(lc, at, &slots); break;
+    case 4: e = dmma_cluster_config<4>(lc, at, &slots); break;
+    case 8: e = dmma_cluster_config<8>(lc, at, &slots); break;
+    default: return 0;
+    }
+    if (e != cudaSuccess) { cudaGetLastError(); return 0; }
+    return slots;
+}
+
+template <int CS>
+int launch_dmma_cluster_cs(const DmmaParams& p, long long tiles, cudaStream_t s) {
+    cudaLaunchConfig_t lc = {};
+    cudaLaunchAttribute at[1];
+    int slots = 0;
+    CK(dmma_cluster_config<CS>(lc, at, &slots));
+    const long long clusters = std::max<long long>(1, std::min<long long>(slots, tiles));
+    lc.gridDim = dim3((unsigned)(clusters * CS));
+    lc.stream = s;
+    CK(cudaLaunchKernelEx(&lc, dmma_fp64_cluster_kernel<DmmaProd, CS>, p));
+    return STARMM_OK;
+}
+
+int launch_dmma_cluster(const DmmaParams& p, int S, long long tiles, cudaStream_t s) {
+    switch (S) {
+    case 2: return launch_dmma_cluster_cs<2>(p, tiles, s);
+    case 4: return launch_dmma_cluster_cs<4>(p, tiles, s);
+    case 8: return launch_dmma_cluster_cs<8>(p, tiles, s);
+    }
+    return STARMM_INTERNAL_ERROR;
+}
 
 template <class Sr>
 int launch_madd(void* C, long long ldc, const void* D, long long ldd, long long rows, long long cols,
@@ -501,7 +587,7 @@ __global__ void select_path_kernel(const unsigned long long* d_range, int sr, in
 // ============================================================================
 int starmm_simt_launch(int path, const starmm::SimtParams& sp, int grid, int sms, cudaStream_t s) {
     switch (path) {
-    case PATH_SIMT_I64: case PATH_SIMT_I64_NARROW: case PATH_SIMT_I64_DP4A:
+    case PATH_SIMT_I64: case PATH_SIMT_I64_NARROW: case PATH_SIMT_I64_DP4A: case PATH_SIMT_I64_CROSS:
         return starmm_simt_launch_int(path, sp, grid, sms, s);
     case PATH_SIMT_F32_PAIR: case PATH_SIMT_I32_CARRIER: case PATH_SIMT_F64T_CARRIER:
         return starmm_simt_launch_pair(path, sp, grid, sms, s);
@@ -687,6 +773,8 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
         // slices per tile -- tropical n=1024, S=8: -27% vs co2 with a flat penalty)
         auto split_pen = [&](int sl) -> double {
             if (sl == 0) return 0.0;
+            // DMMA cluster mode: the S partials merge through DSMEM (~1.5 stages)
+            if (is_dmma && dmma_cluster_mode(P, 1 << sl)) return 1.5;
             const double sar = pen_sar * (double)(1 << sl) / 2.0;
             switch (P->algo) {
             case STARMM_TAR: return pen_tar;
@@ -711,7 +799,12 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
             const double rate1 = occ1_build ? 0.97 : 0.89;
             const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
             for (int sl = 0; sl <= smax; ++sl) {
-                const double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
+                double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
+                if (is_dmma && dmma_cluster_mode(P, 1 << sl)) {   // one tile per cluster at a time
+                    const int slots = dmma_cluster_slots(1 << sl);
+                    if (slots < 1) continue;
+                    waves = std::ceil((double)tiles / (double)slots);
+                }
                 const double ovh = 4.5 + split_pen(sl);
                 const double c = waves * (kst / (double)(1 << sl) + ovh) / rate;
                 if (best == 0 || c < 0.99 * best) { best = c; best_occ = occ; best_s = sl; }
@@ -721,10 +814,13 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
         // same share of the flattened (tile, k-stage) space, pieces of shared tiles merge
         // with the atomic-madd.  Only for tar/star (their split write-back IS the
         // atomic-madd) and exact, cheap atomics (int64 red.add, int32 red.min).
+        // On the DMMA path (fp64 red.add: order-dependent rounding, like every fp64 split)
+        // it is TAR/STAR's atomic-madd for the <= 2 shared pieces per CTA.
         const char* benv = getenv("STARMM_NO_BALANCED");
-        if (simt_path && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
-            (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32) &&
-            P->remote_parts == 0 && !(benv && benv[0] == '1')) {
+        const bool bal_sr = simt_path ? (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32)
+                                      : is_dmma;
+        if ((simt_path || is_dmma) && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
+            bal_sr && P->remote_parts == 0 && !(benv && benv[0] == '1')) {
             const double Gw = (double)P->sms * per_sm;
             const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw * per_sm;
             if (c < 0.97 * best) { balanced = true; best_occ = per_sm; best_s = 0; }
@@ -965,8 +1061,9 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         CK(cudaGetLastError());
         x.launches += 2;
     }
+    const bool cluster = G.is_dmma && dmma_cluster_mode(P, S);
     // ---- per-run protocol state: slots (TileExclusionTable), pair states ----
-    const bool need_slots = (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
+    const bool need_slots = !cluster && (S > 1) && (P->algo == STARMM_SAR || P->algo == STARMM_STAR);
     void* pstate = nullptr;
     const size_t state_bytes = need_slots ? (size_t)(tiles + tiles * (S / 2)) * 4 : 0;
     if (need_slots) {
@@ -992,7 +1089,7 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         }
         P->ws_high_water = std::max<long long>(P->ws_high_water, (long long)wbytes);
     }
-    if (init_identity && (S > 1 || G.balanced) && P->algo != STARMM_CO3 && P->remote_parts == 0) {
+    if (init_identity && (S > 1 || G.balanced) && P->algo != STARMM_CO3 && P->remote_parts == 0 && !cluster) {
         TRY(fill_dispatch(P->sr, C, P->m, P->n, ldc, s, pr));
         ++x.launches;
     }
@@ -1041,15 +1138,43 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         // it: 250 -> 51 GB).  STARMM_DMMA_GATE=1 turns it on; it needs the whole grid
         // co-resident and pays only over several waves, and the host path's
         // overlapping launches never use it.
-        const char* genv = getenv("STARMM_DMMA_GATE");
-        const bool gate = genv && genv[0] == '1' && P->dmma_gate && G.ntasks >= 4LL * grid;
-        TRY(launch_dmma(dp, grid, gate, s));
+        if (cluster) {
+            TRY(launch_dmma_cluster(dp, S, tiles, s));
+        } else if (G.balanced) {
+            static bool bal_attr[starmm_host::MAX_DEVICES] = {};
+            const int dev = current_device();
+            if (!bal_attr[dev]) {
+                CK(cudaFuncSetAttribute(dmma_fp64_balanced_kernel<DmmaProd>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, DmmaProd::SMEM_BYTES));
+                bal_attr[dev] = true;
+            }
+            dmma_fp64_balanced_kernel<DmmaProd><<<grid, DmmaProd::THREADS, DmmaProd::SMEM_BYTES, s>>>(dp);
+            CK(cudaGetLastError());
+        } else {
+            const char* genv = getenv("STARMM_DMMA_GATE");
+            const bool gate = genv && genv[0] == '1' && P->dmma_gate && G.ntasks >= 4LL * grid;
+            TRY(launch_dmma(dp, grid, gate, s));
+        }
     } else {
         SimtParams sp;
         sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = G.g; sp.w = w;
         sp.pr = pr;
         // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
         CK((cudaError_t)starmm_simt_launch(G.path, sp, grid, P->sms, s));
+        if (G.path == PATH_SIMT_I64) {
+            // second pass: the cross terms' 32-bit sum, (sum << 32) folded into C after the
+            // first pass's write-back (whatever its protocol) -- one exclusive fold per tile
+            // (or the peers' atomic-madd under the fused multi-GPU combine)
+            ++x.launches;
+            SimtParams sx = sp;
+            TaskGrid& gx = sx.g;
+            gx.S = 1; gx.log2S = 0; gx.tar_levels = 0; gx.balanced = 0;
+            gx.kslice = Kp; gx.num_tasks = (int)tiles;
+            sx.w.mode_base = STARMM_CO2;
+            sx.w.init_identity = 0;
+            sx.w.slots = nullptr; sx.w.pairs = nullptr; sx.w.W = nullptr; sx.w.scratch = nullptr;
+            CK((cudaError_t)starmm_simt_launch(PATH_SIMT_I64_CROSS, sx, occupancy_grid(P, 1, tiles), P->sms, s));
+        }
     }
     ++x.launches;
     if (ev && G.path != PATH_OZAKI_F64 && (rc = cuda_status(cudaEventRecord(ev[1], s)))) return rc;
@@ -1072,8 +1197,10 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         if (P->alloc == STARMM_RAW) CK(cudaFreeAsync(W, s));
     }
     ci.workers = std::min<long long>(G.ntasks, (long long)P->sms * G.per_sm);
+    if (cluster) ci.workers = std::min<long long>(tiles, dmma_cluster_slots(S)) * S;
+    ci.cluster = cluster ? S : 0;
     ci.balanced_workers = G.balanced ? std::min<long long>(G.ntasks * G.g.kstages, (long long)P->sms * G.per_sm) : 0;
-    if (S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && G.tar_levels < s_log2)
+    if (!cluster && S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && G.tar_levels < s_log2)
         ci.pair_count = tiles * (S / 2);
     return STARMM_OK;
 }
@@ -1278,6 +1405,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     P->st.executes += 1;
     P->st.pair_count += ci.pair_count;
     P->st.candidates = ncand;
+    P->st.cluster_size = ci.cluster;
     return STARMM_OK;
 }
 

@@ -426,3 +426,90 @@ def test_generated_config_panel_product_vs_oracle():
     O.gemm_fold(O.SR_FP64, want, A.cpu().numpy(), B.cpu().numpy(), par=True)
     got = C.cpu().numpy()
     assert np.all(np.abs(got - want) <= 1e-10 * np.sqrt(n) * np.maximum(1, np.abs(want)))
+
+
+# ---- DMMA split-k on thread-block clusters (DSMEM merge) ----------------------------
+@pytest.mark.parametrize("algo", ["tar", "sar", "star"])
+@pytest.mark.parametrize("ksplit", [1, 2, 3])
+def test_dmma_cluster_split_exact_and_deterministic(algo, ksplit):
+    """The S k-slices of each tile run on one cluster and merge through DSMEM in rank
+    order: within tolerance of the oracle, bit-identical from run to run (no atomics),
+    and no tile locks / pair states / lazy global scratch."""
+    n = 768                                           # ragged: 3 x 12 tiles of 256 x 64
+    rng = np.random.default_rng(ksplit)
+    A, B, C0 = rng.standard_normal((n, n)), rng.standard_normal((n, n)), rng.uniform(-1, 1, (n, n))
+    want = C0.copy()
+    O.gemm_fold(O.SR_FP64, want, A, B, par=True)
+    outs = []
+    for _ in range(2):
+        got, st = _run(algo, sm.FLOAT_RING, C0, A, B,
+                       sm.Config(base_dim=64, workers=148, ksplit=ksplit, allow_nonpow2=True))
+        assert st["cluster_size"] == 1 << ksplit and st["ksplit"] == 1 << ksplit
+        assert st["pair_count"] == 0 and st["tile_serializations"] == 3 * 12
+        assert st["lazy_temp_acquires"] == 3 * 12 * ((1 << ksplit) - 1)
+        assert np.all(np.abs(got - want) <= 1e-12 * n * np.maximum(1, np.abs(want)))
+        outs.append(got)
+    assert same_bits(outs[0], outs[1])
+
+
+def test_dmma_cluster_store_flag_and_protocol_fallback(monkeypatch):
+    """C <- A (x) B (init identity) through the cluster merge, and the same split with
+    the global-memory protocols (STARMM_DMMA_CLUSTER=0) agree within rounding."""
+    n = 512
+    rng = np.random.default_rng(9)
+    A, B = rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    s = sm.FLOAT_RING
+    At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    p = _lib.Plan(_lib.SR_FP64, "sar", "pooled", n, n, n, 64, 148, 2, 0, _lib.F_INIT_IDENTITY)
+    C = torch.full((n, n), 7.0, dtype=torch.float64, device="cuda")
+    st = _exec(p, C, At, Bt)
+    p.close()
+    assert st["cluster_size"] == 4
+    want = A @ B
+    assert np.allclose(C.cpu().numpy(), want, rtol=1e-12, atol=1e-10)
+    monkeypatch.setenv("STARMM_DMMA_CLUSTER", "0")
+    got, st = _run("sar", s, np.zeros((n, n)), A, B, sm.Config(base_dim=64, workers=148, ksplit=2))
+    assert st["cluster_size"] == 0 and st["pair_count"] > 0
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-10)
+
+
+# ---- general int64 in two passes (low products, then cross terms) ---------------------
+@pytest.mark.parametrize("algo", ["co2", "co3", "tar", "sar", "star"])
+@pytest.mark.parametrize("ksplit", [0, 1, 2])
+def test_general_int64_two_pass_wraps_bitexact(algo, ksplit):
+    """Full-range int64 (wraps mod 2^64) through the general kernel's two passes under
+    every write-back protocol, bit-exact against the oracle."""
+    n = 384
+    rng = np.random.default_rng(40 + ksplit)
+    A = rng.integers(-2 ** 62, 2 ** 62, (n, n), dtype=np.int64)
+    B = rng.integers(-2 ** 62, 2 ** 62, (n, n), dtype=np.int64)
+    C0 = rng.integers(-2 ** 62, 2 ** 62, (n, n), dtype=np.int64)
+    want = C0.copy()
+    O.gemm_fold(O.SR_INT64, want, A, B, par=True)
+    got, st = _run(algo, sm.INT_RING, C0, A, B,
+                   sm.Config(base_dim=32, workers=148, ksplit=ksplit, allow_nonpow2=True))
+    assert st["path_name"] == "simt_i64"
+    assert same_bits(got, want)
+
+
+@pytest.mark.parametrize("algo", ["tar", "star"])
+@pytest.mark.parametrize("store", [False, True])
+def test_dmma_balanced_slices(algo, store):
+    """n = 2048 fp64 (256 tiles on 148 SMs): tar / star run balanced k-slices on the
+    DMMA path (whole tiles folded exclusively, shared pieces by red.add.f64)."""
+    n = 2048
+    rng = np.random.default_rng(5)
+    A, B = rng.standard_normal((n, n)), rng.standard_normal((n, n))
+    C0 = rng.uniform(-1, 1, (n, n))
+    flags = _lib.F_INIT_IDENTITY if store else 0
+    p = _plan(_lib.SR_FP64, n, flags=flags, algo=algo)
+    try:
+        C = torch.from_numpy(C0.copy()).cuda()
+        st = _exec(p, C, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    finally:
+        p.close()
+    assert st["balanced_workers"] > 0 and st["path_name"] == "dmma_f64"
+    want = np.zeros((n, n)) if store else C0.copy()
+    O.gemm_fold(O.SR_FP64, want, A, B, par=True)
+    got = C.cpu().numpy()
+    assert np.all(np.abs(got - want) <= 1e-10 * np.sqrt(n) * np.maximum(1, np.abs(want)))
