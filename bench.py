@@ -279,7 +279,7 @@ def cpu_baseline(cid, n, device, port_seconds):
     v, desc, cores, secs = cpu_sample(cid, Ah, Bh, port_seconds)
     port = {"value": v / 1e12, "unit": "Tops/s", "cores": cores, "kind": "port",
             "sample": desc + f" ({secs:.1f} s), oracle/starmm_oracle.c"}
-    ref = reference_star_sample(cid, target_s=3.0)
+    ref = reference_star_sample(cid, target_s=8.0)
     sweep = None
     sp = os.path.join(REPO, "profiles", "r02_ref_cpu_sweep.json")
     if os.path.exists(sp):
@@ -356,7 +356,7 @@ def main():
                          "(min,+) without the range-guarded narrow encodings (DESIGN.md §7)")
     ap.add_argument("--parity-tiles", type=int, default=8,
                     help="sampled output tiles each rank checks against the oracle after timing")
-    ap.add_argument("--ref-step-seconds", type=float, default=3.0,
+    ap.add_argument("--ref-step-seconds", type=float, default=8.0,
                     help="--impl reference: target seconds per star_mm step (sets its n)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo: plumbing check with several ranks on fewer GPUs (timings invalid)")

@@ -2,7 +2,9 @@
 # ncu evidence for the bench workloads (run under gpurun; one GPU).
 # Each profiled command first runs plain and must exit 0 (B200_PROFILING.md).
 # usage: bash tools/ncu_capture.sh <tag> [configs...]
-#   configs: 2 3 4 5 (default paths), 2t (config 2 --int-tensor), 4e (config 4 --fp64-emu)
+#   configs: 2 3 4 5 (default paths), 2t (config 2 --int-tensor), 4e (config 4 --fp64-emu),
+#            5f (config 5 at its full n = 49152), 2g / 3g / 5g (the general kernels,
+#            --no-fastpath; 5g at n = 16384)
 #   launch list : the bench command itself (e2e + cpu baseline legs included)
 #   full capture: the tile kernel, from the same command without the e2e / cpu legs
 set -x
@@ -12,7 +14,8 @@ for c in $CFGS; do
   base=${c:0:1}; X=""; F=""
   [ "$base" = "5" ] && X="--size 16384"
   K=simt_mm; [ "$base" = "4" ] && K=dmma
-  case $c in 2t) F="--int-tensor"; K=tcg_kernel;; 4e) F="--fp64-emu"; K=tcg_kernel;; esac
+  case $c in 2t) F="--int-tensor"; K=tcg_kernel;; 4e) F="--fp64-emu"; K=tcg_kernel;;
+             5f) X="";; 2g|3g|5g) F="--no-fastpath";; esac
   B="python bench.py --steps 2 --warmup 1 --config $base $X $F --no-opt-in"
   $B > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \

@@ -59,6 +59,7 @@ def main():
     ap.add_argument("--cap", type=float, default=600.0)
     ap.add_argument("--semirings", default="float,int,tropical")
     ap.add_argument("--workers", default="")
+    ap.add_argument("--out", default="r02_ref_cpu_sweep.json")
     args = ap.parse_args()
     cores = os.cpu_count() or 1
     Ws = [int(x) for x in args.workers.split(",")] if args.workers else sorted({1, cores})
@@ -67,6 +68,7 @@ def main():
                   "b = 32 up to n = 512, else 64; inputs = the BASELINE config distributions "
                   "(bench_configs.make_inputs: float -> config 4, int -> config 2, tropical -> "
                   "config 5's weights up-cast to float64)"}
+    path = os.path.join(REPO, "profiles", args.out)
     for sid in args.semirings.split(","):
         run_one(sid, 64, 1, 32, args.cap)                       # numba JIT into the cache
         for W in Ws:
@@ -86,8 +88,7 @@ def main():
             done = [r for r in rows if r["status"] == "ok" and r["seconds"] <= args.cap]
             out["series"].append({"semiring": sid, "workers": W, "runs": rows})
             out["largest_n"][f"{sid}:W{W}"] = max((r["n"] for r in done), default=None)
-    path = os.path.join(REPO, "profiles", "r02_ref_cpu_sweep.json")
-    json.dump(out, open(path, "w"), indent=1)
+            json.dump(out, open(path, "w"), indent=1)        # after every series
     print(json.dumps(out["largest_n"]))
 
 
