@@ -87,7 +87,7 @@ def main():
     cfgs = sys.argv[2:] or ["4", "2", "3", "5"]
     md = [f"# ncu summary `{tag}` (B200, `--clock-control none`)\n",
           "Launch lists: `ncu --metrics gpu__time_duration.sum` over `python bench.py --steps 2 "
-          "--warmup 1 --no-e2e --no-cpu-baseline --no-opt-in --config C` (config 5 at `--size 16384`; "
+          "--warmup 1 --no-opt-in --config C` (config 5 at `--size 16384`, `5f` at its full n = 49152; "
           "`2t` = config 2 `--int-tensor`, `4e` = config 4 `--fp64-emu`); times are "
           "cold-cache and serialised, so compare SHARES. Full captures: `ncu --set full -k "
           "regex:<tile kernel> -s 1 -c 1` of the same command (tools/ncu_capture.sh).\n"]
@@ -110,9 +110,9 @@ def main():
         md.append("\nTop warp stall reasons (warps per issue): " +
                   ", ".join(f"{n} {v:.2f}" for v, n in stalls[:6]))
         try:
-            rb = float(d["dram__bytes_read.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1,
+            rb = float(d["dram__bytes_read.sum"][0]) * {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "byte": 1,
                                                         "Kbyte": 1e3}[d["dram__bytes_read.sum"][1]]
-            wb = float(d["dram__bytes_write.sum"][0]) * {"Gbyte": 1e9, "Mbyte": 1e6, "byte": 1,
+            wb = float(d["dram__bytes_write.sum"][0]) * {"Tbyte": 1e12, "Gbyte": 1e9, "Mbyte": 1e6, "byte": 1,
                                                          "Kbyte": 1e3}[d["dram__bytes_write.sum"][1]]
             n = plain["config"]["n"]
             key = f"{c[0]}:{path}"
