@@ -130,6 +130,7 @@ typedef struct {
     int64_t candidates;              /* paths queued behind the device-side verdict (1: none) */
     int64_t cluster_size;            /* > 0: the k-slices of a tile ran on one thread-block
                                         cluster and merged through DSMEM (DMMA path)      */
+    int64_t k_chunks;                /* k-outer launches of the tile kernel (L2-sized panels) */
 } starmm_stats;
 
 /* The device's block pool (pool.py:67-167): one per device, shared by every plan and

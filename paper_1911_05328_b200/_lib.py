@@ -41,7 +41,7 @@ class StarmmStats(ctypes.Structure):
         "lazy_temp_acquires", "raw_alloc_count", "raw_alloc_bytes", "tasks", "workers",
         "ksplit", "tar_levels", "kernel_launches", "path", "executes", "main_kernel_ns",
         "main_kernel_launches", "balanced_workers", "live_leaves_max", "guard_syncs",
-        "candidates", "cluster_size")]
+        "candidates", "cluster_size", "k_chunks")]
 
     def to_dict(self):
         return {name: int(getattr(self, name)) for name, _ in self._fields_}

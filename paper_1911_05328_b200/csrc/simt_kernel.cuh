@@ -117,37 +117,6 @@ struct PolI64 {
         c += (unsigned long long)a * (unsigned long long)b;
     }
 };
-// int64 (+,x) mod 2^64 in two passes over the same packed int64 operands:
-//   a*b mod 2^64 = lo(a)lo(b) + 2^32 (lo(a)hi(b) + hi(a)lo(b)) mod 2^64,
-// and only the LOW 32 bits of the cross terms' sum matter.  PolI64Lo accumulates the
-// 64-bit sum of the low products (one IMAD.WIDE.U32 with a 64-bit addend per term,
-// 2 registers per output), PolI64Cross the 32-bit cross sum (two IMADs per term, 1
-// register per output) whose epilogue folds (sum << 32) into C.  3 instructions per
-// term and no register spills, where PolI64 (the compiler's u64 multiply-add, 4-5
-// instructions and register shuffles per term) ran at 7 Tops/s.  Both folds are
-// additions mod 2^64, so the result is bit-exact in any order.
-struct PolI64Lo {
-    using Tp = long long; using Acc = unsigned long long;
-    static constexpr int G = 1;
-    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
-    static constexpr int OCC = 1;
-    static STARMM_DEV Acc init() { return 0ull; }
-    static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
-        c += (unsigned long long)(unsigned)a * (unsigned long long)(unsigned)b;
-    }
-};
-struct PolI64Cross {
-    using Tp = long long; using Acc = unsigned;
-    static constexpr int G = 1;
-    static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
-    static constexpr int OCC = 1;
-    static STARMM_DEV Acc init() { return 0u; }
-    static STARMM_DEV void term(Acc& c, Tp a, Tp b) {
-        const unsigned alo = (unsigned)a, ahi = (unsigned)((unsigned long long)a >> 32);
-        const unsigned blo = (unsigned)b, bhi = (unsigned)((unsigned long long)b >> 32);
-        c += alo * bhi + ahi * blo;
-    }
-};
 struct PolI64Narrow {
     using Tp = int; using Acc = int;
     static constexpr int G = 1;
@@ -205,12 +174,6 @@ template <> struct Finish<PolI32Sat, SrTropI32> {
 };
 template <> struct Finish<PolI64, SrInt64> {
     static STARMM_DEV long long out(unsigned long long v) { return (long long)v; }
-};
-template <> struct Finish<PolI64Lo, SrInt64> {
-    static STARMM_DEV long long out(unsigned long long v) { return (long long)v; }
-};
-template <> struct Finish<PolI64Cross, SrInt64> {
-    static STARMM_DEV long long out(unsigned v) { return (long long)((unsigned long long)v << 32); }
 };
 template <> struct Finish<PolI64Narrow, SrInt64> {
     static STARMM_DEV long long out(int v) { return (long long)v; }

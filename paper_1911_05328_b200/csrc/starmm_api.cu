@@ -135,6 +135,7 @@ struct CandInfo {
     long long raw_count = 0, raw_bytes = 0;
     int s_log2 = 0;
     int cluster = 0;         // > 0: DMMA split-k merged on a cluster of this many CTAs
+    int k_chunks = 1;        // k-outer chunks of a CUDA-core launch (simt_k_chunks)
 };
 
 }  // namespace
@@ -218,7 +219,7 @@ PathShape path_shape(int path) {
         PathShape sh{DmmaProd::BM, DmmaProd::BN, DmmaProd::BK, DmmaProd::MIN_BLOCKS, 8000, 8000};
         return sh;
     }
-    case PATH_SIMT_I64: return simt_shape<PolI64Lo>();
+    case PATH_SIMT_I64: return simt_shape<PolI64>();
     case PATH_SIMT_I64_NARROW: return simt_shape<PolI64Narrow>();
     case PATH_SIMT_F32_PAIR: return simt_shape<PolF32Pair>();
     case PATH_SIMT_I32_CARRIER: return simt_shape<PolF32Pair>();
@@ -587,7 +588,7 @@ __global__ void select_path_kernel(const unsigned long long* d_range, int sr, in
 // ============================================================================
 int starmm_simt_launch(int path, const starmm::SimtParams& sp, int grid, int sms, cudaStream_t s) {
     switch (path) {
-    case PATH_SIMT_I64: case PATH_SIMT_I64_NARROW: case PATH_SIMT_I64_DP4A: case PATH_SIMT_I64_CROSS:
+    case PATH_SIMT_I64: case PATH_SIMT_I64_NARROW: case PATH_SIMT_I64_DP4A:
         return starmm_simt_launch_int(path, sp, grid, sms, s);
     case PATH_SIMT_F32_PAIR: case PATH_SIMT_I32_CARRIER: case PATH_SIMT_F64T_CARRIER:
         return starmm_simt_launch_pair(path, sp, grid, sms, s);
@@ -860,6 +861,31 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
     if (G.ntasks > (1LL << 31) - 1) return STARMM_TOO_LARGE;
     g.num_tasks = (int)G.ntasks;
     return STARMM_OK;
+}
+
+// packed k-group geometry of the CUDA-core paths (simt_kernel.cuh policies)
+int simt_kstep(int path) {
+    return path == PATH_SIMT_I64_DP4A ? 4 : 1;
+}
+int simt_g(int path) {
+    return (path == PATH_SIMT_F32_PAIR || path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER) ? 2 : 1;
+}
+
+// k-outer chunk count of a CUDA-core launch: 1 unless the panels one wave of persistent
+// CTAs streams (group_m tile-rows of A, grid / group_m tile-columns of B, over all of k)
+// exceed twice the L2; then enough chunks to bring them to ~96 MB.  Only for unsplit,
+// unbalanced, local launches (every chunk is then a plain fold of whole tiles).
+int simt_k_chunks(const starmm_plan* P, const Geom& G) {
+    const char* e = getenv("STARMM_K_CHUNKS");
+    if (G.S != 1 || G.balanced || P->remote_parts > 0 || G.path == PATH_MIN_ORDERED) return 1;
+    if (e) return std::max(1, atoi(e));
+    const long long waves_cols = std::max<long long>(1, (long long)P->sms * G.per_sm / G.g.group_m);
+    const double bytes = ((double)std::min<long long>(G.g.group_m, G.tiles_m) * G.TBM * G.shape.a_bytes_per_km +
+                          (double)std::min<long long>(waves_cols, G.tiles_n) * G.TBN * G.shape.b_bytes_per_kn) /
+                         1000.0 * (double)G.Kp;
+    if (bytes <= 2.0 * 126e6) return 1;
+    const long long n = (long long)std::ceil(bytes / 96e6);
+    return (int)std::max<long long>(1, std::min<long long>(n, G.Kp / std::max(4096, G.BK)));
 }
 
 // DMMA reads A and B in place when the tiles divide the problem and rows are 16-byte
@@ -1159,22 +1185,35 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         SimtParams sp;
         sp.Ap = opA; sp.Bp = opB; sp.Mp = Mp; sp.Np = Np; sp.g = G.g; sp.w = w;
         sp.pr = pr;
-        // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
-        CK((cudaError_t)starmm_simt_launch(G.path, sp, grid, P->sms, s));
-        if (G.path == PATH_SIMT_I64) {
-            // second pass: the cross terms' 32-bit sum, (sum << 32) folded into C after the
-            // first pass's write-back (whatever its protocol) -- one exclusive fold per tile
-            // (or the peers' atomic-madd under the fused multi-GPU combine)
-            ++x.launches;
-            SimtParams sx = sp;
-            TaskGrid& gx = sx.g;
-            gx.S = 1; gx.log2S = 0; gx.tar_levels = 0; gx.balanced = 0;
-            gx.kslice = Kp; gx.num_tasks = (int)tiles;
-            sx.w.mode_base = STARMM_CO2;
-            sx.w.init_identity = 0;
-            sx.w.slots = nullptr; sx.w.pairs = nullptr; sx.w.W = nullptr; sx.w.scratch = nullptr;
-            CK((cudaError_t)starmm_simt_launch(PATH_SIMT_I64_CROSS, sx, occupancy_grid(P, 1, tiles), P->sms, s));
+        // k-outer chunks: when the A and B panels one wave of persistent CTAs streams
+        // exceed the L2 many times over, the CTAs drift apart in k and every wave re-reads
+        // its panels from DRAM (config 5, n = 49152: 3.96 TB per launch for 38.6 GB of
+        // operands, profiles/r02j_ncu_summary.md).  Running the k range as a few chunks,
+        // each one launch over all tiles that folds into C (CO2's serialised k-halves,
+        // classic.py:125-128, taken at the top level), keeps a wave's panels L2-sized for
+        // the price of one C read-modify-write per chunk.
+        const int nchunk = simt_k_chunks(P, G);
+        if (nchunk <= 1) {
+            // the CUDA-core tile kernels are instantiated in simt_launch_*.cu (parallel build)
+            CK((cudaError_t)starmm_simt_launch(G.path, sp, grid, P->sms, s));
+        } else {
+            const int KSTEP = simt_kstep(G.path), GG = simt_g(G.path), OUTS = G.shape.bn / 128;
+            const long long kc = round_up((Kp + nchunk - 1) / nchunk, G.BK);
+            const size_t ea = (size_t)G.shape.a_bytes_per_km * KSTEP / 1000 / GG;   // bytes per packed element
+            for (long long k0 = 0; k0 < Kp; k0 += kc) {
+                const long long kl = std::min(kc, Kp - k0);
+                SimtParams sc = sp;
+                sc.Ap = (const char*)opA + (size_t)(k0 / KSTEP) * (size_t)Mp * GG * ea;
+                sc.Bp = (const char*)opB + (size_t)(k0 / KSTEP) * (size_t)(Np / OUTS) * GG * ea;
+                sc.g.kslice = kl;
+                sc.g.kstages = kl / G.BK;
+                if (k0 > 0) sc.w.init_identity = 0;           // later chunks fold
+                CK((cudaError_t)starmm_simt_launch(G.path, sc, grid, P->sms, s));
+                if (k0 > 0) ++x.launches;
+            }
+            ci.k_chunks = nchunk;
         }
+
     }
     ++x.launches;
     if (ev && G.path != PATH_OZAKI_F64 && (rc = cuda_status(cudaEventRecord(ev[1], s)))) return rc;
@@ -1406,6 +1445,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     P->st.pair_count += ci.pair_count;
     P->st.candidates = ncand;
     P->st.cluster_size = ci.cluster;
+    P->st.k_chunks = ci.k_chunks;
     return STARMM_OK;
 }
 

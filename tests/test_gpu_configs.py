@@ -145,6 +145,7 @@ def test_config5_tropical_i32_n49152():
     A, B, C0, C, Am, Bm, st = _run(5)
     assert A is B
     assert st["path_name"] == "simt_i32_via_f32_carrier"
+    assert st["k_chunks"] > 1              # k-outer chunks keep a wave's panels L2-sized
     _check_tiles(5, A, B, C0, C.data, count=64)
     # idempotence on the full 49152^2 output
     first = C.data.clone()

@@ -513,3 +513,30 @@ def test_dmma_balanced_slices(algo, store):
     O.gemm_fold(O.SR_FP64, want, A, B, par=True)
     got = C.cpu().numpy()
     assert np.all(np.abs(got - want) <= 1e-10 * np.sqrt(n) * np.maximum(1, np.abs(want)))
+
+
+# ---- k-outer chunked launches (L2-sized panels) --------------------------------------
+@pytest.mark.parametrize("sid,lo,hi", [("int", -100, 100), ("int", -9, 10), ("tropical_i32", 0, 100000),
+                                       ("tropical_f32", 0, 1000), ("tropical", 0, 50)])
+@pytest.mark.parametrize("store", [False, True])
+def test_k_chunked_launches_bitexact(sid, lo, hi, store, monkeypatch):
+    """STARMM_K_CHUNKS forces the k-outer chunking (auto only for panels > 2x L2, e.g.
+    config 5): every chunk folds whole tiles into C, bit-exact against the oracle."""
+    monkeypatch.setenv("STARMM_K_CHUNKS", "3")
+    n = 640
+    s = sm.get_semiring(sid)
+    rng = np.random.default_rng(hi)
+    A = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    B = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    C0 = rng.integers(lo, hi, (n, n)).astype(s.dtype)
+    want = np.full((n, n), s.zero, dtype=s.dtype) if store else C0.copy()
+    O.gemm_fold(O.SR_BY_NAME[sid], want, A, B, par=True)
+    flags = _lib.F_ALLOW_NONPOW2 | (_lib.F_INIT_IDENTITY if store else 0)
+    p = _lib.Plan(s.sr_id, "co2", "pooled", n, n, n, 64, 148, -1, 0, flags)
+    try:
+        C = torch.from_numpy(C0.copy()).cuda()
+        st = _exec(p, C, torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda())
+    finally:
+        p.close()
+    assert st["k_chunks"] == 3, st
+    assert same_bits(C.cpu().numpy(), want)
