@@ -426,7 +426,10 @@ def _stats(algo, ksplit, workers=4, n=512, mode="pooled"):
         return ex.last_stats, ex.metrics.snapshot(ex.pool), ex.pool.snapshot_counts()
 
 
-def test_tar_scratch_high_water_bounded_by_workers():
+def test_tar_scratch_high_water_bounded_by_workers(monkeypatch):
+    # the global-memory protocols (the DMMA cluster merge has its own tests in
+    # test_gpu_round2.py)
+    monkeypatch.setenv("STARMM_DMMA_CLUSTER", "0")
     st, snap, pool = _stats("tar", ksplit=2)
     tile_bytes = 128 * 128 * 8
     assert st["tar_levels"] == 2
@@ -439,7 +442,8 @@ def test_sar_serial_buys_no_temporaries():
     assert st["lazy_temp_acquires"] == 0 and st["ksplit"] == 1
 
 
-def test_sar_pairs_transition_and_lazy_temps():
+def test_sar_pairs_transition_and_lazy_temps(monkeypatch):
+    monkeypatch.setenv("STARMM_DMMA_CLUSTER", "0")
     st, snap, _ = _stats("sar", ksplit=1)
     pairs = st["pair_count"]
     tiles = st["tasks"] // st["ksplit"]
