@@ -30,7 +30,8 @@ PATH_NAMES = {1: "dmma_f64", 2: "simt_i64", 3: "simt_i64_narrow_i32", 4: "simt_f
               8: "simt_f64_min", 9: "simt_i64_dp4a", 10: "simt_f32_s16x2_viaddmnmx",
               11: "simt_i32_s16x2_viaddmnmx", 12: "simt_f64trop_s16x2_viaddmnmx",
               13: "simt_f64trop_via_f32_carrier", 14: "tcgen05_i8_umma",
-              15: "ozaki2_fp64_tcgen05_i8x16", 16: "minplus_ordered_leaf_order"}
+              15: "ozaki2_fp64_tcgen05_i8x16", 16: "minplus_ordered_leaf_order",
+              17: "tcgen05_i8_radix256_int64"}
 ABI_VERSION = 3
 
 

@@ -26,12 +26,15 @@ STARMM_HD int guard_narrowest(int sr, int flags, long long k, unsigned long long
     case STARMM_SR_FP64:             // Ozaki-II needs finite inputs (its own guard word)
         return bits ? PATH_DMMA_F64 : PATH_OZAKI_F64;
     case STARMM_SR_INT64: {
-        if (!fast) return PATH_SIMT_I64;
+        // opt-in tensor cores: small ranges as one int8 GEMM, anything else as radix-256
+        // digit GEMMs (exact for every int64); CUDA cores otherwise
+        const bool tc = (flags & STARMM_F_INT_TENSOR) != 0;
+        if (!fast) return tc ? PATH_TC_I8_LIMBS : PATH_SIMT_I64;
         // exact iff every int32 partial sum fits: K * max|a| * max|b| < 2^31 (the double
         // product is exact below 2^53, so the comparison is exact where it matters)
         const double bound = (double)k * (double)mx * (double)mx;
-        if (mx <= 127 && bound < 2147483648.0)
-            return (flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8 : PATH_SIMT_I64_DP4A;
+        if (mx <= 127 && bound < 2147483648.0) return tc ? PATH_TC_I8 : PATH_SIMT_I64_DP4A;
+        if (tc) return PATH_TC_I8_LIMBS;
         if (mx < (1ull << 31) && bound < 2147483648.0) return PATH_SIMT_I64_NARROW;
         return PATH_SIMT_I64;
     }
@@ -62,7 +65,7 @@ STARMM_HD int path_rank(int path) {
     case PATH_SIMT_F64T_S16X2: case PATH_OZAKI_F64: return 0;
     case PATH_SIMT_I64_NARROW: case PATH_SIMT_F64T_CARRIER: case PATH_SIMT_F32_PAIR:
     case PATH_SIMT_I32_CARRIER: case PATH_DMMA_F64: return 1;
-    case PATH_SIMT_I64: case PATH_SIMT_F64_MIN: case PATH_SIMT_I32_VMIN: return 2;
+    case PATH_SIMT_I64: case PATH_SIMT_F64_MIN: case PATH_SIMT_I32_VMIN: case PATH_TC_I8_LIMBS: return 2;
     case PATH_SIMT_I32_SAT: return 3;
     case PATH_MIN_ORDERED: return 9;
     }

@@ -12,7 +12,8 @@ enum PathId : int {
     PATH_SIMT_I32_CARRIER = 5, PATH_SIMT_I32_VMIN = 6, PATH_SIMT_I32_SAT = 7, PATH_SIMT_F64_MIN = 8,
     PATH_SIMT_I64_DP4A = 9, PATH_SIMT_F32_S16X2 = 10, PATH_SIMT_I32_S16X2 = 11,
     PATH_SIMT_F64T_S16X2 = 12, PATH_SIMT_F64T_CARRIER = 13, PATH_TC_I8 = 14, PATH_OZAKI_F64 = 15,
-    PATH_MIN_ORDERED = 16   // float (min,+) in the reference's leaf order (ordered_kernel.cuh)
+    PATH_MIN_ORDERED = 16,  // float (min,+) in the reference's leaf order (ordered_kernel.cuh)
+    PATH_TC_I8_LIMBS = 17   // opt-in: any int64 as signed radix-256 digits on tcgen05 kind::i8
 };
 
 // Launch the persistent CUDA-core tile kernel of `path` (grid CTAs; grid <= sms selects the

@@ -239,6 +239,10 @@ PathShape path_shape(int path) {
         PathShape sh{2 * tcg::BM, tcg::BN, tcg::BK, 1, 1000LL * oz::P, 1000LL * oz::P};
         return sh;
     }
+    case PATH_TC_I8_LIMBS: { // 8 radix-256 digit planes of int8 per operand
+        PathShape sh{2 * tcg::BM, tcg::BN, tcg::BK, 1, 8000, 8000};
+        return sh;
+    }
     case PATH_MIN_ORDERED: {  // reads A and B in place
         PathShape sh{ordered::TM, ordered::TN, ordered::TK, 1, 0, 0};
         return sh;
@@ -420,7 +424,9 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                   CUtensorMapFloatOOBfill);
-int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int box_rows) {
+// row_stride: bytes between rows (0: kp, rows densely packed)
+int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int box_rows,
+                 long long row_stride = 0) {
     static EncodeTiledFn fn = nullptr;
     if (!fn) {
         cudaDriverEntryPointQueryResult q;
@@ -428,7 +434,7 @@ int make_i8_tmap(CUtensorMap* map, void* base, long long rows, long long kp, int
         if (!fn || q != cudaDriverEntryPointSuccess) return STARMM_INTERNAL_ERROR;
     }
     cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kp};
+    cuuint64_t strides[1] = {(cuuint64_t)(row_stride > 0 ? row_stride : kp)};
     cuuint32_t box[2] = {(cuuint32_t)tcg::BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, base, dims, strides, box, estr,
@@ -471,11 +477,12 @@ int tcg_max_clusters(int sms) {
 // drift-gate counters: one per (pass, tile round), zeroed before the launch.
 template <class Epi, class Acquire>
 int launch_tcg(const void* Ap, const void* Bp, long long Mp, long long Np, long long Kp, int passes,
-               const Epi& epi, int sms, cudaStream_t s, Acquire&& acquire, Pred pr) {
+               const Epi& epi, int sms, cudaStream_t s, Acquire&& acquire, Pred pr,
+               long long row_stride = 0) {
     if ((long long)passes * Mp >= (1LL << 31) || (long long)passes * Np >= (1LL << 31)) return STARMM_TOO_LARGE;
     CUtensorMap ta, tb;
-    TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp * passes, Kp, tcg::BM));
-    TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np * passes, Kp, tcg::BNH));
+    TRY(make_i8_tmap(&ta, const_cast<void*>(Ap), Mp * passes, Kp, tcg::BM, row_stride));
+    TRY(make_i8_tmap(&tb, const_cast<void*>(Bp), Np * passes, Kp, tcg::BNH, row_stride));
     auto kern = tcg_kernel<Epi>;
     const int clusters = tcg_max_clusters<Epi>(sms);
     TcgShape sh;
@@ -749,8 +756,9 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
     const bool is_dmma = G.is_dmma;
     const int BK = G.BK;
     const long long tiles = G.tiles;
-    const bool simt_path = !is_dmma && path != PATH_TC_I8 && path != PATH_OZAKI_F64;
-    const bool may_split = !(P->algo == STARMM_CO2 || path == PATH_TC_I8 || path == PATH_OZAKI_F64);
+    const bool tc_path = path == PATH_TC_I8 || path == PATH_OZAKI_F64 || path == PATH_TC_I8_LIMBS;
+    const bool simt_path = !is_dmma && !tc_path;
+    const bool may_split = !(P->algo == STARMM_CO2 || tc_path);
     int per_sm = G.per_sm, s_log2 = 0;
     bool balanced = false;
     if ((simt_path || is_dmma) && (P->ksplit_req < 0 || !may_split)) {
@@ -896,6 +904,14 @@ bool dmma_direct(const starmm_plan* P, const Geom& G, const void* A, long long l
            (((uintptr_t)A | (uintptr_t)B) % 16 == 0) && (lda % 2 == 0) && (ldb % 2 == 0);
 }
 
+// K chunking of the radix-256 digit path: chunks of <= 8192 k (every digit group's int32
+// sum (s + 1) K 2^14 stays <= 2^30), multiples of the tcgen05 core's k-stage (tcg::BK)
+void limb_chunks(long long Kp, long long* kc, int* nch) {
+    const long long n = (Kp + 8191) / 8192;
+    *kc = round_up((Kp + n - 1) / n, tcg::BK);
+    *nch = (int)((Kp + *kc - 1) / *kc);
+}
+
 // staging bytes of the packed operands of a path (0: read in place)
 void packed_bytes(const starmm_plan* P, const Geom& G, const void* A, long long lda, const void* B,
                   long long ldb, size_t* ab, size_t* bb) {
@@ -905,6 +921,13 @@ void packed_bytes(const starmm_plan* P, const Geom& G, const void* A, long long 
         if (dmma_direct(P, G, A, lda, B, ldb)) return;
         *ab = (size_t)(G.Mp * G.Kp * 8);
         *bb = (size_t)(G.Kp * G.Np * 8);
+        return;
+    }
+    if (G.path == PATH_TC_I8_LIMBS) {
+        long long kc; int nch;
+        limb_chunks(G.Kp, &kc, &nch);
+        *ab = (size_t)G.Mp * 8 * (size_t)(kc * nch);
+        *bb = (size_t)G.Np * 8 * (size_t)(kc * nch);
         return;
     }
     *ab = (size_t)(G.Mp * G.Kp * G.shape.a_bytes_per_km / 1000);
@@ -985,6 +1008,16 @@ int pack_operands(Exec& x, const Geom& G, const void* A, long long lda, const vo
             (const long long*)B, P->k, P->n, ldb, (int*)pb, Np, Kp, rng);
         rc = cuda_status(cudaGetLastError());
         break;
+    case PATH_TC_I8_LIMBS: {
+        long long kc; int nch;
+        limb_chunks(Kp, &kc, &nch);
+        pack_limbs_rows_kernel<<<dim3((unsigned)((kc * nch / 8 + 255) / 256), (unsigned)std::min<long long>(Mp, 4096)), 256, 0, s>>>(
+            (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, kc, nch, rng, pr);
+        pack_limbs_cols_kernel<<<dim3((unsigned)(Np / 32), (unsigned)((kc * nch + 31) / 32)), dim3(32, 8), 0, s>>>(
+            (const long long*)B, P->k, P->n, ldb, (signed char*)pb, Np, kc, nch, rng, pr);
+        rc = cuda_status(cudaGetLastError());
+        break;
+    }
     case PATH_TC_I8:
         pack_i8_rows_kernel<<<dim3((unsigned)((Kp / 8 + 255) / 256), (unsigned)std::min<long long>(Mp, 4096)), 256, 0, s>>>(
             (const long long*)A, P->m, P->k, lda, (signed char*)pa, Mp, Kp, rng);
@@ -1138,6 +1171,22 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
         e.o = tcg_out(P, C, ldc, init_identity);
         TRY(launch_tcg(opA, opB, Mp, Np, Kp, 1, e, P->sms, s,
                        [&](size_t b, void** p) { return x.acquire(b, p); }, pr));
+    } else if (G.path == PATH_TC_I8_LIMBS) {
+        // per K chunk, the 8 digit groups: group s = one int8 GEMM over (s + 1) Kc of A's
+        // digits 0..s against B's digits s..0, its int32 result folded as << 8s (mod 2^64)
+        long long kc; int nch;
+        limb_chunks(Kp, &kc, &nch);
+        for (int ch = 0; ch < nch; ++ch)
+            for (int sg = 0; sg < 8; ++sg) {
+                EpiFoldI64 e;
+                e.o = tcg_out(P, C, ldc, init_identity && ch == 0 && sg == 0);
+                e.shift = 8 * sg;
+                const signed char* a = (const signed char*)opA + (size_t)ch * Mp * 8 * kc;
+                const signed char* b = (const signed char*)opB + (size_t)ch * Np * 8 * kc + (size_t)(7 - sg) * kc;
+                TRY(launch_tcg(a, b, Mp, Np, (sg + 1) * kc, 1, e, P->sms, s,
+                               [&](size_t bb, void** p) { return x.acquire(bb, p); }, pr, 8 * kc));
+                if (ch || sg) ++x.launches;
+            }
     } else if (G.path == PATH_OZAKI_F64) {
         void* planes = nullptr;
         TRY(x.acquire((size_t)oz::P * Mp * Np, &planes));
@@ -1248,7 +1297,7 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
 int general_path(const starmm_plan* P) {
     switch (P->sr) {
     case STARMM_SR_FP64: return PATH_DMMA_F64;
-    case STARMM_SR_INT64: return PATH_SIMT_I64;
+    case STARMM_SR_INT64: return (P->flags & STARMM_F_INT_TENSOR) ? PATH_TC_I8_LIMBS : PATH_SIMT_I64;
     case STARMM_SR_TROPICAL_F64: return PATH_SIMT_F64_MIN;
     case STARMM_SR_TROPICAL_F32: return PATH_SIMT_F32_PAIR;
     default: return PATH_SIMT_I32_SAT;

@@ -359,6 +359,7 @@ STARMM_DEV void tcg_fold(const TcgOut& o, long long row, long long col, typename
 // loads of a chunk are issued as one batch (16 rows in flight) before any store.
 struct EpiFoldI64 {
     TcgOut o;
+    int shift = 0;   // the accumulator's weight 2^shift (radix-256 digit groups); 0 otherwise
     STARMM_DEV void operator()(const TcgChunk& c, const uint32_t (&v)[32]) const {
         tcg_stage_rows(c, v);
         const long long col = c.col0 + c.lane;
@@ -366,7 +367,8 @@ struct EpiFoldI64 {
             for (int r = 0; r < 32; ++r) {
                 const long long row = c.row0 + r;
                 if (row < o.M && col < o.N)
-                    tcg_fold<SrInt64>(o, row, col, (long long)(int)c.stage[r * tcg::EPI_PITCH + c.lane]);
+                    tcg_fold<SrInt64>(o, row, col, (long long)((unsigned long long)(long long)(int)
+                                                               c.stage[r * tcg::EPI_PITCH + c.lane] << shift));
             }
         } else {
             long long* Cp = (long long*)o.C;
@@ -383,7 +385,7 @@ struct EpiFoldI64 {
                     const long long row = c.row0 + h + r;
                     if (row < o.M && col < o.N)
                         Cp[row * o.ldc + col] = (long long)((unsigned long long)cv[r] +
-                            (unsigned long long)(long long)(int)c.stage[(h + r) * tcg::EPI_PITCH + c.lane]);
+                            ((unsigned long long)(long long)(int)c.stage[(h + r) * tcg::EPI_PITCH + c.lane] << shift));
                 }
             }
         }
@@ -459,6 +461,90 @@ pack_i8_transpose_kernel(const long long* B, long long kdim, long long cols, lon
         const int col = ty + 8 * j;
         const long long cc = c0 + col, kk = k0 + 4 * tx;
         if (cc < colsp && kk < kp) *reinterpret_cast<uint32_t*>(P + cc * kp + kk) = tile[col][tx];
+    }
+}
+
+
+// ---- opt-in general int64 on the int8 tensor cores: signed radix-256 digits ------------
+// x = sum_i d_i 256^i (mod 2^64) with d_i in [-128, 127] (balanced digits, the carry out
+// of the top digit dropped).  a*b mod 2^64 = sum_s 2^(8s) sum_{q<=s} d_q(a) d_{s-q}(b), so
+// digit group s (s = 0..7) is ONE int8 GEMM over a (s+1)-times longer k: A's digits
+// 0..s of each k against B's digits s..0.  Packed per K chunk (<= 8192, so every
+// group's int32 sum (s+1) K 2^14 <= 2^30 is exact), limb-major within a row:
+//   A: P[chunk][row][limb 0..7][Kc]      B^T: P[chunk][col][limb 7..0][Kc]
+// so group s is a contiguous (s+1) Kc window of every row: columns [0, (s+1) Kc) of A,
+// [(7-s) Kc, 8 Kc) of B^T -- one 2-D TMA map each (row stride 8 Kc bytes).
+STARMM_DEV void i64_digits(long long x, signed char (&d)[8]) {
+    unsigned long long u = (unsigned long long)x;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+        int v = (int)(u & 0xffull);
+        u >>= 8;
+        if (v >= 128) { v -= 256; u += 1; }
+        d[i] = (signed char)v;
+    }
+}
+
+// A (rows x kdim) -> digit planes; thread per (row, 8 consecutive k)
+// Both digit packers also run the range guard (RangeAcc): as a plan's first guess they
+// are what tells the next call whether the single-GEMM int8 path would do.
+__global__ void pack_limbs_rows_kernel(const long long* A, long long rows, long long kdim, long long lda,
+                                       signed char* P, long long rowsp, long long kc, int nchunk,
+                                       unsigned long long* range = nullptr, Pred pr = Pred()) {
+    if (pr.off()) return;
+    RangeAcc acc;
+    const long long kw = (long long)blockIdx.x * blockDim.x + threadIdx.x;   // 8-k word within the padded k
+    const long long kp_all = kc * nchunk;
+    const bool live = kw * 8 < kp_all;
+    for (long long r = blockIdx.y; live && r < rowsp; r += gridDim.y) {
+        signed char d[8][8];   // [k][limb]
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            const long long k = kw * 8 + e;
+            const long long x = (r < rows && k < kdim) ? A[r * lda + k] : 0;
+            acc.add(x);
+            i64_digits(x, d[e]);
+        }
+        const long long k0 = kw * 8, ch = k0 / kc, kk = k0 - ch * kc;
+        signed char* base = P + ((ch * rowsp + r) * 8) * kc + kk;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) {
+            unsigned long long w = 0;
+#pragma unroll
+            for (int e = 0; e < 8; ++e) w |= (unsigned long long)(unsigned char)d[e][l] << (8 * e);
+            *reinterpret_cast<unsigned long long*>(base + l * kc) = w;
+        }
+    }
+    if (range) acc.flush(range);   // every thread reaches the flush (full-warp shuffles)
+}
+
+// B (kdim x cols) -> B^T digit planes in reversed limb order; a 32-k x 32-col tile goes
+// through shared memory (reads coalesced along columns, writes along k)
+__global__ void pack_limbs_cols_kernel(const long long* B, long long kdim, long long cols, long long ldb,
+                                       signed char* P, long long colsp, long long kc, int nchunk,
+                                       unsigned long long* range = nullptr, Pred pr = Pred()) {
+    if (pr.off()) return;
+    __shared__ long long tile[32][33];
+    RangeAcc acc;
+    const long long c0 = (long long)blockIdx.x * 32, k0 = (long long)blockIdx.y * 32;
+    const int tx = threadIdx.x, ty = threadIdx.y;      // 32 x 8
+    for (int i = ty; i < 32; i += 8) {
+        const long long k = k0 + i, c = c0 + tx;
+        tile[i][tx] = (k < kdim && c < cols) ? B[k * ldb + c] : 0;
+        acc.add(tile[i][tx]);
+    }
+    if (range) acc.flush(range);
+    __syncthreads();
+    // thread (tx, ty): column c0 + (ty*4 .. ty*4+3), k = k0 + tx
+    for (int j = ty; j < 32; j += 8) {
+        const long long c = c0 + j, k = k0 + tx;
+        if (c >= colsp || k >= kc * nchunk) continue;
+        signed char d[8];
+        i64_digits(tile[tx][j], d);
+        const long long ch = k / kc, kk = k - ch * kc;
+        signed char* base = P + ((ch * colsp + c) * 8) * kc + kk;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) base[(7 - l) * kc] = d[l];
     }
 }
 

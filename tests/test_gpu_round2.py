@@ -540,3 +540,50 @@ def test_k_chunked_launches_bitexact(sid, lo, hi, store, monkeypatch):
         p.close()
     assert st["k_chunks"] == 3, st
     assert same_bits(C.cpu().numpy(), want)
+
+
+# ---- opt-in: any int64 as radix-256 digit GEMMs on the int8 tensor cores ---------------
+@pytest.mark.parametrize("m,n,k", [(256, 256, 256), (512, 384, 1000), (300, 520, 8192), (256, 256, 17000)])
+@pytest.mark.parametrize("store", [False, True])
+def test_int64_radix256_tensor_path_wraps_bitexact(m, n, k, store):
+    """Full-range int64 (wraps mod 2^64) on tcgen05 kind::i8 as 8 digit-group GEMMs per
+    K chunk (<= 8192): bit-exact against the oracle, ragged shapes, several K chunks."""
+    rng = np.random.default_rng(m + k)
+    A = rng.integers(-2 ** 63, 2 ** 63 - 1, (m, k), dtype=np.int64)
+    B = rng.integers(-2 ** 63, 2 ** 63 - 1, (k, n), dtype=np.int64)
+    A[0, :4] = [-2 ** 63, 2 ** 63 - 1, -1, 0]
+    C0 = rng.integers(-2 ** 63, 2 ** 63 - 1, (m, n), dtype=np.int64)
+    want = np.zeros((m, n), np.int64) if store else C0.copy()
+    O.gemm_fold(O.SR_INT64, want, A, B, par=True)
+    flags = _lib.F_ALLOW_NONPOW2 | _lib.F_INT_TENSOR | (_lib.F_INIT_IDENTITY if store else 0)
+    p = _lib.Plan(_lib.SR_INT64, "star", "pooled", m, n, k, 64, 148, -1, 0, flags)
+    try:
+        C = torch.from_numpy(C0.copy()).cuda()
+        At, Bt = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        p.reset_stats()
+        p.execute(C.data_ptr(), n, At.data_ptr(), k, Bt.data_ptr(), n, torch.cuda.current_stream().cuda_stream)
+        st = p.stats()
+    finally:
+        p.close()
+    assert st["path_name"] == "tcgen05_i8_radix256_int64"
+    assert same_bits(C.cpu().numpy(), want)
+
+
+def test_int64_radix256_through_the_public_api_and_guard():
+    """Config(int_tensor_cores=True): small ranges keep the single int8 GEMM, wide ranges
+    take the digit GEMMs -- first call on the host guard, later calls on the device."""
+    n = 512
+    rng = np.random.default_rng(77)
+    s = sm.INT_RING
+    cfg = sm.Config(base_dim=64, workers=148, int_tensor_cores=True)
+    with sm.Executor(cfg) as ex:
+        for lo, hi, path in [(-5, 6, "tcgen05_i8_umma"), (-2 ** 40, 2 ** 40, "tcgen05_i8_radix256_int64"),
+                             (-2 ** 40, 2 ** 40, "tcgen05_i8_radix256_int64"), (-5, 6, "tcgen05_i8_radix256_int64")]:
+            A = rng.integers(lo, hi, (n, n), dtype=np.int64)
+            B = rng.integers(lo, hi, (n, n), dtype=np.int64)
+            C = sm.Matrix(np.zeros((n, n), np.int64), s)
+            sm.run_algorithm(ex, "star", C, sm.Matrix(A, s), sm.Matrix(B, s), s)
+            want = np.zeros((n, n), np.int64)
+            O.gemm_fold(O.SR_INT64, want, A, B, par=True)
+            assert same_bits(C.numpy(), want), path
+            assert ex.last_stats["path_name"] == path
