@@ -88,8 +88,10 @@ PATH_PEAK = {
     "tcgen05_i8_umma": ("int8_tensor", "tcgen05.mma.cta_group::2 kind::i8 (UTCIMMA.2CTA), s32 in TMEM"),
     "ozaki2_fp64_tcgen05_i8x16": ("int8_tensor", "16 x tcgen05.mma.cta_group::2 kind::i8 residue passes + "
                                   "exact CRT epilogue (Ozaki scheme II)"),
+    "tcgen05_i8_radix256_int64": ("int8_tensor", "8 digit-group tcgen05.mma kind::i8 GEMMs per K chunk: "
+                                  "36 signed radix-256 digit products per int64 term (mod 2^64)"),
 }
-INT8_PASSES = {"tcgen05_i8_umma": 1, "ozaki2_fp64_tcgen05_i8x16": 16}
+INT8_PASSES = {"tcgen05_i8_umma": 1, "ozaki2_fp64_tcgen05_i8x16": 16, "tcgen05_i8_radix256_int64": 36}
 
 
 # ---- clocks during the timed region ----------------------------------------
@@ -528,9 +530,11 @@ def roofline(pk, path, local_ops, kern_s):
                 "unit": "int8 Tops/s", "peak_source": "measured cuBLASLt int8 GEMM (torch._int_mm), "
                 + ("sustained n=16384" if sustained else "burst n=8192") + ", profiles/r01_int8_peak.json",
                 "int8_ops_per_semiring_op": passes}
-        if passes > 1:
+        if path == "ozaki2_fp64_tcgen05_i8x16":
             roof["emulated_fp64_tflops"] = achieved / 1e12
             roof["vs_fp64_tensor_peak"] = achieved / pk["fp64_tensor"]
+        if path == "tcgen05_i8_radix256_int64":
+            roof["vs_cuda_core_general_int64"] = "7.0 Tops/s (simt_i64, profiles/r02e_bench_c2_general.json)"
     elif key == "fp64_tensor":
         roof = {"bound": "tensor", "achieved": achieved / 1e12, "peak": pk[key] / 1e12,
                 "unit": "TFLOP/s", "peak_source": "measured: max(DMMA.8x8x4 ubench, cuBLAS DGEMM) "
