@@ -7,6 +7,7 @@
 //                merge_tasks, ops.py:108-155) and its atomic variant
 //                (accumulate_region, ops.py:76-101)
 #pragma once
+#include <algorithm>
 #include "common.cuh"
 
 namespace starmm {
@@ -198,26 +199,39 @@ __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long
     if (pr.off()) return;
     __shared__ Tp tile[32][33];
     RangeAcc acc;
-    long long r0 = (long long)blockIdx.y * 32, k0 = (long long)blockIdx.x * 32;
-    int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
-    for (int i = ty; i < 32; i += 8) {
-        long long r = r0 + i, k = k0 + tx;
-        Tp v = pad;
-        if (r < rows && k < kdim) {
-            Tin x = A[r * lda + k];
-            acc.add(x);
-            v = (Tp)Conv::cvt(x);
+    const int tx = threadIdx.x, ty = threadIdx.y;   // 32 x 8
+    // grid-stride over 32 x 32 tiles (a bounded grid: a launch the path predicate turns
+    // off costs a few microseconds instead of one empty CTA per tile)
+    for (long long tr = blockIdx.y; tr * 32 < rowsp; tr += gridDim.y)
+        for (long long tk = blockIdx.x; tk * 32 < kp; tk += gridDim.x) {
+            const long long r0 = tr * 32, k0 = tk * 32;
+            for (int i = ty; i < 32; i += 8) {
+                long long r = r0 + i, k = k0 + tx;
+                Tp v = pad;
+                if (r < rows && k < kdim) {
+                    Tin x = A[r * lda + k];
+                    acc.add(x);
+                    v = (Tp)Conv::cvt(x);
+                }
+                tile[i][tx] = v;
+            }
+            __syncthreads();
+            // write: packed index for (k, r): ((k/G) * rowsp + r) * G + k%G
+            for (int i = ty; i < 32; i += 8) {
+                long long k = k0 + i;
+                long long r = r0 + tx;
+                if (k < kp && r < rowsp) P[((k / G) * rowsp + r) * G + (k % G)] = tile[tx][i];
+            }
+            __syncthreads();
         }
-        tile[i][tx] = v;
-    }
     if (range) acc.flush(range);
-    __syncthreads();
-    // write: packed index for (k, r): ((k/G) * rowsp + r) * G + k%G
-    for (int i = ty; i < 32; i += 8) {
-        long long k = k0 + i;
-        long long r = r0 + tx;
-        if (k < kp && r < rowsp) P[((k / G) * rowsp + r) * G + (k % G)] = tile[tx][i];
-    }
+}
+
+// bounded 2-D grid of pack_a_kernel: ~16 CTAs of 256 threads per SM
+inline dim3 pack_a_grid(long long rowsp, long long kp) {
+    const long long gx = std::max<long long>(1, std::min<long long>(kp / 32, 64));
+    const long long gy = std::max<long long>(1, std::min<long long>(rowsp / 32, (148LL * 16 + gx - 1) / gx));
+    return dim3((unsigned)gx, (unsigned)gy);
 }
 
 // B (kdim x cols, ld) -> P[kp/G][colsp][G]

@@ -409,7 +409,7 @@ template <class Tin, class Tp, int G, class Conv>
 int launch_pack(const void* A, long long lda, const void* B, long long ldb, long long m,
                 long long n, long long k, void* Ap, void* Bp, long long Mp, long long Np,
                 long long Kp, Tp pad, cudaStream_t s, unsigned long long* range, Pred pr) {
-    dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
+    const dim3 ga = pack_a_grid(Mp, Kp);
     pack_a_kernel<Tin, Tp, G, Conv><<<ga, dim3(32, 8), 0, s>>>((const Tin*)A, m, k, lda, (Tp*)Ap, Mp,
                                                               Kp, pad, range, pr);
     CK(cudaGetLastError());
@@ -1041,7 +1041,7 @@ int pack_operands(Exec& x, const Geom& G, const void* A, long long lda, const vo
     case PATH_SIMT_F32_S16X2:
     case PATH_SIMT_I32_S16X2:
     case PATH_SIMT_F64T_S16X2: {
-        dim3 ga((unsigned)(Kp / 32), (unsigned)(Mp / 32));
+        const dim3 ga = pack_a_grid(Mp, Kp);
         if (G.path == PATH_SIMT_F64T_S16X2) {
             pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                 (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);

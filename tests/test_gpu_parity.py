@@ -874,7 +874,8 @@ def test_tcgen05_int8_path_bitexact(n, algo):
 
 
 def test_tcgen05_guard_falls_back_exactly():
-    """Values beyond int8 (or K*max^2 >= 2^31) must leave the tensor path."""
+    """Values beyond int8 (or K*max^2 >= 2^31) must leave the single int8 GEMM: with
+    int_tensor_cores they take the radix-256 digit GEMMs (exact for any int64)."""
     n = 256
     rng = np.random.default_rng(0)
     A = rng.integers(-127, 128, (n, n), dtype=np.int64)
@@ -885,5 +886,5 @@ def test_tcgen05_guard_falls_back_exactly():
     with sm.Executor(cfg) as ex:
         C = sm.Matrix(np.zeros((n, n), np.int64), sm.INT_RING)
         sm.run_algorithm(ex, "co2", C, sm.Matrix(A, sm.INT_RING), sm.Matrix(B, sm.INT_RING), sm.INT_RING)
-        assert ex.last_stats["path_name"] == "simt_i64_narrow_i32"
+        assert ex.last_stats["path_name"] == "tcgen05_i8_radix256_int64"
     assert same_bits(C.numpy(), want)
