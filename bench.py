@@ -50,6 +50,14 @@ def _measured(name, key, default):
         return default
 
 
+def _measured_peaks(key, default):
+    """A figure from the driver-written MEASURED_PEAKS.json (repo root), else `default`."""
+    try:
+        return float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get(key, default))
+    except Exception:
+        return default
+
+
 def _packed(op_prefix, default):
     p = os.path.join(REPO, "profiles", "r01_packed_ops_microbench.jsonl")
     try:
@@ -524,12 +532,16 @@ def roofline(pk, path, local_ops, kern_s):
                                           "VIADDMNMX / IMAD), 64 terms/clk/SM"))
     if key == "int8_tensor":
         passes = INT8_PASSES[path]
-        sustained = kern_s > 0.010          # long kernels run into the power cap
-        peak = pk["int8_tensor_sustained" if sustained else "int8_tensor_burst"]
+        # denominator: the larger of cuBLASLt's measured int8 burst (profiles/r01_int8_peak.json)
+        # and twice MEASURED_PEAKS.json's dense bf16 burst (int8 issues at 2x bf16); our
+        # long kernels outrun cuBLASLt's power-capped SUSTAINED figure, so that one is not
+        # a ceiling.  NVIDIA's nominal dense int8 (4.5 POPS) is reported beside it.
+        bf16 = 2e12 * _measured_peaks("bf16_tflops", 1664.4)
+        peak = max(pk["int8_tensor_burst"], bf16)
         roof = {"bound": "tensor", "achieved": passes * achieved / 1e12, "peak": peak / 1e12,
-                "unit": "int8 Tops/s", "peak_source": "measured cuBLASLt int8 GEMM (torch._int_mm), "
-                + ("sustained n=16384" if sustained else "burst n=8192") + ", profiles/r01_int8_peak.json",
-                "int8_ops_per_semiring_op": passes}
+                "unit": "int8 Tops/s", "peak_source": "max(measured cuBLASLt int8 burst n=8192 "
+                "(profiles/r01_int8_peak.json), 2 x MEASURED_PEAKS.json bf16_tflops)",
+                "nominal_dense_int8": 4500.0, "int8_ops_per_semiring_op": passes}
         if path == "ozaki2_fp64_tcgen05_i8x16":
             roof["emulated_fp64_tflops"] = achieved / 1e12
             roof["vs_fp64_tensor_peak"] = achieved / pk["fp64_tensor"]
