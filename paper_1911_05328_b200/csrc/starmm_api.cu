@@ -1303,6 +1303,16 @@ int general_path(const starmm_plan* P) {
     default: return PATH_SIMT_I32_SAT;
     }
 }
+// the exact fallback queued behind a device-side verdict: cheap to launch predicated off.
+// For int-tensor plans that is the CUDA-core 64-bit kernel (2 packers + 1 tile launch),
+// not the radix-256 digit path (8 tcgen05 launches per K chunk, each with its own
+// tensor maps and gate reset: ~30% of a small config-2 step when skipped); the next call
+// starts from the digit path when the verdict says the data needs it.
+int fallback_path(const starmm_plan* P) {
+    if (P->sr == STARMM_SR_INT64) return PATH_SIMT_I64;
+    return general_path(P);
+}
+
 int fastest_path(const starmm_plan* P) {
     const bool fast = !(P->flags & STARMM_F_NO_FASTPATH);
     if (!fast) return general_path(P);
@@ -1422,7 +1432,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         host_decided = false;
         int cands[3] = {first, 0, 0};
         ncand = 1;
-        const int general = general_path(P);
+        const int general = fallback_path(P);
         if (general != first) cands[ncand++] = general;
         if (float_min(P) && ordered_ok) cands[ncand++] = PATH_MIN_ORDERED;
         Geom G[3];

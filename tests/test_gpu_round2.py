@@ -571,13 +571,15 @@ def test_int64_radix256_tensor_path_wraps_bitexact(m, n, k, store):
 
 def test_int64_radix256_through_the_public_api_and_guard():
     """Config(int_tensor_cores=True): small ranges keep the single int8 GEMM, wide ranges
-    take the digit GEMMs -- first call on the host guard, later calls on the device."""
+    take the digit GEMMs -- first call on the host guard, later calls on the device; a
+    call whose data outgrows the first guess runs the CUDA-core fallback (cheap to queue
+    predicated off) and the next call starts from the digit GEMMs."""
     n = 512
     rng = np.random.default_rng(77)
     s = sm.INT_RING
     cfg = sm.Config(base_dim=64, workers=148, int_tensor_cores=True)
     with sm.Executor(cfg) as ex:
-        for lo, hi, path in [(-5, 6, "tcgen05_i8_umma"), (-2 ** 40, 2 ** 40, "tcgen05_i8_radix256_int64"),
+        for lo, hi, path in [(-5, 6, "tcgen05_i8_umma"), (-2 ** 40, 2 ** 40, "simt_i64"),
                              (-2 ** 40, 2 ** 40, "tcgen05_i8_radix256_int64"), (-5, 6, "tcgen05_i8_radix256_int64")]:
             A = rng.integers(lo, hi, (n, n), dtype=np.int64)
             B = rng.integers(lo, hi, (n, n), dtype=np.int64)
