@@ -402,7 +402,7 @@ def main():
     dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
                         group_ks=group_ks, device=local_rank, time_kernel=True,
                         combine=args.combine, int_tensor=args.int_tensor, fp64_emu=args.fp64_emu,
-                        fastpath=not args.no_fastpath)
+                        fastpath=not args.no_fastpath, async_exec=True)
 
     # ---- input distribution: each rank generates its own panels on its device ----
     # (counter-based, no collective: DESIGN.md §8c); timed separately from the steps
@@ -573,7 +573,7 @@ def opt_in_run(args, s, cid, n, grid, rank, sms, local_rank, A, B, C, pk):
     cfg = CONFIGS[cid]
     dmm = DistributedMM(n, s, grid, rank, algo=args.algo, base_dim=cfg["b"], workers=sms,
                         device=local_rank, time_kernel=True, combine=args.combine,
-                        int_tensor=(cid == 2), fp64_emu=(cid == 4))
+                        int_tensor=(cid == 2), fp64_emu=(cid == 4), async_exec=True)
     C2 = C.clone()
     steps, warm = max(1, min(args.steps, 3)), max(1, min(args.warmup, 2))
     for _ in range(warm):

@@ -164,7 +164,22 @@ struct starmm_plan {
     long long total_allocated = 0;              // bytes this plan's acquisitions cudaMalloc'ed
     long long ws_fresh = 0, ws_reuse = 0, ws_high_water = 0;
     long long raw_count = 0, raw_bytes = 0;
-    cudaEvent_t tev[6] = {};                    // STARMM_F_TIME_MAIN, a pair per candidate
+    // STARMM_F_TIME_MAIN: each timed execute leaves one record (an event pair per queued
+    // candidate); which candidate ran is known on the device, so with a device-side
+    // verdict the select kernel writes it into a mapped ring slot.  Records are resolved
+    // when the call blocks anyway, or lazily by starmm_plan_stats: an asynchronous timed
+    // execute never waits (the bench's back-to-back steps leave no host gap).
+    struct TimedRec {
+        cudaEvent_t ev[6];
+        int ncand, ran;             // ran < 0: read ring[slot]
+        int path[3];
+        int slot;
+    };
+    std::vector<TimedRec> timed;
+    std::vector<cudaEvent_t> ev_pool;
+    unsigned long long* ring = nullptr;         // mapped pinned: selected path per timed call
+    unsigned long long* ring_dev = nullptr;
+    int ring_next = 0;
     int hint = 0;                               // narrowest path the last guard allowed
     bool spec_used = false;                     // hs[3] carries a device-written hint
     starmm_plan* twin = nullptr;                // host path: the second compute stream's plan
@@ -177,6 +192,8 @@ struct starmm_plan {
     // the last fence recorded on each stream this plan ran on (destroy waits for them)
     std::vector<FenceRef> fences;
 };
+
+static int resolve_timed(starmm_plan* P, bool block);
 
 namespace {
 
@@ -580,13 +597,14 @@ int ensure_bookkeeping(starmm_plan* P, cudaStream_t s) {
 // kernel of the semiring.  Published to the plan's mapped host words as well.
 __global__ void select_path_kernel(const unsigned long long* d_range, int sr, int flags, long long k,
                                    int first, int general, int ordered_ok, unsigned* d_sel,
-                                   unsigned long long* h) {
+                                   unsigned long long* h, unsigned long long* ring_slot) {
     if (threadIdx.x != 0) return;
     const unsigned long long mx = d_range[0], bits = d_range[1];
     const int nar = guard_narrowest(sr, flags, k, mx, bits, ordered_ok);
     const int sel = path_allowed(first, nar) ? first : (nar == PATH_MIN_ORDERED ? PATH_MIN_ORDERED : general);
     *d_sel = (unsigned)sel;
     h[0] = mx; h[1] = bits; h[2] = (unsigned long long)sel; h[3] = (unsigned long long)nar;
+    if (ring_slot) *ring_slot = (unsigned long long)sel;
     __threadfence_system();
 }
 
@@ -681,8 +699,10 @@ void starmm_plan_destroy(starmm_plan* P) {
     for (auto& f : P->fences)
         if (f && f->ev) cudaEventSynchronize(f->ev);
     P->fences.clear();
-    for (auto& e : P->tev)
-        if (e) cudaEventDestroy(e);
+    for (auto& r : P->timed)
+        for (int i = 0; i < 2 * r.ncand; ++i) cudaEventDestroy(r.ev[i]);
+    for (auto e : P->ev_pool) cudaEventDestroy(e);
+    if (P->ring) cudaFreeHost(P->ring);
     if (P->twin) starmm_plan_destroy(P->twin);
     if (P->book) P->ctx->arena.release(P->book, nullptr);
     if (P->hs) P->ctx->slots.put(P->hs, P->hs_dev);
@@ -691,6 +711,12 @@ void starmm_plan_destroy(starmm_plan* P) {
 
 int starmm_plan_reset_stats(starmm_plan* P) {
     if (!P) return STARMM_CONTRACT_VIOLATION;
+    // timed records of earlier executes belong to the stats being discarded
+    for (auto& r : P->timed) {
+        cudaEventSynchronize(r.ev[2 * r.ncand - 1]);
+        for (int i = 0; i < 2 * r.ncand; ++i) P->ev_pool.push_back(r.ev[i]);
+    }
+    P->timed.clear();
     if (P->d_counters) {
         CK(cudaMemset(P->d_counters, 0, CNT__N * 8));
         CK(cudaMemset(P->d_worker_used, 0, (size_t)P->max_workers * 4));
@@ -703,6 +729,11 @@ int starmm_plan_reset_stats(starmm_plan* P) {
 
 int starmm_plan_stats(starmm_plan* P, starmm_stats* out) {
     if (!P || !out) return STARMM_CONTRACT_VIOLATION;
+    {
+        DeviceGuard dg;
+        TRY(dg.set(P->device));
+        TRY(resolve_timed(P, true));          // timed async executes: wait for their events
+    }
     *out = P->st;
     unsigned long long c[CNT__N];
     memset(c, 0, sizeof(c));
@@ -1335,6 +1366,32 @@ bool needs_guard(const starmm_plan* P) {
 
 }  // namespace
 
+// Resolve timed records: every one (block = true) or those already complete.
+static int resolve_timed(starmm_plan* P, bool block) {
+    size_t done = 0;
+    for (; done < P->timed.size(); ++done) {
+        auto& r = P->timed[done];
+        const cudaEvent_t last = r.ev[2 * r.ncand - 1];
+        if (block) CK(cudaEventSynchronize(last));
+        else if (cudaEventQuery(last) != cudaSuccess) { cudaGetLastError(); break; }
+        int ran = r.ran;
+        if (ran < 0) {
+            ran = 0;
+            const int sel = (int)P->ring[r.slot];
+            for (int c = 0; c < r.ncand; ++c)
+                if (r.path[c] == sel) ran = c;
+            P->st.path = sel;
+        }
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, r.ev[2 * ran], r.ev[2 * ran + 1]));
+        P->st.main_kernel_ns += (int64_t)((double)ms * 1e6);
+        P->st.main_kernel_launches += 1;
+        for (int i = 0; i < 2 * r.ncand; ++i) P->ev_pool.push_back(r.ev[i]);
+    }
+    P->timed.erase(P->timed.begin(), P->timed.begin() + (long)done);
+    return STARMM_OK;
+}
+
 // force_async: the caller synchronises (host path, Strassen leaves).  host_guard: read
 // the range guard on the host every call -- the host-buffer schedule, whose row blocks
 // alternate between two compute streams: a predicated-off fallback TILE kernel still
@@ -1354,8 +1411,28 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     TRY(ensure_bookkeeping(P, s));
     const bool async = (P->flags & STARMM_F_ASYNC) || force_async;
     const bool timed = (P->flags & STARMM_F_TIME_MAIN) != 0;
-    if (timed && !P->tev[0])
-        for (auto& e : P->tev) CK(cudaEventCreate(&e));
+    starmm_plan::TimedRec rec{};
+    if (timed) {
+        TRY(resolve_timed(P, false));                  // recycle what has completed
+        if (P->timed.size() >= 64) TRY(resolve_timed(P, true));
+        if (!P->ring) {
+            void* h = nullptr;
+            CK(cudaHostAlloc(&h, 64 * sizeof(unsigned long long), cudaHostAllocMapped));
+            P->ring = (unsigned long long*)h;
+            CK(cudaHostGetDevicePointer((void**)&P->ring_dev, h, 0));
+        }
+        for (int i = 0; i < 6; ++i) {
+            if (P->ev_pool.empty()) {
+                cudaEvent_t e;
+                CK(cudaEventCreate(&e));
+                P->ev_pool.push_back(e);
+            }
+            rec.ev[i] = P->ev_pool.back();
+            P->ev_pool.pop_back();
+        }
+        rec.slot = P->ring_next;
+        P->ring_next = (P->ring_next + 1) % 64;
+    }
     // an earlier call's device-side verdict (mapped host word; stale is fine: a hint)
     if (P->spec_used && P->hs[3]) P->hint = (int)P->hs[3];
     const bool ordered_ok = P->remote_parts == 0;
@@ -1388,7 +1465,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             long long olda, oldb;
             if ((rc = pack_operands(x, G, A, lda, B, ldb, pa, pb, nullptr, Pred(), &opA, &olda, &opB, &oldb))) break;
             rc = launch_candidate(x, G, C, ldc, A, lda, B, ldb, opA, olda, opB, oldb, Pred(),
-                                  timed ? &P->tev[0] : nullptr, info[0]);
+                                  timed ? &rec.ev[0] : nullptr, info[0]);
             ncand = 1;
             break;
         }
@@ -1422,7 +1499,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
                     if (nar != first) { first = nar; continue; }   // re-pack for the allowed path
                 }
                 rc = launch_candidate(x, G, C, ldc, A, lda, B, ldb, opA, olda, opB, oldb, Pred(),
-                                      timed ? &P->tev[0] : nullptr, info[0]);
+                                      timed ? &rec.ev[0] : nullptr, info[0]);
                 ncand = 1;
                 break;
             }
@@ -1456,7 +1533,8 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
         if ((rc = pack_operands(x, G[0], A, lda, B, ldb, pa, pb, P->d_range, Pred(), &opA[0], &olda[0],
                                 &opB[0], &oldb[0]))) break;
         select_path_kernel<<<1, 32, 0, s>>>(P->d_range, P->sr, P->flags, P->k, first, general,
-                                            ordered_ok ? 1 : 0, P->d_sel, P->hs_dev);
+                                            ordered_ok ? 1 : 0, P->d_sel, P->hs_dev,
+                                            timed ? P->ring_dev + rec.slot : nullptr);
         if ((rc = cuda_status(cudaGetLastError()))) break;
         ++x.launches;
         P->spec_used = true;
@@ -1465,7 +1543,7 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
             if (c > 0 && (rc = pack_operands(x, G[c], A, lda, B, ldb, pa, pb, nullptr, pr, &opA[c], &olda[c],
                                              &opB[c], &oldb[c]))) break;
             rc = launch_candidate(x, G[c], C, ldc, A, lda, B, ldb, opA[c], olda[c], opB[c], oldb[c], pr,
-                                  timed ? &P->tev[2 * c] : nullptr, info[c]);
+                                  timed ? &rec.ev[2 * c] : nullptr, info[c]);
         }
     } while (0);
 
@@ -1485,11 +1563,12 @@ static int execute_impl(starmm_plan* P, void* C, int64_t ldc, const void* A, int
     }
     const CandInfo& ci = info[ran];
     if (timed) {
-        CK(cudaEventSynchronize(P->tev[2 * ran + 1]));
-        float ms = 0.f;
-        CK(cudaEventElapsedTime(&ms, P->tev[2 * ran], P->tev[2 * ran + 1]));
-        P->st.main_kernel_ns += (int64_t)((double)ms * 1e6);
-        P->st.main_kernel_launches += 1;
+        rec.ncand = ncand;
+        for (int c = 0; c < ncand; ++c) rec.path[c] = info[c].path;
+        rec.ran = (host_decided || !async) ? ran : -1;
+        for (int i = 2 * ncand; i < 6; ++i) P->ev_pool.push_back(rec.ev[i]);   // unused pairs
+        P->timed.push_back(rec);
+        if (!async) TRY(resolve_timed(P, true));
     }
     P->raw_count += ci.raw_count;
     P->raw_bytes += ci.raw_bytes;

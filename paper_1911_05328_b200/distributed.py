@@ -89,7 +89,7 @@ class DistributedMM:
                  base_dim: int = 64, workers: int = 1, group_ks=None,
                  local_mm: Optional[Callable] = None, device: Optional[int] = None,
                  time_kernel: bool = False, combine: str = "nccl", int_tensor: bool = False,
-                 fp64_emu: bool = False, fastpath: bool = True):
+                 fp64_emu: bool = False, fastpath: bool = True, async_exec: bool = False):
         self.n, self.s, self.grid, self.rank = n, semiring, grid, rank
         self.I, self.J, self.K = grid.coords(rank)
         self.r0, self.r1 = block_bounds(n, grid.pr, self.I)
@@ -123,6 +123,8 @@ class DistributedMM:
                 flags |= _lib.F_FP64_EMU
             if not fastpath:
                 flags |= _lib.F_NO_FASTPATH
+            if async_exec:            # stream-ordered, the caller synchronises (bench loops)
+                flags |= _lib.F_ASYNC
             self.plan = _lib.Plan(semiring.sr_id, algo, "pooled", self.m, self.nn, self.k,
                                   base_dim, workers, -1,
                                   device if device is not None else torch.cuda.current_device(),
