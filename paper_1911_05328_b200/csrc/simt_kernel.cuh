@@ -33,6 +33,7 @@
 // are 4 (rows) x 8 (cols) threads so A reads broadcast across 8 lanes and B
 // reads across 4.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 #include "writeback.cuh"
 #include "dmma_kernel.cuh"   // cp.async helpers
@@ -213,6 +214,11 @@ constexpr int smem_bytes() {
 }
 }  // namespace simt
 
+// Unroll factor of the k-group loop inside a stage: a policy may set KGU (the fully
+// unrolled dp4a stage is 1024 IDP.4A = 21 KB of SASS); default full.
+template <class P, class = void> struct KgUnroll { static constexpr int v = P::BK / P::KSTEP; };
+template <class P> struct KgUnroll<P, std::void_t<decltype(P::KGU)>> { static constexpr int v = P::KGU; };
+
 struct SimtParams {
     const void* Ap;   // packed [Kp/KSTEP][Mp][G]
     const void* Bp;   // packed [Kp/KSTEP][Np/OUTS][G]
@@ -222,80 +228,109 @@ struct SimtParams {
     Pred pr;          // device-side path predicate (common.cuh)
 };
 
-template <class Pol, class Sr, int MINB = 1, bool MB = false>
+template <class Pol, class Sr, int MINB = 1>
 __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams p) {
     using namespace simt;
     using Tp = typename Pol::Tp;
     using Acc = typename Pol::Acc;
+    using T = typename Sr::T;
     if (p.pr.off()) return;
     constexpr int G = Pol::G, KSTEP = Pol::KSTEP, OUTS = Pol::OUTS, BK = Pol::BK;
     constexpr int BN = BNW * OUTS;                      // output columns per tile
     constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // positions per 16-byte load
     constexpr int NQ = 8 / VEC;                         // 16-byte loads per operand per k-group
     constexpr int KG = BK / KSTEP;                      // k-groups per stage
+    constexpr int KGU = KgUnroll<Pol>::v;               // unroll of the k-group loop
     constexpr int A_STAGE = KG * BM * G;                // elements
     constexpr int B_STAGE = KG * BNW * G;
     constexpr int CHUNK = 16 / (int)sizeof(Tp);         // elements per cp.async
+    // Each thread copies the same PASSES 16-byte chunks of every k-stage: its global
+    // source pointers advance by one stage per fill (fills are issued in k order), so the
+    // steady-state loop carries two 64-bit adds instead of re-deriving the addresses
+    // from the stage index (IMAD.WIDE chains, spilled in the 128-register builds).
+    constexpr int ROW_CHUNKS = BM * G / CHUNK;          // == BNW * G / CHUNK
+    constexpr int RPP = THREADS / ROW_CHUNKS;           // k-group rows per pass
+    constexpr int PASSES = KG / RPP;
+    static_assert(BM == BNW && KG % RPP == 0 && THREADS % ROW_CHUNKS == 0, "stage copy shape");
     extern __shared__ __align__(128) unsigned char smem_raw[];
     Tp* As = reinterpret_cast<Tp*>(smem_raw);
     Tp* Bs = As + STAGES * A_STAGE;
-    unsigned long long* full = reinterpret_cast<unsigned long long*>(Bs + STAGES * B_STAGE);
-    unsigned long long* empty = full + STAGES;
-    int* smem_word = reinterpret_cast<int*>(empty + STAGES);
+    int* smem_word = reinterpret_cast<int*>(Bs + STAGES * B_STAGE);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int ty = (warp >> 1) * 4 + (lane >> 3);      // 0..15
     const int tx = (warp & 1) * 8 + (lane & 7);        // 0..15
     const TaskGrid& g = p.g;
-    const Tp* Ap = reinterpret_cast<const Tp*>(p.Ap);
-    const Tp* Bp = reinterpret_cast<const Tp*>(p.Bp);
-    if constexpr (MB) {          // mbarrier ring (see dmma_fp64_kernel_mb); off by default:
-                                 // tools/sweep_simt.cu shows the spin costs these
-                                 // issue-bound loops 2-6%
-        if (tid == 0) {
-            for (int st = 0; st < STAGES; ++st) {
-                mbar_init(&full[st], THREADS);
-                mbar_init(&empty[st], THREADS);
-            }
-        }
-        __syncthreads();
-    }
-    long long gk = 0;
+    const long long Nw = p.Np / OUTS;
+    const int r0 = tid / ROW_CHUNKS, q0 = tid % ROW_CHUNKS;
+    const int s_off = r0 * BM * G + q0 * CHUNK;
+    const long long a_pass = (long long)RPP * p.Mp * G, b_pass = (long long)RPP * Nw * G;
+    const long long a_adv = (long long)KG * p.Mp * G, b_adv = (long long)KG * Nw * G;
+    const Tp* pa = nullptr;      // this thread's next k-stage of A / B in global memory
+    const Tp* pb = nullptr;
 
-    // one output tile over k-stages [kst0, kst0 + nk) with write-back protocol `mode`
-    auto process = [&](int tm, int tn, int s, int tile, int mode, int pair_seen, long long kst0,
-                       int nk) {
-        // k-group row kg of A covers Mp*G contiguous elements, of B (Np/OUTS)*G
-        const long long kg0 = kst0 * KG;
-        const long long Nw = p.Np / OUTS;
-        const Tp* Ag = Ap + kg0 * p.Mp * G + (long long)tm * BM * G;
-        const Tp* Bg = Bp + kg0 * Nw * G + (long long)tn * BNW * G;
-
-        auto load_stage = [&](int kt, int stage) {
-            const long long kgs = (long long)kt * KG;
-            Tp* as = As + stage * A_STAGE;
-            Tp* bs = Bs + stage * B_STAGE;
-            constexpr int ROW_CHUNKS = BM * G / CHUNK;
-            constexpr int TOTAL = KG * ROW_CHUNKS;
+    auto load_next = [&](int stage) {
+        Tp* as = As + stage * A_STAGE + s_off;
+        Tp* bs = Bs + stage * B_STAGE + s_off;
 #pragma unroll
-            for (int i = 0; i < TOTAL / THREADS; ++i) {
-                int c = tid + i * THREADS;
-                int r = c / ROW_CHUNKS, q = c % ROW_CHUNKS;
-                cp_async16(as + r * BM * G + q * CHUNK, Ag + (kgs + r) * p.Mp * G + q * CHUNK);
-                cp_async16(bs + r * BNW * G + q * CHUNK, Bg + (kgs + r) * Nw * G + q * CHUNK);
-            }
-        };
+        for (int i = 0; i < PASSES; ++i) {
+            cp_async16(as + i * RPP * BM * G, pa + i * a_pass);
+            cp_async16(bs + i * RPP * BNW * G, pb + i * b_pass);
+        }
+        pa += a_adv;
+        pb += b_adv;
+    };
 
-        Acc acc[8][8];
+    // begin(): point the stage copies at tile (tm, tn), k-stages [kst0, kst0 + nk), and
+    // put the first STAGES - 1 of them in flight.  The shared-memory ring must be idle.
+    // k-group row kg of A covers Mp*G contiguous elements, of B (Np/OUTS)*G.
+    auto begin = [&](int tm, int tn, long long kst0, int nk) {
+        const long long kg0 = kst0 * KG;
+        pa = reinterpret_cast<const Tp*>(p.Ap) + (kg0 + r0) * p.Mp * G + (long long)tm * BM * G + q0 * CHUNK;
+        pb = reinterpret_cast<const Tp*>(p.Bp) + (kg0 + r0) * Nw * G + (long long)tn * BNW * G + q0 * CHUNK;
+#pragma unroll
+        for (int st = 0; st < STAGES - 1; ++st) {
+            if (st < nk) load_next(st);
+            cp_async_commit();
+        }
+    };
+
+    // An exclusive fold reads its C tile once, at the end: ask L2 for it now, so the
+    // epilogue's loads (issued by every CTA of a wave at the same moment) do not wait
+    // on DRAM.  One 128-byte line per thread and pass.
+    auto prefetch_c = [&](int tm, int tn) {
+        constexpr int LINES_PER_ROW = BN * (int)sizeof(T) / 128;
+        static_assert(LINES_PER_ROW >= 1 && THREADS % LINES_PER_ROW == 0, "C tile prefetch shape");
+        constexpr int ROWS_PER_PASS = THREADS / LINES_PER_ROW;
+        const T* C = reinterpret_cast<const T*>(p.w.C);
+        const long long gc = (long long)tn * BN + (long long)(tid % LINES_PER_ROW) * (128 / (int)sizeof(T));
+        if (gc >= p.w.N) return;
+#pragma unroll
+        for (int r = tid / LINES_PER_ROW; r < BM; r += ROWS_PER_PASS) {
+            const long long gr = (long long)tm * BM + r;
+            if (gr < p.w.M) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + gr * p.w.ldc + gc));
+        }
+    };
+
+    Acc acc[8][8];
+
+    // mainloop(): the nk k-stages begin() addressed, into acc.  Leaves the ring idle.
+    auto mainloop = [&](int nk) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = Pol::init();
-
-        auto compute_stage = [&](int slot) {
-            const Tp* as = As + slot * A_STAGE + ty * VEC * G;
-            const Tp* bs = Bs + slot * B_STAGE + tx * VEC * G;
-#pragma unroll
+        const Tp* as0 = As + ty * VEC * G;
+        const Tp* bs0 = Bs + tx * VEC * G;
+        int ld_slot = STAGES - 1, cp_slot = 0;
+        for (int kt = 0; kt < nk; ++kt) {
+            cp_async_wait<STAGES - 2>();
+            __syncthreads();
+            if (kt + STAGES - 1 < nk) load_next(ld_slot);
+            cp_async_commit();
+            const Tp* as = as0 + cp_slot * A_STAGE;
+            const Tp* bs = bs0 + cp_slot * B_STAGE;
+#pragma unroll KGU
             for (int kg = 0; kg < KG; ++kg) {
                 // 8 row operands / 8 column operands, each G elements wide
                 Tp a[8 * G], b[8 * G];
@@ -318,43 +353,65 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                         }
                     }
             }
-        };
-        if constexpr (MB) {
-            auto fill = [&](int kt) {
-                const long long gidx = gk + kt;
-                const int slot = (int)(gidx % STAGES);
-                if (gidx >= STAGES) mbar_wait(&empty[slot], (unsigned)(((gidx / STAGES) - 1) & 1));
-                load_stage(kt, slot);
-                mbar_cp_async_arrive(&full[slot]);
-            };
-            for (int st = 0; st < STAGES - 1 && st < nk; ++st) fill(st);
-            for (int kt = 0; kt < nk; ++kt) {
-                const long long gidx = gk + kt;
-                const int slot = (int)(gidx % STAGES);
-                mbar_wait(&full[slot], (unsigned)((gidx / STAGES) & 1));
-                compute_stage(slot);
-                mbar_arrive(&empty[slot]);
-                if (kt + STAGES - 1 < nk) fill(kt + STAGES - 1);
-            }
-            gk += nk;
-        } else {
-#pragma unroll
-            for (int st = 0; st < STAGES - 1; ++st) {
-                if (st < nk) load_stage(st, st);
-                cp_async_commit();
-            }
-            for (int kt = 0; kt < nk; ++kt) {
-                cp_async_wait<STAGES - 2>();
-                __syncthreads();
-                int nxt = kt + STAGES - 1;
-                if (nxt < nk) load_stage(nxt, nxt % STAGES);
-                cp_async_commit();
-                compute_stage(kt % STAGES);
-            }
-            cp_async_wait<0>();
-            __syncthreads();
+            ld_slot = ld_slot == STAGES - 1 ? 0 : ld_slot + 1;
+            cp_slot = cp_slot == STAGES - 1 ? 0 : cp_slot + 1;
         }
-        using T = typename Sr::T;
+        cp_async_wait<0>();
+        __syncthreads();
+    };
+
+    // finish(): acc -> C under write-back protocol `mode`.  Exclusive folds / stores of a
+    // full tile whose rows are 16-byte aligned take the vectorised epilogue
+    // (writeback.cuh epilogue_row_vec: whole 32-byte sectors per warp access); ragged
+    // edges, unaligned targets and the k-split protocols take the generic one.
+    auto finish = [&](int tm, int tn, int s, int tile, int mode, int pair_seen) {
+        if (mode == WB_STORE || mode == WB_FOLD) {
+            T* dst = reinterpret_cast<T*>(p.w.C);
+            long long ld = p.w.ldc;
+            if (mode == WB_STORE && p.w.mode_base == 1 && s > 0) {   // co3: slice s>0 -> workspace D_s
+                dst = reinterpret_cast<T*>(p.w.W) + (long long)(s - 1) * p.w.wstride;
+                ld = p.w.ldw;
+            }
+            const long long m0 = (long long)tm * BM, n0 = (long long)tn * BN;
+            const bool vec_ok = m0 + BM <= p.w.M && n0 + BN <= p.w.N &&
+                                (reinterpret_cast<unsigned long long>(dst) & 15) == 0 &&
+                                (ld * (long long)sizeof(T)) % 16 == 0;
+            if (vec_ok) {
+                constexpr int W = VEC * OUTS;        // consecutive output columns per fragment
+                // rows per batch (all loads of a batch are issued before its stores): the
+                // one-CTA-per-SM builds have the registers for two rows in flight
+#ifdef STARMM_EPI_ROWS
+                constexpr int RB = STARMM_EPI_ROWS;
+#else
+                constexpr int RB = (MINB == 1 && W * (int)sizeof(T) <= 32) ? 2 : 1;
+#endif
+                const bool odd = (lane & 1) != 0;
+#pragma unroll
+                for (int ib = 0; ib < 8; ib += RB) {
+                    T frag[RB * NQ][W];
+                    T* gp[RB * NQ];
+#pragma unroll
+                    for (int ir = 0; ir < RB; ++ir) {
+                        const int i = ib + ir;
+                        const int r = (i / VEC) * 16 * VEC + ty * VEC + (i % VEC);
+#pragma unroll
+                        for (int jb = 0; jb < NQ; ++jb) {
+#pragma unroll
+                            for (int x = 0; x < W; ++x) {
+                                if constexpr (OUTS == 1) {
+                                    frag[ir * NQ + jb][x] = (T)Finish<Pol, Sr>::out(acc[i][jb * VEC + x]);
+                                } else {
+                                    frag[ir * NQ + jb][x] = (T)Finish<Pol, Sr>::out2(acc[i][jb * VEC + x / 2], x % 2);
+                                }
+                            }
+                            gp[ir * NQ + jb] = dst + (m0 + r) * ld + n0 + (long long)(jb * 16 * VEC + tx * VEC) * OUTS;
+                        }
+                    }
+                    epilogue_row_vec<Sr, W, RB * NQ>(frag, gp, mode == WB_FOLD, odd);
+                }
+                return;
+            }
+        }
         writeback<Sr, BM, BN, THREADS, 16>(p.w, g, tm, tn, s, tile, blockIdx.x, mode, pair_seen,
                               [&](auto f) {
 #pragma unroll
@@ -379,9 +436,9 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         // exclusively, pieces of a tile shared by workers merge with the atomic-madd.
         TaskGrid g1 = g;
         g1.S = 1; g1.log2S = 0;
-        const long long T = (long long)g.tiles_m * g.tiles_n * g.kstages;
-        long long it = T * blockIdx.x / gridDim.x;
-        const long long end = T * (blockIdx.x + 1) / gridDim.x;
+        const long long Tn = (long long)g.tiles_m * g.tiles_n * g.kstages;
+        long long it = Tn * blockIdx.x / gridDim.x;
+        const long long end = Tn * (blockIdx.x + 1) / gridDim.x;
         while (it < end) {
             const long long tl = it / g.kstages;
             const long long ks = it - tl * g.kstages;
@@ -392,21 +449,48 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
             if (ks == 0 && ke == g.kstages && p.w.remote_parts == 0)
                 mode = p.w.init_identity ? WB_STORE : WB_FOLD;
             leaf_enter(p.w);
-            process(tm, tn, 0, tile, mode, PAIR_EMPTY, ks, (int)(ke - ks));
+            begin(tm, tn, ks, (int)(ke - ks));
+            if (mode == WB_FOLD) prefetch_c(tm, tn);
+            mainloop((int)(ke - ks));
+            finish(tm, tn, 0, tile, mode, PAIR_EMPTY);
             leaf_exit(p.w);
             it += ke - ks;
         }
         return;
     }
-    for (int t = blockIdx.x; t < g.num_tasks; t += gridDim.x) {
-        int tm, tn, s, tile;
+    // Persistent task loop.  The next task's first k-stages are put in flight BEFORE this
+    // task's write-back (the ring is idle by then), so the copy latency of a tile start
+    // hides behind the epilogue of the previous tile.  SAR pair tasks announce themselves
+    // (pair_arrive) when their leaf starts, so they begin after the write-back instead.
+    const int nk = (int)(g.kslice / BK);
+    int t = blockIdx.x;
+    int tm = 0, tn = 0, s = 0, tile = 0, mode = 0;
+    bool begun = false;
+    if (t < g.num_tasks) {
         decode_task(g, t, tm, tn, s, tile);
-        const int mode = task_mode(p.w, g, s);
+        mode = task_mode(p.w, g, s);
+    }
+    while (t < g.num_tasks) {
         int pair_seen = PAIR_EMPTY;
         if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
         leaf_enter(p.w);
-        process(tm, tn, s, tile, mode, pair_seen, (long long)s * g.kslice / BK, (int)(g.kslice / BK));
+        if (!begun) begin(tm, tn, (long long)s * nk, nk);
+        if (mode == WB_FOLD) prefetch_c(tm, tn);
+        mainloop(nk);
+        const int t2 = t + gridDim.x;
+        int tm2 = 0, tn2 = 0, s2 = 0, tile2 = 0, mode2 = 0;
+        begun = false;
+        if (t2 < g.num_tasks) {
+            decode_task(g, t2, tm2, tn2, s2, tile2);
+            mode2 = task_mode(p.w, g, s2);
+            if (mode2 != WB_PAIR) {
+                begin(tm2, tn2, (long long)s2 * nk, nk);
+                begun = true;
+            }
+        }
+        finish(tm, tn, s, tile, mode, pair_seen);
         leaf_exit(p.w);
+        t = t2; tm = tm2; tn = tn2; s = s2; tile = tile2; mode = mode2;
     }
 }
 

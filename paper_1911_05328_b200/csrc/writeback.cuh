@@ -57,6 +57,138 @@ STARMM_DEV void fold_batched(Each each, Addr addr, bool cg) {
     }
 }
 
+
+// ---------------------------------------------------------------------------
+// Vectorised exclusive epilogue (WB_FOLD / WB_STORE of full, 16-byte-aligned tiles).
+//
+// A CUDA-core thread owns FRAGMENTS of W consecutive output columns (FB = W * sizeof(T)
+// bytes: 8, 16, 32 or 64), and the lanes tx, tx+1, ... of a row own adjacent fragments.
+// Written element by element that is one 8-byte generic ST per lane at a 32-byte stride:
+// every warp store touches 32 sectors and fills a quarter of each (ncu, int64 dp4a tile:
+// 16.8 M L2 sectors requested for 4.2 M ideal, and ~11 us per tile boundary).  Here a
+// fragment moves as 16-byte PIECES; when FB >= 32 the two lanes of an even/odd pair first
+// swap pieces so that instruction k of the pair covers bytes [32k, 32k + 32) of the pair's
+// 2*FB contiguous bytes -- every warp access reads or writes whole 32-byte sectors.
+// ---------------------------------------------------------------------------
+STARMM_DEV uint4 ldg16(const void* p) {
+    uint4 v;
+    asm volatile("ld.global.v4.u32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(__cvta_generic_to_global(p)));
+    return v;
+}
+STARMM_DEV void stg16(void* p, uint4 v) {
+    asm volatile("st.global.v4.u32 [%0], {%1,%2,%3,%4};"
+                 ::"l"(__cvta_generic_to_global(p)), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
+STARMM_DEV uint2 ldg8(const void* p) {
+    uint2 v;
+    asm volatile("ld.global.v2.u32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "l"(__cvta_generic_to_global(p)));
+    return v;
+}
+STARMM_DEV void stg8(void* p, uint2 v) {
+    asm volatile("st.global.v2.u32 [%0], {%1,%2};" ::"l"(__cvta_generic_to_global(p)), "r"(v.x), "r"(v.y) : "memory");
+}
+STARMM_DEV uint4 shfl_xor1_16(uint4 v) {
+    v.x = __shfl_xor_sync(0xffffffffu, v.x, 1);
+    v.y = __shfl_xor_sync(0xffffffffu, v.y, 1);
+    v.z = __shfl_xor_sync(0xffffffffu, v.z, 1);
+    v.w = __shfl_xor_sync(0xffffffffu, v.w, 1);
+    return v;
+}
+STARMM_DEV uint4 sel16(bool c, uint4 a, uint4 b) {
+    return make_uint4(c ? a.x : b.x, c ? a.y : b.y, c ? a.z : b.z, c ? a.w : b.w);
+}
+
+// Lane parity b of a pair owns pieces b*NPL + i (i < NPL) of the pair's 2*NPL pieces;
+// afterwards q[k] is pair piece 2k + b.  All 32 lanes must call.
+template <int NPL>
+STARMM_DEV void pair_exchange(uint4 (&q)[NPL], bool odd) {
+    static_assert(NPL >= 2 && NPL % 2 == 0, "pieces per lane");
+    uint4 out[NPL];
+#pragma unroll
+    for (int r = 0; r < NPL / 2; ++r) {
+        const uint4 recv = shfl_xor1_16(sel16(odd, q[2 * r], q[2 * r + 1]));
+        out[r] = sel16(odd, recv, q[2 * r]);
+        out[NPL / 2 + r] = sel16(odd, q[2 * r + 1], recv);
+    }
+#pragma unroll
+    for (int k = 0; k < NPL; ++k) q[k] = out[k];
+}
+
+template <class Sr>
+STARMM_DEV uint4 fold16(uint4 old, uint4 v) {
+    using T = typename Sr::T;
+    constexpr int N = 16 / (int)sizeof(T);
+    union U { uint4 q; T e[N]; } a, b;
+    a.q = old; b.q = v;
+#pragma unroll
+    for (int x = 0; x < N; ++x) a.e[x] = Sr::fold(a.e[x], b.e[x]);
+    return a.q;
+}
+
+// One thread's NF fragments of one output row: frag[f] holds W elements destined for
+// gp[f][0..W) (16-byte aligned, or 8-byte when FB == 8).  fold: C <- fold(C, v), else
+// plain store.  `odd`: parity of this lane within its even/odd pair (lane & 1); the
+// partner's fragments are the next (odd) / previous (even) FB bytes.  Warp-collective.
+template <class Sr, int W, int NF>
+STARMM_DEV void epilogue_row_vec(typename Sr::T (&frag)[NF][W], typename Sr::T* (&gp)[NF], bool fold,
+                                 bool odd) {
+    using T = typename Sr::T;
+    constexpr int FB = W * (int)sizeof(T);
+    static_assert(FB == 8 || FB == 16 || FB == 32 || FB == 64, "fragment bytes");
+    if constexpr (FB == 8) {
+        union U { uint2 q; T e[W]; };
+        U v[NF], old[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+#pragma unroll
+            for (int x = 0; x < W; ++x) v[f].e[x] = frag[f][x];
+            if (fold) old[f].q = ldg8(gp[f]);
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+            if (fold) {
+#pragma unroll
+                for (int x = 0; x < W; ++x) v[f].e[x] = Sr::fold(old[f].e[x], v[f].e[x]);
+            }
+            stg8(gp[f], v[f].q);
+        }
+    } else {
+        constexpr int NPL = FB / 16;
+        constexpr int EPV = 16 / (int)sizeof(T);
+        union U { uint4 q; T e[EPV]; };
+        uint4 v[NF][NPL], old[NF][NPL];
+        char* base[NF];
+#pragma unroll
+        for (int f = 0; f < NF; ++f) {
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) {
+                U u;
+#pragma unroll
+                for (int x = 0; x < EPV; ++x) u.e[x] = frag[f][k * EPV + x];
+                v[f][k] = u.q;
+            }
+            base[f] = reinterpret_cast<char*>(gp[f]);
+            if constexpr (NPL >= 2) {
+                pair_exchange<NPL>(v[f], odd);
+                base[f] += odd ? (16 - FB) : 0;      // pair base + 16*b; piece k at + 32*k
+            }
+            if (fold) {
+#pragma unroll
+                for (int k = 0; k < NPL; ++k) old[f][k] = ldg16(base[f] + (NPL >= 2 ? 32 : 16) * k);
+            }
+        }
+#pragma unroll
+        for (int f = 0; f < NF; ++f)
+#pragma unroll
+            for (int k = 0; k < NPL; ++k) {
+                uint4 x = v[f][k];
+                if (fold) x = fold16<Sr>(old[f][k], x);
+                stg16(base[f] + (NPL >= 2 ? 32 : 16) * k, x);
+            }
+    }
+}
+
 // FOLD_CH: elements per batched read-fold-write chunk; 0 = element by element (the DMMA
 // kernel, whose full aligned FOLD tiles take its own vectorised epilogue (EPI=1,
 // dmma_kernel.cuh) -- this generic path only sees its ragged / protocol tiles; changes

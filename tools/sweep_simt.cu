@@ -7,15 +7,16 @@
 using namespace starmm;
 
 template <class Pol, class Sr, int MINB, bool MB = true>
-void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long long* cnt, int sms) {
+void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long long* cnt, int sms, int store = 0) {
     SimtParams p{};
     p.Ap = Ap; p.Bp = Bp; p.Mp = n; p.Np = n;
     TaskGrid& g = p.g;
     g.tiles_m = n / 128; g.tiles_n = n / simt::bn<Pol>(); g.S = 1; g.log2S = 0; g.group_m = 8; g.kslice = n;
     g.num_tasks = g.tiles_m * g.tiles_n;
     WbParams& w = p.w;
-    w.mode_base = 0; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
-    auto kern = simt_mm_kernel<Pol, Sr, MINB, MB>;
+    w.mode_base = 0; w.init_identity = store; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
+    auto kern = simt_mm_kernel<Pol, Sr, MINB>;   // (MB: the mbarrier ring variant was removed in round 2,
+                                                  //  -1..-6%: profiles/r01n_sweep_simt_occ1_mbarrier.jsonl)
     constexpr int smem = simt::smem_bytes<Pol>();
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int occ = 0;
@@ -38,6 +39,22 @@ struct PolI8Dp4aBK32 : PolI8Dp4a { static constexpr int BK = 32; };
 template <> struct starmm::Finish<PolI8Dp4aBK128, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 template <> struct starmm::Finish<PolI8Dp4aBK32, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 
+// k-group loop unroll variants (the fully unrolled dp4a stage is 21 KB of SASS)
+struct PolI8Dp4aU2 : PolI8Dp4a { static constexpr int KGU = 2; };
+struct PolI8Dp4aU4 : PolI8Dp4a { static constexpr int KGU = 4; };
+struct PolI8Dp4aU8 : PolI8Dp4a { static constexpr int KGU = 8; };
+template <> struct starmm::Finish<PolI8Dp4aU2, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
+template <> struct starmm::Finish<PolI8Dp4aU4, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
+template <> struct starmm::Finish<PolI8Dp4aU8, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
+struct PolS16U4 : PolS16x2Min { static constexpr int KGU = 4; };
+struct PolS16U8 : PolS16x2Min { static constexpr int KGU = 8; };
+template <> struct starmm::Finish<PolS16U4, SrTropF32> : starmm::Finish<PolS16x2Min, SrTropF32> {};
+template <> struct starmm::Finish<PolS16U8, SrTropF32> : starmm::Finish<PolS16x2Min, SrTropF32> {};
+struct PolF32PairU2 : PolF32Pair { static constexpr int KGU = 2; };
+struct PolF32PairU4 : PolF32Pair { static constexpr int KGU = 4; };
+template <> struct starmm::Finish<PolF32PairU2, SrTropI32> : starmm::Finish<PolF32Pair, SrTropI32> {};
+template <> struct starmm::Finish<PolF32PairU4, SrTropI32> : starmm::Finish<PolF32Pair, SrTropI32> {};
+
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 8192;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -45,12 +62,21 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
-    if (argc > 2 && argv[2][0] == 'm') {   // one CTA per SM: barrier ring vs mbarrier ring
+    if (argc > 2 && argv[2][0] == 'u') {   // k-group loop unroll
         for (int rep = 0; rep < 2; ++rep) {
-            run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1_bar", n, A, B, C, cnt, sms);
-            run<PolI8Dp4a, SrInt64, 1, true>("i64_dp4a_occ1_mbar", n, A, B, C, cnt, sms);
-            run<PolS16x2Min, SrTropF32, 1, false>("s16x2_occ1_bar", n, A, B, C, cnt, sms);
-            run<PolS16x2Min, SrTropF32, 1, true>("s16x2_occ1_mbar", n, A, B, C, cnt, sms);
+            run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_ufull_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aU8, SrInt64, 2, false>("i64_dp4a_u8_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aU4, SrInt64, 2, false>("i64_dp4a_u4_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aU2, SrInt64, 2, false>("i64_dp4a_u2_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_ufull_occ1", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aU4, SrInt64, 1, false>("i64_dp4a_u4_occ1", n, A, B, C, cnt, sms);
+            run<PolI8Dp4aU2, SrInt64, 1, false>("i64_dp4a_u2_occ1", n, A, B, C, cnt, sms);
+            run<PolS16x2Min, SrTropF32, 2, false>("s16x2_ufull_occ2", n, A, B, C, cnt, sms);
+            run<PolS16U8, SrTropF32, 2, false>("s16x2_u8_occ2", n, A, B, C, cnt, sms);
+            run<PolS16U4, SrTropF32, 2, false>("s16x2_u4_occ2", n, A, B, C, cnt, sms);
+            run<PolF32Pair, SrTropI32, 2, false>("f32pair_ufull_occ2", n, A, B, C, cnt, sms);
+            run<PolF32PairU4, SrTropI32, 2, false>("f32pair_u4_occ2", n, A, B, C, cnt, sms);
+            run<PolF32PairU2, SrTropI32, 2, false>("f32pair_u2_occ2", n, A, B, C, cnt, sms);
         }
         return 0;
     }
@@ -63,6 +89,7 @@ int main(int argc, char** argv) {
         return 0;
     }
     run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1", n, A, B, C, cnt, sms);
+    run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_occ1_store", n, A, B, C, cnt, sms, 1);
     run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_occ2", n, A, B, C, cnt, sms);
     run<PolS16x2Min, SrTropF32, 1, false>("minplus_s16x2_occ1", n, A, B, C, cnt, sms);
     run<PolS16x2Min, SrTropF32, 2, false>("minplus_s16x2_occ2", n, A, B, C, cnt, sms);
