@@ -134,6 +134,7 @@ struct PolI8Dp4a {
     using Tp = int; using Acc = int;            // Tp packs A[i][4q..4q+3] / B[4q..4q+3][j] as s8x4
     static constexpr int G = 1, KSTEP = 4, OUTS = 1, BK = 64;
     static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
+    static constexpr bool XSTAGE = true;   // half-rate pipe, spare issue slots: cross-stage prefetch
     static STARMM_DEV Acc init() { return 0; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __dp4a(a, b, c); }
 };
@@ -205,19 +206,22 @@ template <> struct Finish<PolS16x2Min, SrTropI32> {
 };
 
 namespace simt {
-constexpr int BM = 128, BNW = 128, STAGES = 3, THREADS = 256;   // BNW: B positions per tile row
+constexpr int BM = 128, BNW = 128, THREADS = 256;   // BNW: B positions per tile row
 template <class Pol> constexpr int bn() { return BNW * Pol::OUTS; }   // output columns per tile
 template <class Pol>
-constexpr int smem_bytes() {
-    return STAGES * (BM + BNW) * (Pol::BK / Pol::KSTEP) * Pol::G * (int)sizeof(typename Pol::Tp) +
-           16 * STAGES + 64;
+constexpr int stage_bytes() {
+    return (BM + BNW) * (Pol::BK / Pol::KSTEP) * Pol::G * (int)sizeof(typename Pol::Tp);
 }
+// Cross-stage fragment prefetch (see mainloop): policies that set XSTAGE, in their
+// one-CTA-per-SM build.  It runs a 4-stage ring (two stages resident at every barrier,
+// copies issued three ahead); the stage-local loop keeps 3.
+template <class P, class = void> struct HasXStage : std::false_type {};
+template <class P> struct HasXStage<P, std::void_t<decltype(P::XSTAGE)>> : std::bool_constant<P::XSTAGE> {};
+template <class Pol, int MINB> constexpr bool xstage() { return HasXStage<Pol>::value && MINB == 1; }
+template <class Pol, int MINB> constexpr int stages() { return xstage<Pol, MINB>() ? 4 : 3; }
+template <class Pol, int MINB>
+constexpr int smem_bytes() { return stages<Pol, MINB>() * stage_bytes<Pol>() + 64; }
 }  // namespace simt
-
-// Unroll factor of the k-group loop inside a stage: a policy may set KGU (the fully
-// unrolled dp4a stage is 1024 IDP.4A = 21 KB of SASS); default full.
-template <class P, class = void> struct KgUnroll { static constexpr int v = P::BK / P::KSTEP; };
-template <class P> struct KgUnroll<P, std::void_t<decltype(P::KGU)>> { static constexpr int v = P::KGU; };
 
 struct SimtParams {
     const void* Ap;   // packed [Kp/KSTEP][Mp][G]
@@ -236,11 +240,12 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     using T = typename Sr::T;
     if (p.pr.off()) return;
     constexpr int G = Pol::G, KSTEP = Pol::KSTEP, OUTS = Pol::OUTS, BK = Pol::BK;
+    constexpr int STAGES = stages<Pol, MINB>();
+    constexpr bool XS = xstage<Pol, MINB>();
     constexpr int BN = BNW * OUTS;                      // output columns per tile
     constexpr int VEC = 16 / (G * (int)sizeof(Tp));     // positions per 16-byte load
     constexpr int NQ = 8 / VEC;                         // 16-byte loads per operand per k-group
     constexpr int KG = BK / KSTEP;                      // k-groups per stage
-    constexpr int KGU = KgUnroll<Pol>::v;               // unroll of the k-group loop
     constexpr int A_STAGE = KG * BM * G;                // elements
     constexpr int B_STAGE = KG * BNW * G;
     constexpr int CHUNK = 16 / (int)sizeof(Tp);         // elements per cp.async
@@ -315,49 +320,116 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     Acc acc[8][8];
 
     // mainloop(): the nk k-stages begin() addressed, into acc.  Leaves the ring idle.
+    //
+    // Cross-stage ring (XS; the pipe-bound dp4a policy at one CTA per SM -- the issue-bound
+    // policies lose 1-5% to the extra registers and moves, profiles/r02z_sweep_xstage.jsonl,
+    // and keep the stage-local loop below): at the top of iteration kt the stages kt and kt+1 are resident and
+    // visible to every warp, and every warp has finished reading stage kt-1 -- so the
+    // copy of stage kt+STAGES-1 (into stage kt-1's slot) is issued first, and the operand
+    // fragments are double-buffered in registers ACROSS the stage boundary: the last
+    // k-group of stage kt prefetches the first k-group of stage kt+1, and the first term
+    // after the barrier issues without waiting on shared memory.  (With the fragments
+    // fetched inside each stage only, every stage began with the barrier, the address
+    // set-up and one LDS round trip in series: 6.8% of the in-loop samples of the dp4a
+    // kernel, profiles/r02y_dp4a_occ1_regions.txt.)  The barrier sits at the END of the
+    // iteration and waits for stage kt+2, copied at least one whole stage earlier.
     auto mainloop = [&](int nk) {
 #pragma unroll
         for (int i = 0; i < 8; ++i)
 #pragma unroll
             for (int j = 0; j < 8; ++j) acc[i][j] = Pol::init();
-        const Tp* as0 = As + ty * VEC * G;
-        const Tp* bs0 = Bs + tx * VEC * G;
-        int ld_slot = STAGES - 1, cp_slot = 0;
-        for (int kt = 0; kt < nk; ++kt) {
-            cp_async_wait<STAGES - 2>();
-            __syncthreads();
-            if (kt + STAGES - 1 < nk) load_next(ld_slot);
-            cp_async_commit();
-            const Tp* as = as0 + cp_slot * A_STAGE;
-            const Tp* bs = bs0 + cp_slot * B_STAGE;
-#pragma unroll KGU
-            for (int kg = 0; kg < KG; ++kg) {
-                // 8 row operands / 8 column operands, each G elements wide
-                Tp a[8 * G], b[8 * G];
+        if constexpr (XS) {
+            const Tp* as0 = As + ty * VEC * G;
+            const Tp* bs0 = Bs + tx * VEC * G;
+            Tp fa[2][8 * G], fb[2][8 * G];
+            auto fetch = [&](int buf, int slot, int kg) {
+                const Tp* as = as0 + slot * A_STAGE + kg * BM * G;
+                const Tp* bs = bs0 + slot * B_STAGE + kg * BNW * G;
 #pragma unroll
                 for (int q = 0; q < NQ; ++q) {
-                    *reinterpret_cast<int4*>(&a[q * VEC * G]) =
-                        *reinterpret_cast<const int4*>(as + kg * BM * G + q * 16 * VEC * G);
-                    *reinterpret_cast<int4*>(&b[q * VEC * G]) =
-                        *reinterpret_cast<const int4*>(bs + kg * BNW * G + q * 16 * VEC * G);
+                    *reinterpret_cast<int4*>(&fa[buf][q * VEC * G]) =
+                        *reinterpret_cast<const int4*>(as + q * 16 * VEC * G);
+                    *reinterpret_cast<int4*>(&fb[buf][q * VEC * G]) =
+                        *reinterpret_cast<const int4*>(bs + q * 16 * VEC * G);
                 }
+            };
+            static_assert(KG % 2 == 0, "fragment double buffer parity");
+            cp_async_wait<STAGES - 3>();
+            __syncthreads();
+            if (nk > 0) fetch(0, 0, 0);
+            int ld_slot = STAGES - 1, cp_slot = 0;
+            for (int kt = 0; kt < nk; ++kt) {
+                if (kt + STAGES - 1 < nk) load_next(ld_slot);
+                cp_async_commit();
+                const int nx_slot = cp_slot == STAGES - 1 ? 0 : cp_slot + 1;
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        if constexpr (G == 2) {
-                            Pol::term2(acc[i][j], make_float2(a[2 * i], a[2 * i + 1]),
-                                       make_float2(b[2 * j], b[2 * j + 1]));
-                        } else {
-                            Pol::term(acc[i][j], a[i], b[j]);
-                        }
+                for (int kg = 0; kg < KG; ++kg) {
+                    // 8 row operands / 8 column operands, each G elements wide
+                    if (kg + 1 < KG) {
+                        fetch((kg + 1) & 1, cp_slot, kg + 1);
+                    } else if (kt + 1 < nk) {
+                        fetch(0, nx_slot, 0);
                     }
+                    const Tp* a = fa[kg & 1];
+                    const Tp* b = fb[kg & 1];
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if constexpr (G == 2) {
+                                Pol::term2(acc[i][j], make_float2(a[2 * i], a[2 * i + 1]),
+                                           make_float2(b[2 * j], b[2 * j + 1]));
+                            } else {
+                                Pol::term(acc[i][j], a[i], b[j]);
+                            }
+                        }
+                }
+                cp_async_wait<STAGES - 3>();
+                __syncthreads();
+                ld_slot = ld_slot == STAGES - 1 ? 0 : ld_slot + 1;
+                cp_slot = nx_slot;
             }
-            ld_slot = ld_slot == STAGES - 1 ? 0 : ld_slot + 1;
-            cp_slot = cp_slot == STAGES - 1 ? 0 : cp_slot + 1;
+            cp_async_wait<0>();
+        } else {
+            const Tp* as0 = As + ty * VEC * G;
+            const Tp* bs0 = Bs + tx * VEC * G;
+            int ld_slot = STAGES - 1, cp_slot = 0;
+            for (int kt = 0; kt < nk; ++kt) {
+                cp_async_wait<STAGES - 2>();
+                __syncthreads();
+                if (kt + STAGES - 1 < nk) load_next(ld_slot);
+                cp_async_commit();
+                const Tp* as = as0 + cp_slot * A_STAGE;
+                const Tp* bs = bs0 + cp_slot * B_STAGE;
+#pragma unroll
+                for (int kg = 0; kg < KG; ++kg) {
+                    // 8 row operands / 8 column operands, each G elements wide
+                    Tp a[8 * G], b[8 * G];
+#pragma unroll
+                    for (int q = 0; q < NQ; ++q) {
+                        *reinterpret_cast<int4*>(&a[q * VEC * G]) =
+                            *reinterpret_cast<const int4*>(as + kg * BM * G + q * 16 * VEC * G);
+                        *reinterpret_cast<int4*>(&b[q * VEC * G]) =
+                            *reinterpret_cast<const int4*>(bs + kg * BNW * G + q * 16 * VEC * G);
+                    }
+#pragma unroll
+                    for (int i = 0; i < 8; ++i)
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if constexpr (G == 2) {
+                                Pol::term2(acc[i][j], make_float2(a[2 * i], a[2 * i + 1]),
+                                           make_float2(b[2 * j], b[2 * j + 1]));
+                            } else {
+                                Pol::term(acc[i][j], a[i], b[j]);
+                            }
+                        }
+                }
+                ld_slot = ld_slot == STAGES - 1 ? 0 : ld_slot + 1;
+                cp_slot = cp_slot == STAGES - 1 ? 0 : cp_slot + 1;
+            }
+            cp_async_wait<0>();
+            __syncthreads();
         }
-        cp_async_wait<0>();
-        __syncthreads();
     };
 
     // finish(): acc -> C under write-back protocol `mode`.  Exclusive folds / stores of a

@@ -29,11 +29,11 @@ inline int sl_device() {
 
 template <class Pol, class Sr>
 int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
-    constexpr int smem = simt::smem_bytes<Pol>();
     const int dev = sl_device();
     if constexpr (has_occ1_build<Pol>() && Pol::OCC > 1) {
         if (grid <= sms) {
             auto k1 = simt_mm_kernel<Pol, Sr, 1>;
+            constexpr int smem = simt::smem_bytes<Pol, 1>();
             static bool attr1[SL_MAX_DEV] = {};
             if (!attr1[dev]) {
                 SL_CK(cudaFuncSetAttribute(k1, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -45,6 +45,7 @@ int launch_simt(const SimtParams& p, int grid, int sms, cudaStream_t s) {
         }
     }
     auto kern = simt_mm_kernel<Pol, Sr, Pol::OCC>;
+    constexpr int smem = simt::smem_bytes<Pol, Pol::OCC>();
     static bool attr_done[SL_MAX_DEV] = {};
     if (!attr_done[dev]) {
         SL_CK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));

@@ -831,13 +831,17 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
                 ++smax;
         double best = 0;
         int best_occ = per_sm, best_s = 0;
+        const bool occ1_build = path == PATH_SIMT_I64_DP4A || path == PATH_SIMT_F32_PAIR ||
+                                path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER ||
+                                path == PATH_SIMT_F32_S16X2 || path == PATH_SIMT_I32_S16X2 ||
+                                path == PATH_SIMT_F64T_S16X2;                // has_occ1_build
+        // (the dp4a policy's one-CTA build runs the cross-stage fragment ring and beats its
+        // own two-CTA build: 137.2 vs 132.1 Tops/s at n = 8192, tools/sweep_simt.cu)
+        const double rate1 = path == PATH_SIMT_I64_DP4A ? 1.03 : (occ1_build ? 0.97 : 0.89);
+        // rate of ONE CTA, in units of a full SM running per_sm co-resident CTAs
+        auto cta_rate = [&](int occ) { return occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ; };
         for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
-            const bool occ1_build = path == PATH_SIMT_I64_DP4A || path == PATH_SIMT_F32_PAIR ||
-                                    path == PATH_SIMT_I32_CARRIER || path == PATH_SIMT_F64T_CARRIER ||
-                                    path == PATH_SIMT_F32_S16X2 || path == PATH_SIMT_I32_S16X2 ||
-                                    path == PATH_SIMT_F64T_S16X2;                // has_occ1_build
-            const double rate1 = occ1_build ? 0.97 : 0.89;
-            const double rate = occ == 1 ? (per_sm == 1 ? 1.0 : rate1) : 1.0 / occ;
+            const double rate = cta_rate(occ);
             for (int sl = 0; sl <= smax; ++sl) {
                 double waves = std::ceil((double)(tiles << sl) / ((double)P->sms * occ));
                 if (is_dmma && dmma_cluster_mode(P, 1 << sl)) {   // one tile per cluster at a time
@@ -859,11 +863,17 @@ int plan_geometry(const starmm_plan* P, int path, Geom& G) {
         const char* benv = getenv("STARMM_NO_BALANCED");
         const bool bal_sr = simt_path ? (P->sr == STARMM_SR_INT64 || P->sr == STARMM_SR_TROPICAL_I32)
                                       : is_dmma;
-        if ((simt_path || is_dmma) && may_split && (P->algo == STARMM_TAR || P->algo == STARMM_STAR) &&
+        // STAR merges by atomic-madd only above its switch depth (classic.py:280-296): with
+        // p workers too few to have a TAR level (switch_depth(p) == 0) it is pure SAR.
+        const bool bal_algo = P->algo == STARMM_TAR ||
+                              (P->algo == STARMM_STAR && switch_depth(P->workers) >= 1);
+        if ((simt_path || is_dmma) && may_split && bal_algo &&
             bal_sr && P->remote_parts == 0 && !(benv && benv[0] == '1')) {
-            const double Gw = (double)P->sms * per_sm;
-            const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw * per_sm;
-            if (c < 0.97 * best) { balanced = true; best_occ = per_sm; best_s = 0; }
+            for (int occ = per_sm; occ >= (is_dmma ? per_sm : 1); --occ) {
+                const double Gw = (double)P->sms * occ;
+                const double c = ((double)tiles * (kst + 4.5) + Gw * (4.5 + 2.0)) / Gw / cta_rate(occ);
+                if (c < 0.97 * best) { balanced = true; best = c / 0.97; best_occ = occ; best_s = 0; }
+            }
         }
         per_sm = best_occ;
         s_log2 = best_s;
@@ -1319,6 +1329,7 @@ int launch_candidate(Exec& x, const Geom& G, void* C, long long ldc, const void*
     if (cluster) ci.workers = std::min<long long>(tiles, dmma_cluster_slots(S)) * S;
     ci.cluster = cluster ? S : 0;
     ci.balanced_workers = G.balanced ? std::min<long long>(G.ntasks * G.g.kstages, (long long)P->sms * G.per_sm) : 0;
+    if (G.balanced) ci.workers = ci.balanced_workers;    // every CTA of the grid owns a slice
     if (!cluster && S > 1 && (P->algo == STARMM_SAR || P->algo == STARMM_STAR) && G.tar_levels < s_log2)
         ci.pair_count = tiles * (S / 2);
     return STARMM_OK;

@@ -1,7 +1,7 @@
 // Variant sweep for the CUDA-core semiring tile kernel (csrc/simt_kernel.cuh):
 // inner-term policy x co-resident CTAs per SM, CO2 FOLD write-back, packed
 // operands of zeros (throughput only), CUDA events, 1 warm-up + 3 timed.
-//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/sweep_simt tools/sweep_simt.cu
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 --expt-relaxed-constexpr -o tools/sweep_simt_bin tools/sweep_simt.cu
 #include <cstdio>
 #include "../paper_1911_05328_b200/csrc/simt_kernel.cuh"
 using namespace starmm;
@@ -17,7 +17,7 @@ void run(const char* name, int n, void* Ap, void* Bp, void* C, unsigned long lon
     w.mode_base = 0; w.init_identity = store; w.C = C; w.ldc = n; w.M = n; w.N = n; w.counters = cnt;
     auto kern = simt_mm_kernel<Pol, Sr, MINB>;   // (MB: the mbarrier ring variant was removed in round 2,
                                                   //  -1..-6%: profiles/r01n_sweep_simt_occ1_mbarrier.jsonl)
-    constexpr int smem = simt::smem_bytes<Pol>();
+    constexpr int smem = simt::smem_bytes<Pol, MINB>();
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     int occ = 0;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, simt::THREADS, smem);
@@ -39,22 +39,6 @@ struct PolI8Dp4aBK32 : PolI8Dp4a { static constexpr int BK = 32; };
 template <> struct starmm::Finish<PolI8Dp4aBK128, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 template <> struct starmm::Finish<PolI8Dp4aBK32, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 
-// k-group loop unroll variants (the fully unrolled dp4a stage is 21 KB of SASS)
-struct PolI8Dp4aU2 : PolI8Dp4a { static constexpr int KGU = 2; };
-struct PolI8Dp4aU4 : PolI8Dp4a { static constexpr int KGU = 4; };
-struct PolI8Dp4aU8 : PolI8Dp4a { static constexpr int KGU = 8; };
-template <> struct starmm::Finish<PolI8Dp4aU2, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
-template <> struct starmm::Finish<PolI8Dp4aU4, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
-template <> struct starmm::Finish<PolI8Dp4aU8, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
-struct PolS16U4 : PolS16x2Min { static constexpr int KGU = 4; };
-struct PolS16U8 : PolS16x2Min { static constexpr int KGU = 8; };
-template <> struct starmm::Finish<PolS16U4, SrTropF32> : starmm::Finish<PolS16x2Min, SrTropF32> {};
-template <> struct starmm::Finish<PolS16U8, SrTropF32> : starmm::Finish<PolS16x2Min, SrTropF32> {};
-struct PolF32PairU2 : PolF32Pair { static constexpr int KGU = 2; };
-struct PolF32PairU4 : PolF32Pair { static constexpr int KGU = 4; };
-template <> struct starmm::Finish<PolF32PairU2, SrTropI32> : starmm::Finish<PolF32Pair, SrTropI32> {};
-template <> struct starmm::Finish<PolF32PairU4, SrTropI32> : starmm::Finish<PolF32Pair, SrTropI32> {};
-
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 8192;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -62,24 +46,8 @@ int main(int argc, char** argv) {
     size_t bytes = (size_t)n * n * 8;
     cudaMalloc(&A, bytes); cudaMalloc(&B, bytes); cudaMalloc(&C, bytes); cudaMalloc(&cnt, 512);
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
-    if (argc > 2 && argv[2][0] == 'u') {   // k-group loop unroll
-        for (int rep = 0; rep < 2; ++rep) {
-            run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_ufull_occ2", n, A, B, C, cnt, sms);
-            run<PolI8Dp4aU8, SrInt64, 2, false>("i64_dp4a_u8_occ2", n, A, B, C, cnt, sms);
-            run<PolI8Dp4aU4, SrInt64, 2, false>("i64_dp4a_u4_occ2", n, A, B, C, cnt, sms);
-            run<PolI8Dp4aU2, SrInt64, 2, false>("i64_dp4a_u2_occ2", n, A, B, C, cnt, sms);
-            run<PolI8Dp4a, SrInt64, 1, false>("i64_dp4a_ufull_occ1", n, A, B, C, cnt, sms);
-            run<PolI8Dp4aU4, SrInt64, 1, false>("i64_dp4a_u4_occ1", n, A, B, C, cnt, sms);
-            run<PolI8Dp4aU2, SrInt64, 1, false>("i64_dp4a_u2_occ1", n, A, B, C, cnt, sms);
-            run<PolS16x2Min, SrTropF32, 2, false>("s16x2_ufull_occ2", n, A, B, C, cnt, sms);
-            run<PolS16U8, SrTropF32, 2, false>("s16x2_u8_occ2", n, A, B, C, cnt, sms);
-            run<PolS16U4, SrTropF32, 2, false>("s16x2_u4_occ2", n, A, B, C, cnt, sms);
-            run<PolF32Pair, SrTropI32, 2, false>("f32pair_ufull_occ2", n, A, B, C, cnt, sms);
-            run<PolF32PairU4, SrTropI32, 2, false>("f32pair_u4_occ2", n, A, B, C, cnt, sms);
-            run<PolF32PairU2, SrTropI32, 2, false>("f32pair_u2_occ2", n, A, B, C, cnt, sms);
-        }
-        return 0;
-    }
+    // (round 2: k-group unroll 2/4/8 and BK 128/256 at a 16-group unroll were swept on the
+    //  stage-local fragment loop -- profiles/r02y_sweep_unroll_*.jsonl -- full unroll won)
     if (argc > 2 && argv[2][0] == 'd') {   // dp4a k-stage depth
         for (int rep = 0; rep < 2; ++rep) {
             run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_bk64_occ2", n, A, B, C, cnt, sms);
