@@ -589,3 +589,64 @@ def test_int64_radix256_through_the_public_api_and_guard():
             O.gemm_fold(O.SR_INT64, want, A, B, par=True)
             assert same_bits(C.numpy(), want), path
             assert ex.last_stats["path_name"] == path
+
+
+# ---- vectorised exclusive epilogue of the CUDA-core tile kernel ----------------------
+# (writeback.cuh epilogue_row_vec: 16-byte pieces, even/odd lanes swap pieces so a warp
+# access covers whole sectors; taken for full tiles whose rows are 16-byte aligned)
+SR_IDS = O.SR_BY_NAME
+EPI_CASES = [  # (semiring, value range hi, expected kernel path prefix)
+    ("int", 17, "simt_i64_dp4a"),            # 32-byte fragments (4 x int64): paired pieces
+    ("int", 1000, "simt_i64_narrow_i32"),        # 32-byte fragments from int32 accumulators
+    ("int", 2 ** 40, "simt_i64"),            # 16-byte fragments (2 x int64)
+    ("tropical_f32", 100, "simt_f32_s16x2_viaddmnmx"),     # 8 x float = 32 bytes, two outputs per lane-op
+    ("tropical_f32", 10 ** 5, "simt_f32_fadd2_fmnmx3"),  # 2 x float = 8-byte fragments
+    ("tropical_i32", 100, "simt_i32_s16x2_viaddmnmx"),
+    ("tropical_i32", 10 ** 5, "simt_i32_via_f32_carrier"),
+    ("tropical_i32", 2 ** 26, "simt_i32_viaddmnmx"),  # 4 x int32 = 16 bytes
+    ("tropical", 100, "simt_f64trop_s16x2_viaddmnmx"),        # 8 x double = 64-byte fragments (4 pieces)
+    ("tropical", 10 ** 5, "simt_f64trop_via_f32_carrier"),   # 2 x double = 16 bytes
+]
+
+
+@pytest.mark.parametrize("sid,hi,path", EPI_CASES)
+@pytest.mark.parametrize("algo,store", [("star", False), ("star", True), ("co3", False)])
+def test_vector_epilogue_windows(sid, hi, path, algo, store):
+    """C as a column window of a wider buffer, at offsets that leave its rows 16-byte
+    aligned (vector epilogue, ld != cols) and misaligned (generic element epilogue), folded
+    and overwritten (STARMM_F_INIT_IDENTITY), and co3 with a forced 2-way split (slice 1
+    stores into the workspace, whose merge folds into C).  n = 640: five full tile rows;
+    the two-outputs-per-lane policies (256-column tiles) end on a ragged tile column.  The
+    bytes outside the window must not change."""
+    s = sm.get_semiring(sid)
+    n, pad = 640, 24
+    rng = np.random.default_rng(hi % 1000 + n)
+    gen = lambda shape: rng.integers(0 if sid != "int" else -hi + 1, hi, shape).astype(s.dtype)  # noqa: E731
+    A, B = gen((n, n)), gen((n, n))
+    es = np.dtype(s.dtype).itemsize
+    for off in (16 // es, 1, 0):                       # aligned window, misaligned, no offset
+        Cb = gen((n, n + pad))
+        want = np.ascontiguousarray(Cb[:, off:off + n]).copy()
+        Cd = torch.from_numpy(Cb).cuda()
+        Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        plan = _lib.Plan(s.sr_id, algo, "pooled", n, n, n, 64, 148, 1 if algo == "co3" else -1, 0,
+                         _lib.F_ALLOW_NONPOW2 | (_lib.F_INIT_IDENTITY if store else 0))
+        plan.execute(Cd.data_ptr() + off * es, n + pad, Ad.data_ptr(), n, Bd.data_ptr(), n,
+                     torch.cuda.current_stream().cuda_stream)
+        st = plan.stats()
+        plan.close()
+        assert st["path_name"] == path, st["path_name"]
+        if store:
+            want = _identity_like(sid, want)
+        O.gemm_fold(SR_IDS[sid], want, A, B, par=True)
+        got = Cd.cpu().numpy()
+        assert same_bits(got[:, off:off + n], want), (off, diff_count(got[:, off:off + n], want))
+        assert same_bits(got[:, :off], Cb[:, :off]) and same_bits(got[:, off + n:], Cb[:, off + n:]), off
+
+
+def _identity_like(sid, x):
+    if sid == "int":
+        return np.zeros_like(x)
+    if sid == "tropical_i32":
+        return np.full_like(x, O.I32_INF)
+    return np.full_like(x, np.inf)
