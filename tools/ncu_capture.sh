@@ -13,16 +13,19 @@ CFGS=${@:-4 3 5 2}
 for c in $CFGS; do
   base=${c:0:1}; X=""; F=""
   [ "$base" = "5" ] && X="--size 16384"
-  K=simt_mm; [ "$base" = "4" ] && K=dmma
+  # the tile kernel by its demangled name (policy included): a plan also launches
+  # predicated-off fallback kernels of other policies, which -k regex:simt_mm would catch
+  K=simt_mm; [ "$base" = "4" ] && K=dmma_fp64
+  [ "$base" = "2" ] && K=PolI8Dp4a; [ "$base" = "3" ] && K=PolS16x2Min; [ "$base" = "5" ] && K=PolF32Pair
   case $c in 2t) F="--int-tensor"; K=tcg_kernel;; 4e) F="--fp64-emu"; K=tcg_kernel;;
-             5f) X="";; 2g|3g|5g) F="--no-fastpath";; esac
+             5f) X="";; 2g) F="--no-fastpath"; K="PolI64,";; 3g) F="--no-fastpath"; K=PolF32Pair;; 5g) F="--no-fastpath"; K=PolI32Sat;; esac
   B="python bench.py --steps 2 --warmup 1 --config $base $X $F --no-opt-in"
   $B > gpurun_out/${TAG}_plain_c$c.json 2> gpurun_out/${TAG}_plain_c$c.err || exit 1
   ncu --metrics gpu__time_duration.sum --clock-control none --csv \
       --log-file gpurun_out/${TAG}_launches_c$c.csv $B > /dev/null 2>&1 || exit 2
   B2="$B --no-e2e --no-cpu-baseline"
   $B2 > /dev/null 2>&1 || exit 3
-  ncu --set full --clock-control none --import-source on -k regex:$K -s 1 -c 1 \
+  ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k regex:"$K" -s 1 -c 1 \
       -o gpurun_out/${TAG}_prof_c$c $B2 > gpurun_out/${TAG}_ncu_c$c.log 2>&1 || exit 4
   # raw page as CSV (what tools/summarize_ncu.py reads); the 12-16 MB report only with KEEP_REP=1
   ncu -i gpurun_out/${TAG}_prof_c$c.ncu-rep --page raw --csv > gpurun_out/${TAG}_prof_c$c.raw.csv 2>/dev/null
