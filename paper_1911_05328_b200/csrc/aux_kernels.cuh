@@ -305,10 +305,16 @@ __global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr:
 }
 
 // launch shape for the 2-D elementwise kernels (x: 256-column blocks, y: rows, both
-// grid-strided): about 16 CTAs per SM in total, so each thread handles several rows
+// grid-strided): at most one resident wave of CTAs (8 x 256 threads per SM), and the
+// row dimension cut so that every CTA runs the same number of grid-stride iterations
+// (1024 rows over 296 CTA-rows ran 3.46 -> 4 iterations on the slowest CTA: the int8
+// B packer spent 14% of its time in that tail).
 inline dim3 grid2d(long long rows, long long cols) {
     const long long bx = std::max<long long>(1, std::min<long long>((cols + 255) / 256, 64));
-    const long long by = std::max<long long>(1, std::min<long long>(rows, (148LL * 16 + bx - 1) / bx));
+    const long long cap = std::max<long long>(1, (148LL * 8) / bx);
+    const long long by0 = std::max<long long>(1, std::min<long long>(rows, cap));
+    const long long iters = (rows + by0 - 1) / by0;
+    const long long by = std::max<long long>(1, (rows + iters - 1) / std::max<long long>(1, iters));
     return dim3((unsigned)bx, (unsigned)by);
 }
 

@@ -29,9 +29,13 @@
 //                output columns per lane-op.
 //
 // CTA tile 128 x (128*OUTS), 256 threads, 8x8 accumulators per thread (each
-// accumulator holds OUTS outputs), k-stage Pol::BK, 3-deep cp.async ring.  Warps
+// accumulator holds OUTS outputs), k-stage Pol::BK, cp.async ring of 3 stages (4 for
+// the cross-stage fragment ring of the XSTAGE policies, see mainloop).  Warps
 // are 4 (rows) x 8 (cols) threads so A reads broadcast across 8 lanes and B
-// reads across 4.
+// reads across 4.  The kernel is persistent: begin() / mainloop() / finish() per
+// leaf task, the next task's first k-stages in flight before the write-back, and
+// exclusive write-backs of full aligned tiles through the vectorised epilogue
+// (writeback.cuh epilogue_row_vec).
 #pragma once
 #include <type_traits>
 #include "common.cuh"

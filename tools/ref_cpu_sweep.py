@@ -7,6 +7,9 @@ rather than burnt.  Writes profiles/r02_ref_cpu_sweep.json (largest n completed 
 semiring and W, Gop/s at every n).
 
   python tools/ref_cpu_sweep.py [--cap 600] [--semirings float,int,tropical]
+  python tools/ref_cpu_sweep.py --native-matmul     # the reference's own leaf kernel,
+        Semiring.matmul (semiring.py:92-94, numba _mm_*), single-threaded, n = 512..2048
+        -> profiles/r02_ref_native_matmul.json
 """
 import argparse
 import json
@@ -38,6 +41,43 @@ print(json.dumps({"seconds": time.perf_counter() - t0}))
 
 CID_OF = {"float": 4, "int": 2, "tropical": 5}
 
+NATIVE = r"""
+import os, sys, time, json
+sys.dont_write_bytecode = True
+sys.path.insert(0, os.path.join(%(repo)r, "baseline", "_ref"))
+sys.path.insert(0, %(repo)r)
+import numpy as np
+import starmm as ref
+from bench_configs import make_inputs, to_reference
+cid, n = %(cid)d, %(n)d
+s = ref.get_semiring(%(sid)r)
+A, B, C = make_inputs(cid, n)
+A = to_reference(cid, A); B = A if B is A else to_reference(cid, B)
+s.matmul(A[:64, :64].copy(), B[:64, :64].copy())          # JIT
+t0 = time.perf_counter()
+s.matmul(A, B)
+print(json.dumps({"seconds": time.perf_counter() - t0}))
+"""
+
+
+def native_matmul(out_name):
+    env = dict(os.environ, NUMBA_CACHE_DIR="/tmp/starmm_ref_numba_cache", NUMBA_NUM_THREADS="1",
+               OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    out = {"host_cores": os.cpu_count(), "threads": 1, "rows": [],
+           "how": "reference Semiring.matmul (baseline/_ref, unmodified; numba leaf kernels / numpy "
+                  "matmul as the reference chooses), one call on the BASELINE config distributions"}
+    for sid in ("float", "int", "tropical"):
+        for n in (512, 1024, 2048):
+            code = NATIVE % {"repo": REPO, "cid": CID_OF[sid], "n": n, "sid": sid}
+            p = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, timeout=900, env=env)
+            if p.returncode != 0:
+                out["rows"].append({"semiring": sid, "n": n, "status": "error", "stderr": p.stderr[-300:]})
+                continue
+            sec = json.loads(p.stdout.strip().splitlines()[-1])["seconds"]
+            out["rows"].append({"semiring": sid, "n": n, "seconds": sec, "gops": 2.0 * n ** 3 / sec / 1e9})
+            print(out["rows"][-1], flush=True)
+    json.dump(out, open(os.path.join(REPO, "profiles", out_name), "w"), indent=1)
+
 
 def run_one(sid, n, W, b, cap):
     code = CHILD % {"repo": REPO, "cid": CID_OF[sid], "n": n, "W": W, "b": b, "sid": sid}
@@ -60,7 +100,11 @@ def main():
     ap.add_argument("--semirings", default="float,int,tropical")
     ap.add_argument("--workers", default="")
     ap.add_argument("--out", default="r02_ref_cpu_sweep.json")
+    ap.add_argument("--native-matmul", action="store_true")
     args = ap.parse_args()
+    if args.native_matmul:
+        native_matmul("r02_ref_native_matmul.json")
+        return
     cores = os.cpu_count() or 1
     Ws = [int(x) for x in args.workers.split(",")] if args.workers else sorted({1, cores})
     out = {"host_cores": cores, "cap_seconds": args.cap, "series": [], "largest_n": {},
