@@ -650,3 +650,36 @@ def _identity_like(sid, x):
     if sid == "tropical_i32":
         return np.full_like(x, O.I32_INF)
     return np.full_like(x, np.inf)
+
+
+# ---- the k-stage ring at its edges ----------------------------------------------------
+@pytest.mark.parametrize("sid,hi,path", [("int", 17, "simt_i64_dp4a"),                 # cross-stage ring, 4 stages
+                                         ("tropical_i32", 100, "simt_i32_s16x2_viaddmnmx"),
+                                         ("tropical_i32", 10 ** 5, "simt_i32_via_f32_carrier")])
+@pytest.mark.parametrize("algo", ["co2", "tar"])
+def test_stage_ring_short_and_ragged_k(sid, hi, path, algo):
+    """Rectangular products whose k extent is 1 .. 7 k-stages of the policy (and not a
+    multiple of the stage), on 3 x 3 output tiles: the copy ring's prologue, its
+    cross-stage fragment prefetch and the early start of the next tile see every short
+    case; tar adds forced and balanced k-slices (pieces of 1 .. few stages).  Each case
+    runs three times (a race would be timing dependent) and must equal the oracle."""
+    s = sm.get_semiring(sid)
+    m = n = 384
+    rng = np.random.default_rng(hi % 97 + len(algo))
+    for k in (64, 96, 128, 192, 200, 256, 320, 448):
+        A = rng.integers(0 if sid != "int" else -hi + 1, hi, (m, k)).astype(s.dtype)
+        B = rng.integers(0 if sid != "int" else -hi + 1, hi, (k, n)).astype(s.dtype)
+        C0 = rng.integers(0, hi, (m, n)).astype(s.dtype)
+        want = C0.copy()
+        O.gemm_fold(SR_IDS[sid], want, A, B, par=True)
+        Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+        for ks in ((-1,) if algo == "co2" else (-1, 1)):
+            plan = _lib.Plan(s.sr_id, algo, "pooled", m, n, k, 32, 148, ks, 0, _lib.F_ALLOW_NONPOW2)
+            for rep in range(3):
+                Cd = torch.from_numpy(C0.copy()).cuda()
+                plan.execute(Cd.data_ptr(), n, Ad.data_ptr(), k, Bd.data_ptr(), n,
+                             torch.cuda.current_stream().cuda_stream)
+                got = Cd.cpu().numpy()
+                assert same_bits(got, want), (k, ks, rep, diff_count(got, want))
+            assert plan.stats()["path_name"] == path, plan.stats()["path_name"]
+            plan.close()
