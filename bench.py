@@ -481,7 +481,9 @@ def main():
     clocks = clk.summary()
     pk = peaks(clocks["sm_max_mhz"] or 1965.0)
     roof, mix = roofline(pk, st["path_name"], 2.0 * dmm.m * dmm.nn * dmm.k, kern_s)
-    roof["traffic"] = _ncu_traffic(cid, st["path_name"])
+    # the committed ncu capture is of the full-size single-GPU launch: no figure for a
+    # sharded (N > 1) or size-overridden launch
+    roof["traffic"] = _ncu_traffic(cid, st["path_name"]) if (world == 1 and args.size is None) else None
     roof["kernel_share_of_step"] = kern_s / t_step
 
     # ---- the opt-in tensor-core path of this config, measured as a secondary line ----
