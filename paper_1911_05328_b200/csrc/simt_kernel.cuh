@@ -82,6 +82,9 @@ struct PolF64Min {
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static constexpr int OCC = 1;   // CTAs per SM (tools/sweep_simt.cu)
+    // FP64-pipe bound (2 FP64 instructions per term), spare issue slots: the cross-stage
+    // fragment ring gives +8..11% (profiles/r02z_sweep_xs_general.jsonl)
+    static constexpr bool XSTAGE = true;
     static STARMM_DEV Acc init() { return __longlong_as_double(0x7ff0000000000000ULL); }
     // the reference's own rule (semiring.py:56-58): v = a + b; if v < out: out = v --
     // a NaN candidate never wins, and -0.0 does not replace +0.0 (fmin would, and costs
@@ -441,7 +444,10 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
     // (writeback.cuh epilogue_row_vec: whole 32-byte sectors per warp access); ragged
     // edges, unaligned targets and the k-split protocols take the generic one.
     auto finish = [&](int tm, int tn, int s, int tile, int mode, int pair_seen) {
-        if (mode == WB_STORE || mode == WB_FOLD) {
+        // (not for the policies with 64-bit accumulators -- general int64, general float64
+        // (min,+): their 255-register one-CTA builds pay 3% in the main loop for the extra
+        // epilogue code, and their tiles are ~10x longer, profiles/r02z_sweep_xs_general.jsonl)
+        if constexpr (sizeof(Acc) < 8) if (mode == WB_STORE || mode == WB_FOLD) {
             T* dst = reinterpret_cast<T*>(p.w.C);
             long long ld = p.w.ldc;
             if (mode == WB_STORE && p.w.mode_base == 1 && s > 0) {   // co3: slice s>0 -> workspace D_s
@@ -456,11 +462,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                 constexpr int W = VEC * OUTS;        // consecutive output columns per fragment
                 // rows per batch (all loads of a batch are issued before its stores): the
                 // one-CTA-per-SM builds have the registers for two rows in flight
-#ifdef STARMM_EPI_ROWS
-                constexpr int RB = STARMM_EPI_ROWS;
-#else
                 constexpr int RB = (MINB == 1 && W * (int)sizeof(T) <= 32) ? 2 : 1;
-#endif
                 const bool odd = (lane & 1) != 0;
 #pragma unroll
                 for (int ib = 0; ib < 8; ib += RB) {

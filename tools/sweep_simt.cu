@@ -39,6 +39,14 @@ struct PolI8Dp4aBK32 : PolI8Dp4a { static constexpr int BK = 32; };
 template <> struct starmm::Finish<PolI8Dp4aBK128, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 template <> struct starmm::Finish<PolI8Dp4aBK32, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 
+// cross-stage fragment ring on the one-CTA-per-SM general policies
+struct PolF64MinXS : PolF64Min { static constexpr bool XSTAGE = true; };
+struct PolI64XS : PolI64 { static constexpr bool XSTAGE = true; };
+struct PolI32SatXS : PolI32Sat { static constexpr bool XSTAGE = true; };
+template <> struct starmm::Finish<PolF64MinXS, SrTropF64> : starmm::Finish<PolF64Min, SrTropF64> {};
+template <> struct starmm::Finish<PolI64XS, SrInt64> : starmm::Finish<PolI64, SrInt64> {};
+template <> struct starmm::Finish<PolI32SatXS, SrTropI32> : starmm::Finish<PolI32Sat, SrTropI32> {};
+
 int main(int argc, char** argv) {
     int n = argc > 1 ? atoi(argv[1]) : 8192;
     int sms; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
@@ -48,6 +56,17 @@ int main(int argc, char** argv) {
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
     // (round 2: k-group unroll 2/4/8 and BK 128/256 at a 16-group unroll were swept on the
     //  stage-local fragment loop -- profiles/r02y_sweep_unroll_*.jsonl -- full unroll won)
+    if (argc > 2 && argv[2][0] == 'x') {   // cross-stage ring on the general one-CTA policies
+        for (int rep = 0; rep < 2; ++rep) {
+            run<PolF64Min, SrTropF64, 1, false>("f64min_occ1", n, A, B, C, cnt, sms);
+            run<PolF64MinXS, SrTropF64, 1, false>("f64min_xs_occ1", n, A, B, C, cnt, sms);
+            run<PolI64, SrInt64, 1, false>("i64_occ1", n, A, B, C, cnt, sms);
+            run<PolI64XS, SrInt64, 1, false>("i64_xs_occ1", n, A, B, C, cnt, sms);
+            run<PolI32Sat, SrTropI32, 1, false>("i32sat_occ1", n, A, B, C, cnt, sms);
+            run<PolI32SatXS, SrTropI32, 1, false>("i32sat_xs_occ1", n, A, B, C, cnt, sms);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'd') {   // dp4a k-stage depth
         for (int rep = 0; rep < 2; ++rep) {
             run<PolI8Dp4a, SrInt64, 2, false>("i64_dp4a_bk64_occ2", n, A, B, C, cnt, sms);
