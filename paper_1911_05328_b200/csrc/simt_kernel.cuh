@@ -307,23 +307,6 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         }
     };
 
-    // An exclusive fold reads its C tile once, at the end: ask L2 for it now, so the
-    // epilogue's loads (issued by every CTA of a wave at the same moment) do not wait
-    // on DRAM.  One 128-byte line per thread and pass.
-    auto prefetch_c = [&](int tm, int tn) {
-        constexpr int LINES_PER_ROW = BN * (int)sizeof(T) / 128;
-        static_assert(LINES_PER_ROW >= 1 && THREADS % LINES_PER_ROW == 0, "C tile prefetch shape");
-        constexpr int ROWS_PER_PASS = THREADS / LINES_PER_ROW;
-        const T* C = reinterpret_cast<const T*>(p.w.C);
-        const long long gc = (long long)tn * BN + (long long)(tid % LINES_PER_ROW) * (128 / (int)sizeof(T));
-        if (gc >= p.w.N) return;
-#pragma unroll
-        for (int r = tid / LINES_PER_ROW; r < BM; r += ROWS_PER_PASS) {
-            const long long gr = (long long)tm * BM + r;
-            if (gr < p.w.M) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + gr * p.w.ldc + gc));
-        }
-    };
-
     Acc acc[8][8];
 
     // mainloop(): the nk k-stages begin() addressed, into acc.  Leaves the ring idle.
@@ -528,7 +511,6 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
                 mode = p.w.init_identity ? WB_STORE : WB_FOLD;
             leaf_enter(p.w);
             begin(tm, tn, ks, (int)(ke - ks));
-            if (mode == WB_FOLD) prefetch_c(tm, tn);
             mainloop((int)(ke - ks));
             finish(tm, tn, 0, tile, mode, PAIR_EMPTY);
             leaf_exit(p.w);
@@ -553,7 +535,6 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         if (mode == WB_PAIR) pair_seen = pair_arrive(p.w, g, tile, s, smem_word);
         leaf_enter(p.w);
         if (!begun) begin(tm, tn, (long long)s * nk, nk);
-        if (mode == WB_FOLD) prefetch_c(tm, tn);
         mainloop(nk);
         const int t2 = t + gridDim.x;
         int tm2 = 0, tn2 = 0, s2 = 0, tile2 = 0, mode2 = 0;
