@@ -99,6 +99,9 @@ struct PolI32Vmin {
     static constexpr int G = 1;
     static constexpr int KSTEP = 1, OUTS = 1, BK = 16;
     static constexpr int OCC = 2;   // CTAs per SM (tools/sweep_simt.cu)
+    // generic element epilogue: with the vectorised one compiled in, this 128-register
+    // build lost 1.8% in the main loop (34.08 vs 34.58 Tops/s raw at n = 8192)
+    static constexpr bool NO_VEC_EPI = true;
     static STARMM_DEV Acc init() { return 0x7fffffff; }
     static STARMM_DEV void term(Acc& c, Tp a, Tp b) { c = __viaddmin_s32(a, b, c); }
 };
@@ -224,6 +227,8 @@ constexpr int stage_bytes() {
 // copies issued three ahead); the stage-local loop keeps 3.
 template <class P, class = void> struct HasXStage : std::false_type {};
 template <class P> struct HasXStage<P, std::void_t<decltype(P::XSTAGE)>> : std::bool_constant<P::XSTAGE> {};
+template <class P, class = void> struct NoVecEpi : std::false_type {};
+template <class P> struct NoVecEpi<P, std::void_t<decltype(P::NO_VEC_EPI)>> : std::bool_constant<P::NO_VEC_EPI> {};
 template <class Pol, int MINB> constexpr bool xstage() { return HasXStage<Pol>::value && MINB == 1; }
 template <class Pol, int MINB> constexpr int stages() { return xstage<Pol, MINB>() ? 4 : 3; }
 template <class Pol, int MINB>
@@ -430,7 +435,7 @@ __global__ void __launch_bounds__(simt::THREADS, MINB) simt_mm_kernel(SimtParams
         // (not for the policies with 64-bit accumulators -- general int64, general float64
         // (min,+): their 255-register one-CTA builds pay 3% in the main loop for the extra
         // epilogue code, and their tiles are ~10x longer, profiles/r02z_sweep_xs_general.jsonl)
-        if constexpr (sizeof(Acc) < 8) if (mode == WB_STORE || mode == WB_FOLD) {
+        if constexpr (sizeof(Acc) < 8 && !NoVecEpi<Pol>::value) if (mode == WB_STORE || mode == WB_FOLD) {
             T* dst = reinterpret_cast<T*>(p.w.C);
             long long ld = p.w.ldc;
             if (mode == WB_STORE && p.w.mode_base == 1 && s > 0) {   // co3: slice s>0 -> workspace D_s

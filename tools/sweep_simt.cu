@@ -39,6 +39,8 @@ struct PolI8Dp4aBK32 : PolI8Dp4a { static constexpr int BK = 32; };
 template <> struct starmm::Finish<PolI8Dp4aBK128, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 template <> struct starmm::Finish<PolI8Dp4aBK32, SrInt64> : starmm::Finish<PolI8Dp4a, SrInt64> {};
 
+struct PolI32VminNV : PolI32Vmin { static constexpr bool NO_VEC_EPI = true; };
+template <> struct starmm::Finish<PolI32VminNV, SrTropI32> : starmm::Finish<PolI32Vmin, SrTropI32> {};
 // cross-stage fragment ring on the one-CTA-per-SM general policies
 struct PolF64MinXS : PolF64Min { static constexpr bool XSTAGE = true; };
 struct PolI64XS : PolI64 { static constexpr bool XSTAGE = true; };
@@ -56,6 +58,31 @@ int main(int argc, char** argv) {
     cudaMemset(A, 0, bytes); cudaMemset(B, 0, bytes); cudaMemset(C, 0, bytes);
     // (round 2: k-group unroll 2/4/8 and BK 128/256 at a 16-group unroll were swept on the
     //  stage-local fragment loop -- profiles/r02y_sweep_unroll_*.jsonl -- full unroll won)
+    if (argc > 2 && argv[2][0] == 'a') {   // every production policy build (A/B against another revision)
+        for (int rep = 0; rep < 2; ++rep) {
+            run<PolI64Narrow, SrInt64, 2, false>("narrow_occ2", n, A, B, C, cnt, sms);
+            run<PolI32Vmin, SrTropI32, 2, false>("i32vmin_occ2", n, A, B, C, cnt, sms);
+            run<PolF32Pair, SrTropF32, 1, false>("f32pair_f32_occ1", n, A, B, C, cnt, sms);
+            run<PolF32Pair, SrTropF32, 2, false>("f32pair_f32_occ2", n, A, B, C, cnt, sms);
+            run<PolF32Pair, SrTropI32, 1, false>("f32pair_i32_occ1", n, A, B, C, cnt, sms);
+            run<PolF32Pair, SrTropI32, 2, false>("f32pair_i32_occ2", n, A, B, C, cnt, sms);
+            run<PolI32Sat, SrTropI32, 1, false>("i32sat_occ1", n, A, B, C, cnt, sms);
+            run<PolS16x2Min, SrTropF32, 1, false>("s16x2_occ1", n, A, B, C, cnt, sms);
+            run<PolS16x2Min, SrTropF32, 2, false>("s16x2_occ2", n, A, B, C, cnt, sms);
+            run<PolI8Dp4a, SrInt64, 1, false>("dp4a_occ1", n, A, B, C, cnt, sms);
+            run<PolI8Dp4a, SrInt64, 2, false>("dp4a_occ2", n, A, B, C, cnt, sms);
+            run<PolF64Min, SrTropF64, 1, false>("f64min_occ1", n, A, B, C, cnt, sms);
+            run<PolI64, SrInt64, 1, false>("i64_occ1", n, A, B, C, cnt, sms);
+        }
+        return 0;
+    }
+    if (argc > 2 && argv[2][0] == 'v') {
+        for (int rep = 0; rep < 2; ++rep) {
+            run<PolI32Vmin, SrTropI32, 2, false>("i32vmin_occ2", n, A, B, C, cnt, sms);
+            run<PolI32VminNV, SrTropI32, 2, false>("i32vmin_novec_occ2", n, A, B, C, cnt, sms);
+        }
+        return 0;
+    }
     if (argc > 2 && argv[2][0] == 'x') {   // cross-stage ring on the general one-CTA policies
         for (int rep = 0; rep < 2; ++rep) {
             run<PolF64Min, SrTropF64, 1, false>("f64min_occ1", n, A, B, C, cnt, sms);
