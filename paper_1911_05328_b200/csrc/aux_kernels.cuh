@@ -142,7 +142,7 @@ __global__ void pack_a_s8x4_kernel(const long long* A, long long rows, long long
 // B (kdim x cols) -> P[kp/4][colsp].  2-D grid (x: column pairs, y: k-words), no 64-bit
 // division per element (the grid-stride form spent 3x pack_a's time on it); two columns
 // per thread with 16-byte loads when the rows allow it.
-__global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
+__global__ void __launch_bounds__(256, 8) pack_b_s8x4_kernel(const long long* B, long long kdim, long long cols, long long ldb,
                                    int* P, long long colsp, long long kp, unsigned long long* range) {
     RangeAcc acc;
     const bool vec = ((reinterpret_cast<uintptr_t>(B) | (uintptr_t)(ldb * 8)) & 15) == 0;
@@ -174,7 +174,7 @@ __global__ void pack_b_s8x4_kernel(const long long* B, long long kdim, long long
 }
 // (min,+) B (kdim x cols) -> P[kp][colsp/2] words (enc(B[k][2w]), enc(B[k][2w+1]))
 template <class T>
-__global__ void pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, long long ldb,
+__global__ void __launch_bounds__(256, 8) pack_b_s16x2_kernel(const T* B, long long kdim, long long cols, long long ldb,
                                     unsigned* P, long long colsp, long long kp, unsigned long long* range) {
     RangeAcc acc;
     const long long wpr = colsp / 2;
@@ -236,7 +236,7 @@ inline dim3 pack_a_grid(long long rowsp, long long kp) {
 
 // B (kdim x cols, ld) -> P[kp/G][colsp][G]
 template <class Tin, class Tp, int G, class Conv>
-__global__ void pack_b_kernel(const Tin* B, long long kdim, long long cols, long long ldb,
+__global__ void __launch_bounds__(256, 8) pack_b_kernel(const Tin* B, long long kdim, long long cols, long long ldb,
                               Tp* P, long long colsp, long long kp, Tp pad,
                               unsigned long long* range = nullptr, Pred pr = Pred()) {
     if (pr.off()) return;
@@ -304,7 +304,8 @@ __global__ void madd_kernel(typename Sr::T* C, long long ldc, const typename Sr:
         }
 }
 
-// launch shape for the 2-D elementwise kernels (x: 256-column blocks, y: rows, both
+// launch shape for the 2-D elementwise kernels (256 threads, __launch_bounds__(256, 8) on
+// the packers so that 8 CTAs per SM really are resident; x: 256-column blocks, y: rows, both
 // grid-strided): at most one resident wave of CTAs (8 x 256 threads per SM), and the
 // row dimension cut so that every CTA runs the same number of grid-stride iterations
 // (1024 rows over 296 CTA-rows ran 3.46 -> 4 iterations on the slowest CTA: the int8
