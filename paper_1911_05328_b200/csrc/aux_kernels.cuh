@@ -191,7 +191,9 @@ __global__ void __launch_bounds__(256, 8) pack_b_s16x2_kernel(const T* B, long l
 }
 
 // A (rows x kdim, ld) -> P[kp/G][rowsp][G], transposing through a 32x32 smem tile
-// so that both the global reads and the packed writes are coalesced.
+// so that both the global reads and the packed writes are coalesced.  (A 32 x 128 tile
+// with 16 loads per thread before the barrier was slower -- 304 vs 211 us on config 3's
+// A panel: fewer resident CTAs, longer bulk-synchronous phases.)
 template <class Tin, class Tp, int G, class Conv>
 __global__ void pack_a_kernel(const Tin* A, long long rows, long long kdim, long long lda,
                               Tp* P, long long rowsp, long long kp, Tp pad,

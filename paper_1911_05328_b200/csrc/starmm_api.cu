@@ -1111,7 +1111,8 @@ int pack_operands(Exec& x, const Geom& G, const void* A, long long lda, const vo
 
 template <class Sr>
 int launch_ordered(const OrderedParams& op, long long tiles_m, long long tiles_n, cudaStream_t s) {
-    minplus_ordered_kernel<Sr><<<dim3((unsigned)tiles_n, (unsigned)tiles_m), ordered::THREADS, 0, s>>>(op);
+    const long long grid = std::max<long long>(1, std::min<long long>(tiles_m * tiles_n, 148LL * 6));
+    minplus_ordered_kernel<Sr><<<(unsigned)grid, ordered::THREADS, 0, s>>>(op);
     CK(cudaGetLastError());
     return STARMM_OK;
 }
