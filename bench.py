@@ -104,7 +104,8 @@ INT8_PASSES = {"tcgen05_i8_umma": 1, "ozaki2_fp64_tcgen05_i8x16": 16, "tcgen05_i
 
 # ---- clocks during the timed region ----------------------------------------
 class ClockSampler:
-    def __init__(self, device_index: int, period=0.2):
+    def __init__(self, device_index: int, period=0.01):
+        # 10 ms: config 2's whole timed region is ~12 ms (a 200 ms period gave it 1 sample)
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
         self._dev = device_index
