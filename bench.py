@@ -104,8 +104,7 @@ INT8_PASSES = {"tcgen05_i8_umma": 1, "ozaki2_fp64_tcgen05_i8x16": 16, "tcgen05_i
 
 # ---- clocks during the timed region ----------------------------------------
 class ClockSampler:
-    def __init__(self, device_index: int, period=0.01):
-        # 10 ms: config 2's whole timed region is ~12 ms (a 200 ms period gave it 1 sample)
+    def __init__(self, device_index: int, period=0.2):
         self.samples, self.reasons, self.max_mhz = [], set(), None
         self._stop = threading.Event()
         self._dev = device_index
@@ -431,15 +430,22 @@ def main():
     def step():
         dmm.step(C, A, B)
 
+    import time as _time
+    torch.cuda.synchronize()
+    _w0 = _time.perf_counter()
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    warm_s = (_time.perf_counter() - _w0) / max(1, args.warmup)
+    # NVML sampling period: ~20 samples over the timed region, between 5 and 200 ms (polling
+    # at 100 Hz cost config 4 0.25%; a fixed 200 ms gave config 2's 12-24 ms region 1 sample)
+    clk_period = min(0.2, max(0.005, warm_s * args.steps / 20.0))
     dmm.plan.reset_stats()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local_rank) as clk:
+    with ClockSampler(local_rank, clk_period) as clk:
         e0.record()
         for _ in range(args.steps):
             step()
