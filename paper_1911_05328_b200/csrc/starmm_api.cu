@@ -1086,17 +1086,17 @@ int pack_operands(Exec& x, const Geom& G, const void* A, long long lda, const vo
         if (G.path == PATH_SIMT_F64T_S16X2) {
             pack_a_kernel<double, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                 (const double*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-            pack_b_s16x2_kernel<double><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+            pack_b_s16x2_kernel<double><<<grid2d((Kp + 3) / 4, Np / 2), 256, 0, s>>>(
                 (const double*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
         } else if (G.path == PATH_SIMT_F32_S16X2) {
             pack_a_kernel<float, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                 (const float*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-            pack_b_s16x2_kernel<float><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+            pack_b_s16x2_kernel<float><<<grid2d((Kp + 3) / 4, Np / 2), 256, 0, s>>>(
                 (const float*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
         } else {
             pack_a_kernel<int, unsigned, 1, ConvS16Dup><<<ga, dim3(32, 8), 0, s>>>(
                 (const int*)A, P->m, P->k, lda, (unsigned*)pa, Mp, Kp, s16pad, rng);
-            pack_b_s16x2_kernel<int><<<grid2d(Kp, Np / 2), 256, 0, s>>>(
+            pack_b_s16x2_kernel<int><<<grid2d((Kp + 3) / 4, Np / 2), 256, 0, s>>>(
                 (const int*)B, P->k, P->n, ldb, (unsigned*)pb, Np, Kp, rng);
         }
         rc = cuda_status(cudaGetLastError());
